@@ -1,0 +1,233 @@
+"""Pins for oracle.model: the fp64 layer is checked against things other than itself
+(the paper's printed parameter counts, torch.autograd fp64 with torch's own LayerNorm /
+SDPA / GELU, central finite differences, closed-form special cases and invariants)."""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from oracle import model as om
+from oracle import schedule as osch
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rng(seed=0):
+    return np.random.default_rng(seed)
+
+
+def _params(d, L, rng, scale=0.2):
+    pl = om.layer_param_count(d)
+    out = []
+    for _ in range(L):
+        p = rng.standard_normal(pl) * scale
+        v = om.unpack(p, d)
+        v["ln1_w"][:] = 1 + 0.1 * rng.standard_normal(d)
+        v["ln2_w"][:] = 1 + 0.1 * rng.standard_normal(d)
+        out.append(p)
+    return out
+
+
+# ------------------------------------------------------------------ P7: parameter counts
+
+def test_param_count_matches_paper_table():
+    rows = [l.split() for l in open(os.path.join(GOLDEN, "x_model_table.txt")) if l.strip() and not l.startswith("#")]
+    assert len(rows) == 9
+    for name, p_printed, unit, dm, dl in rows:
+        p = om.param_count(int(dm), int(dl))
+        printed = float(p_printed) * float(unit)
+        digits = len(p_printed.replace(".", "").lstrip("0"))
+        # X_[x] rows are the formula printed to 3 significant digits (X_2 exactly); the real models
+        # (BERT, Megatron-LM, T-NLG, GPT-3) carry their published counts, which the formula matches
+        # to within 1%
+        tol = 0.01 if not name.startswith("X_") else 0.5 * 10 ** (math.floor(math.log10(printed)) - digits + 1) / printed
+        assert abs(p - printed) / printed <= tol + 1e-12, (name, p, printed)
+    assert om.param_count(4, 2) == 488                    # X_2 exact
+    assert om.layer_param_count(64) == 49_984             # config C1
+
+
+def test_x_family_closed_form():
+    # p = 12 x^5 + 13 x^3 with d_m = x^2, d_l = x
+    for x in (2, 4, 8, 32, 64, 160):
+        assert om.param_count(x * x, x) == 12 * x ** 5 + 13 * x ** 3
+
+
+def test_layout_is_contiguous_and_complete():
+    d = 8
+    offs = om.layer_offsets(d)
+    names = list(offs)
+    assert names == ["ln1_w", "ln1_b", "Wqkv", "bqkv", "Wo", "bo", "ln2_w", "ln2_b", "W1", "b1", "W2", "b2"]
+    end = 0
+    for n in names:
+        o, s = offs[n]
+        assert o == end
+        end = o + int(np.prod(s))
+    assert end == 12 * d * d + 13 * d
+
+
+def test_synth_layout_agrees_with_oracle_layout():
+    import synth
+    for d in (4, 64, 768):
+        spec, pl = synth.layout(d)
+        offs = om.layer_offsets(d)
+        assert pl == om.layer_param_count(d)
+        for name, off, shape in spec:
+            assert offs[name] == (off, shape)
+
+
+# ------------------------------------------------------------------ P1: torch.autograd fp64
+
+def _torch_layer(x, flat, d, heads, causal, eps=om.LN_EPS):
+    p = {k: torch.from_numpy(v.copy()).requires_grad_(True) for k, v in om.unpack(flat, d).items()}
+    xt = torch.from_numpy(x.copy()).requires_grad_(True)
+    b, s, _ = x.shape
+    a = F.layer_norm(xt, (d,), p["ln1_w"], p["ln1_b"], eps)
+    qkv = a @ p["Wqkv"] + p["bqkv"]
+    q, k, v = qkv.split(d, dim=-1)
+    sh = lambda t: t.reshape(b, s, heads, d // heads).transpose(1, 2)
+    o = F.scaled_dot_product_attention(sh(q), sh(k), sh(v), is_causal=causal)
+    o = o.transpose(1, 2).reshape(b, s, d)
+    h1 = xt + o @ p["Wo"] + p["bo"]
+    c = F.layer_norm(h1, (d,), p["ln2_w"], p["ln2_b"], eps)
+    u = c @ p["W1"] + p["b1"]
+    y = h1 + F.gelu(u, approximate="none") @ p["W2"] + p["b2"]
+    return xt, p, y
+
+
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("d,heads,s,b", [(16, 2, 7, 2), (32, 4, 12, 1)])
+def test_layer_matches_torch_autograd_fp64(causal, d, heads, s, b):
+    rng = _rng(1)
+    flat = _params(d, 1, rng)[0]
+    x = rng.standard_normal((b, s, d))
+    dy = rng.standard_normal((b, s, d))
+    cfg = om.LayerCfg(d=d, heads=heads, causal=causal)
+    y, cache = om.layer_forward(x, flat, cfg)
+    dx, g = om.layer_backward(dy, cache, flat, cfg)
+
+    xt, p, yt = _torch_layer(x, flat, d, heads, causal)
+    yt.backward(torch.from_numpy(dy))
+    np.testing.assert_allclose(y, yt.detach().numpy(), rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(dx, xt.grad.numpy(), rtol=1e-10, atol=1e-12)
+    gv = om.unpack(g, d)
+    for k in gv:
+        ref = p[k].grad.numpy()
+        err = np.linalg.norm(gv[k] - ref) / max(np.linalg.norm(ref), 1e-30)
+        if k == "bqkv":  # the key-bias block is exactly 0 (pin P4); compare it absolutely
+            assert np.max(np.abs(gv[k] - ref)) < 1e-12
+        else:
+            assert err < 1e-10, (k, err)
+
+
+# ------------------------------------------------------------------ P2: finite differences
+
+def test_step_gradient_matches_central_differences():
+    """Brute force on tiny inputs: every parameter of the whole 2-layer, 2x2-micro-batch step."""
+    rng = _rng(2)
+    d, heads, s, b, L, D, N = 8, 2, 5, 2, 2, 2, 2
+    cfg = om.LayerCfg(d=d, heads=heads, causal=True)
+    params = _params(d, L, rng, scale=0.3)
+    X = rng.standard_normal((D, N, b, s, d))
+    T = rng.standard_normal((D, N, b, s, d))
+    _, grads = osch.grads_standard(params, X, T, cfg)
+    h = 1e-6
+    for l in range(L):
+        fd = np.zeros_like(params[l])
+        for i in range(params[l].size):
+            pp = [q.copy() for q in params]
+            pp[l][i] += h
+            lp = osch.loss(pp, X, T, cfg)
+            pp[l][i] -= 2 * h
+            lm = osch.loss(pp, X, T, cfg)
+            fd[i] = (lp - lm) / (2 * h)
+        err = np.linalg.norm(grads[l] - fd) / np.linalg.norm(fd)
+        assert err < 1e-7, (l, err)
+
+
+# ------------------------------------------------------------------ P3 / P4: special cases
+
+def test_single_position_reduces_to_value_path():
+    """s = 1: softmax over one key is 1, so o = v and the layer is
+    x + (LN1(x) W_V + b_V) W_o + b_o followed by the FFN block; dW_Q, dW_K, db_Q, db_K are exactly 0."""
+    rng = _rng(3)
+    d, heads = 16, 4
+    flat = _params(d, 1, rng)[0]
+    p = om.unpack(flat, d)
+    x = rng.standard_normal((3, 1, d))
+    cfg = om.LayerCfg(d=d, heads=heads)
+    y, cache = om.layer_forward(x, flat, cfg)
+    # closed form, written independently of layer_forward
+    mu = x.mean(-1, keepdims=True)
+    a = (x - mu) / np.sqrt(x.var(-1, keepdims=True) + om.LN_EPS) * p["ln1_w"] + p["ln1_b"]
+    v = a @ p["Wqkv"][:, 2 * d:] + p["bqkv"][2 * d:]
+    h1 = x + v @ p["Wo"] + p["bo"]
+    mu2 = h1.mean(-1, keepdims=True)
+    c = (h1 - mu2) / np.sqrt(h1.var(-1, keepdims=True) + om.LN_EPS) * p["ln2_w"] + p["ln2_b"]
+    u = c @ p["W1"] + p["b1"]
+    from scipy.special import erf
+    yref = h1 + (u * 0.5 * (1 + erf(u / np.sqrt(2)))) @ p["W2"] + p["b2"]
+    np.testing.assert_allclose(y, yref, rtol=1e-12, atol=1e-13)
+    _, g = om.layer_backward(rng.standard_normal(x.shape), cache, flat, cfg)
+    gv = om.unpack(g, d)
+    assert np.all(gv["Wqkv"][:, :2 * d] == 0.0)
+    assert np.all(gv["bqkv"][:2 * d] == 0.0)
+    assert np.any(gv["Wqkv"][:, 2 * d:] != 0.0)
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_key_bias_gradient_vanishes(causal):
+    """Adding a constant to every key of a head shifts each score row by q.b_K, which softmax
+    ignores (also under the causal mask), so dL/db_K = 0; dL/db_Q is not."""
+    rng = _rng(4)
+    d, heads = 16, 2
+    flat = _params(d, 1, rng)[0]
+    x = rng.standard_normal((2, 9, d))
+    cfg = om.LayerCfg(d=d, heads=heads, causal=causal)
+    _, cache = om.layer_forward(x, flat, cfg)
+    _, g = om.layer_backward(rng.standard_normal(x.shape), cache, flat, cfg)
+    b = om.unpack(g, d)["bqkv"]
+    assert np.max(np.abs(b[d:2 * d])) < 1e-13 * np.max(np.abs(b[:d]))
+    assert np.max(np.abs(b[:d])) > 1e-6
+
+
+def test_causal_invariant_future_does_not_leak():
+    rng = _rng(5)
+    d, heads, s = 16, 2, 8
+    flat = _params(d, 1, rng)[0]
+    x = rng.standard_normal((1, s, d))
+    cfg = om.LayerCfg(d=d, heads=heads, causal=True)
+    y, _ = om.layer_forward(x, flat, cfg)
+    x2 = x.copy()
+    x2[0, 5:] = rng.standard_normal((s - 5, d))
+    y2, _ = om.layer_forward(x2, flat, cfg)
+    np.testing.assert_array_equal(y[0, :5], y2[0, :5])
+    assert not np.allclose(y[0, 5:], y2[0, 5:])
+
+
+def test_pieces_against_textbook_definitions():
+    rng = _rng(6)
+    u = rng.standard_normal(1000) * 3
+    np.testing.assert_allclose(om.gelu(u), F.gelu(torch.from_numpy(u), approximate="none").numpy(), rtol=1e-14, atol=1e-15)
+    assert om.gelu(np.array([0.0]))[0] == 0.0 and om.gelu_grad(np.array([0.0]))[0] == 0.5
+    h = 1e-6
+    np.testing.assert_allclose(om.gelu_grad(u), (om.gelu(u + h) - om.gelu(u - h)) / (2 * h), rtol=1e-8, atol=1e-9)
+    x = rng.standard_normal((4, 33)) * 5 + 2
+    y, (xhat, rstd) = om.layernorm_fwd(x, np.ones(33), np.zeros(33), 0.0)
+    np.testing.assert_allclose(y.mean(-1), 0, atol=1e-14)
+    np.testing.assert_allclose(y.var(-1), 1, rtol=1e-12)
+    q = rng.standard_normal((1, 1, 6, 4)); k = rng.standard_normal((1, 1, 6, 4)); v = rng.standard_normal((1, 1, 6, 4))
+    o, P = om.attention_fwd(q, k, v, True)
+    np.testing.assert_allclose(P.sum(-1), 1, rtol=1e-14)
+    assert np.all(np.triu(P[0, 0], 1) == 0)
+    np.testing.assert_allclose(o[0, 0, 0], v[0, 0, 0], rtol=1e-14)   # first query sees only key 0
+
+
+def test_mse_loss_closed_form():
+    y = np.array([[[1.0, 2.0], [3.0, 4.0]]])
+    T = np.zeros_like(y)
+    l, dy = om.mse_loss(y, T)
+    assert l == 0.5 * (1 + 4 + 9 + 16) / 4
+    np.testing.assert_array_equal(dy, y / 4)
