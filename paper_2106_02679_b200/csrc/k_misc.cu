@@ -1,0 +1,376 @@
+// k_misc.cu -- HBM-bound kernels of the LGA step: LayerNorm fwd/bwd, column sums for the
+// bias / LayerNorm gradients, MSE loss + seed gradient, sharded AdamW, casts, seeded init,
+// pipeline flags.  Every reduction runs in a fixed order (no float atomics), so a step is
+// bitwise reproducible.
+#include "kernels.cuh"
+
+#include <cmath>
+
+namespace lga {
+
+// =============================================================== LayerNorm forward
+// Block per row; VPT values per thread stay in registers (exact two-pass mean / variance).
+template <int VPT>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x, const void* gamma,
+                                                     const void* beta, DT pdt, void* y, DT ydt,
+                                                     float2* __restrict__ stats, int d, float eps) {
+  __shared__ float red[64];
+  const int64_t row = blockIdx.x;
+  const float* xr = x + row * d;
+  float v[VPT];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    v[i] = c < d ? xr[c] : 0.f;
+    s += v[i];
+  }
+  const float mean = block_sum2(s, 0.f, red).x / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    const float t = c < d ? v[i] - mean : 0.f;
+    q += t * t;
+  }
+  const float var = block_sum2(q, 0.f, red).x / d;
+  const float rstd = rsqrtf(var + eps);
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    if (c < d) {
+      const float yv = (v[i] - mean) * rstd * ld_elem(gamma, c, pdt) + ld_elem(beta, c, pdt);
+      st_elem(y, row * d + c, ydt, yv);
+    }
+  }
+  if (threadIdx.x == 0) stats[row] = make_float2(mean, rstd);
+}
+
+void ln_fwd(const float* x, const void* gamma, const void* beta, DT pdt, void* y, DT ydt,
+            float2* stats, int rows, int d, float eps, cudaStream_t st) {
+  if (rows <= 0) return;
+  const int bd = d >= 1024 ? 256 : (d >= 256 ? 128 : 64);
+  const int vpt = (d + bd - 1) / bd;
+#define LNF(V) ln_fwd_kernel<V><<<rows, bd, 0, st>>>(x, gamma, beta, pdt, y, ydt, stats, d, eps)
+  if (vpt <= 1) LNF(1); else if (vpt <= 2) LNF(2); else if (vpt <= 4) LNF(4);
+  else if (vpt <= 8) LNF(8); else if (vpt <= 16) LNF(16); else LNF(32);
+#undef LNF
+}
+
+// =============================================================== LayerNorm backward
+// Block handles rows [blk*R, blk*R+R); per row two block reductions; the column partials of
+// dgamma / dbeta accumulate in registers across the block's rows (fixed order).
+constexpr int LN_BWD_ROWS = 32;
+
+int ln_bwd_blocks(int rows) { return (rows + LN_BWD_ROWS - 1) / LN_BWD_ROWS; }
+
+template <int VPT>
+__global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ dout, const float* __restrict__ x,
+                                                     const float2* __restrict__ stats, const void* gamma, DT pdt,
+                                                     const float* __restrict__ resid, float* dx, void* dx_e, DT edt,
+                                                     float* __restrict__ partial, int rows, int d) {
+  __shared__ float red[64];
+  float g[VPT], dg[VPT], db[VPT];
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    g[i] = c < d ? ld_elem(gamma, c, pdt) : 0.f;
+    dg[i] = 0.f; db[i] = 0.f;
+  }
+  const int r0 = blockIdx.x * LN_BWD_ROWS;
+  const int r1 = min(rows, r0 + LN_BWD_ROWS);
+  for (int r = r0; r < r1; ++r) {
+    const float2 sr = stats[r];
+    const int64_t base = (int64_t)r * d;
+    float xh[VPT], dxh[VPT];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int c = threadIdx.x + i * blockDim.x;
+      if (c < d) {
+        const float go = dout[base + c];
+        xh[i] = (x[base + c] - sr.x) * sr.y;
+        dxh[i] = go * g[i];
+        dg[i] += go * xh[i];
+        db[i] += go;
+      } else {
+        xh[i] = 0.f; dxh[i] = 0.f;
+      }
+      s1 += dxh[i];
+      s2 += dxh[i] * xh[i];
+    }
+    const float2 s = block_sum2(s1, s2, red);
+    const float m1 = s.x / d, m2 = s.y / d;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int c = threadIdx.x + i * blockDim.x;
+      if (c < d) {
+        float v = sr.y * (dxh[i] - m1 - xh[i] * m2);
+        if (resid) v += resid[base + c];
+        dx[base + c] = v;
+        if (dx_e) st_elem(dx_e, base + c, edt, v);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    if (c < d) {
+      partial[(int64_t)blockIdx.x * 2 * d + c] = dg[i];
+      partial[(int64_t)blockIdx.x * 2 * d + d + c] = db[i];
+    }
+  }
+}
+
+int ln_bwd(const float* dout, const float* x, const float2* stats, const void* gamma, DT pdt,
+           const float* resid, float* dx, void* dx_e, DT edt, float* partial, int rows, int d,
+           cudaStream_t st) {
+  const int nblk = ln_bwd_blocks(rows);
+  if (rows <= 0) return 0;
+  const int bd = d >= 1024 ? 256 : (d >= 256 ? 128 : 64);
+  const int vpt = (d + bd - 1) / bd;
+#define LNB(V) ln_bwd_kernel<V><<<nblk, bd, 0, st>>>(dout, x, stats, gamma, pdt, resid, dx, dx_e, edt, partial, rows, d)
+  if (vpt <= 1) LNB(1); else if (vpt <= 2) LNB(2); else if (vpt <= 4) LNB(4);
+  else if (vpt <= 8) LNB(8); else if (vpt <= 16) LNB(16); else LNB(32);
+#undef LNB
+  return nblk;
+}
+
+// =============================================================== column sums
+constexpr int COLSUM_ROWS = 64;
+int colsum_blocks(int rows) { return (rows + COLSUM_ROWS - 1) / COLSUM_ROWS; }
+
+__global__ void colsum_partial_kernel(const void* __restrict__ X, DT xdt, int64_t ldx, int rows, int n,
+                                      float* __restrict__ partial) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int r0 = blockIdx.y * COLSUM_ROWS, r1 = min(rows, r0 + COLSUM_ROWS);
+  float s = 0.f;
+  for (int r = r0; r < r1; ++r) s += ld_elem(X, (int64_t)r * ldx + c, xdt);
+  partial[(int64_t)blockIdx.y * n + c] = s;
+}
+
+int colsum_partial(const void* X, DT xdt, int64_t ldx, int rows, int n, float* partial, cudaStream_t st) {
+  const int nblk = colsum_blocks(rows);
+  if (rows <= 0 || n <= 0) return 0;
+  dim3 grid((n + 255) / 256, nblk);
+  colsum_partial_kernel<<<grid, 256, 0, st>>>(X, xdt, ldx, rows, n, partial);
+  return nblk;
+}
+
+__global__ void colsum_finish_kernel(const float* __restrict__ partial, int nblk, int64_t pstride, int n,
+                                     const float* acc_in, void* out, DT out_dt) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  float s = 0.f;
+  for (int k = 0; k < nblk; ++k) s += partial[(int64_t)k * pstride + c];
+  if (acc_in) s += acc_in[c];
+  st_elem(out, c, out_dt, s);
+}
+
+void colsum_finish(const float* partial, int nblk, int64_t pstride, int n, const float* acc_in,
+                   void* out, DT out_dt, cudaStream_t st) {
+  if (n <= 0) return;
+  colsum_finish_kernel<<<(n + 255) / 256, 256, 0, st>>>(partial, nblk, pstride, n, acc_in, out, out_dt);
+}
+
+// =============================================================== MSE loss + seed gradient
+constexpr int MSE_THREADS = 256;
+constexpr int MSE_PER_THREAD = 16;
+int mse_blocks(int64_t n) { return (int)((n + MSE_THREADS * MSE_PER_THREAD - 1) / (MSE_THREADS * MSE_PER_THREAD)); }
+
+__global__ void __launch_bounds__(MSE_THREADS) mse_kernel(const float* __restrict__ y, const float* __restrict__ T,
+                                                          float* __restrict__ dY, double* __restrict__ partial,
+                                                          int64_t n, float inv_numel) {
+  __shared__ double red[32];
+  const int64_t base = (int64_t)blockIdx.x * MSE_THREADS * MSE_PER_THREAD + threadIdx.x;
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < MSE_PER_THREAD; ++i) {
+    const int64_t k = base + (int64_t)i * MSE_THREADS;
+    if (k < n) {
+      const float diff = y[k] - T[k];
+      dY[k] = diff * inv_numel;
+      s += (double)diff * (double)diff;
+    }
+  }
+  s = warp_sum_d(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < MSE_THREADS / 32; ++w) t += red[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
+void mse_fwd_bwd(const float* y, const float* T, float* dY, double* partial, int64_t n,
+                 float inv_numel_mb, cudaStream_t st) {
+  if (n <= 0) return;
+  mse_kernel<<<mse_blocks(n), MSE_THREADS, 0, st>>>(y, T, dY, partial, n, inv_numel_mb);
+}
+
+__global__ void mse_finish_kernel(const double* partial, int nblk, double scale, double* out) {
+  double s = 0.0;
+  for (int k = threadIdx.x; k < nblk; k += 32) s += partial[k];
+  s = warp_sum_d(s);
+  if (threadIdx.x == 0) out[0] = s * scale;
+}
+
+void mse_finish(const double* partial, int nblk, double scale, double* out, cudaStream_t st) {
+  mse_finish_kernel<<<1, 32, 0, st>>>(partial, nblk, scale, out);
+}
+
+// =============================================================== AdamW
+template <typename GE, typename PE>
+__global__ void adamw_kernel(const GE* __restrict__ gin, float gscale, float* __restrict__ master,
+                             float* __restrict__ m, float* __restrict__ v, PE* __restrict__ pout,
+                             float* __restrict__ keep, int64_t n, float lr, float b1, float b2, float eps,
+                             float wd, float bc1, float bc2) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float g = to_f(gin[i]) * gscale;
+    float th = master[i];
+    th = th * (1.0f - lr * wd);
+    const float mi = b1 * m[i] + (1.0f - b1) * g;
+    const float vi = b2 * v[i] + (1.0f - b2) * g * g;
+    m[i] = mi;
+    v[i] = vi;
+    const float mhat = mi / bc1;
+    const float vhat = vi / bc2;
+    th = th - lr * mhat / (sqrtf(vhat) + eps);
+    master[i] = th;
+    pout[i] = from_f<PE>(th);
+    if (keep) keep[i] = g;
+  }
+}
+
+void adamw(const void* gin, DT gdt, float gscale, float* master, float* m, float* v,
+           void* param_out, DT pdt, float* keep, int64_t n, float lr, float beta1, float beta2,
+           float eps, float wd, float bc1, float bc2, cudaStream_t st) {
+  if (n <= 0) return;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+#define AD(GE, PE) adamw_kernel<GE, PE><<<grid, 256, 0, st>>>((const GE*)gin, gscale, master, m, v, (PE*)param_out, keep, n, lr, beta1, beta2, eps, wd, bc1, bc2)
+  if (gdt == DT::F32 && pdt == DT::F32) AD(float, float);
+  else if (gdt == DT::F32) AD(float, __nv_bfloat16);
+  else if (pdt == DT::F32) AD(__nv_bfloat16, float);
+  else AD(__nv_bfloat16, __nv_bfloat16);
+#undef AD
+}
+
+__global__ void shard_acc_kernel(const void* g, DT gdt, float* acc, int64_t n, bool first) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc[i] = (first ? 0.f : acc[i]) + ld_elem(g, i, gdt);
+}
+void shard_accumulate(const void* g, DT gdt, float* acc, int64_t n, bool first, cudaStream_t st) {
+  if (n <= 0) return;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  shard_acc_kernel<<<grid, 256, 0, st>>>(g, gdt, acc, n, first);
+}
+
+// =============================================================== casts / fills
+__global__ void cast_kernel(const float* __restrict__ x, void* y, DT ydt, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    st_elem(y, i, ydt, x[i]);
+}
+void cast_f32(const float* x, void* y, DT ydt, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  cast_kernel<<<grid, 256, 0, st>>>(x, y, ydt, n);
+}
+__global__ void to_f32_kernel(const void* x, DT xdt, float* y, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = ld_elem(x, i, xdt);
+}
+void copy_to_f32(const void* x, DT xdt, float* y, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  to_f32_kernel<<<grid, 256, 0, st>>>(x, xdt, y, n);
+}
+__global__ void fill_kernel(float* p, float v, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+void fill_f32(float* p, float v, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  fill_kernel<<<grid, 256, 0, st>>>(p, v, n);
+}
+
+// =============================================================== seeded device init
+// splitmix64 counter hash -> two uniforms -> Box-Muller normal.  Kind by canonical offset.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void init_kernel(float* out, int64_t n, int64_t pl, int d, int f, int L_total, int64_t first_layer,
+                            uint64_t seed) {
+  // canonical offsets
+  const int64_t o_ln1w = 0, o_ln1b = d, o_wqkv = 2 * d, o_bqkv = o_wqkv + 3LL * d * d, o_wo = o_bqkv + 3 * d,
+                o_bo = o_wo + (int64_t)d * d, o_ln2w = o_bo + d, o_ln2b = o_ln2w + d, o_w1 = o_ln2b + d,
+                o_b1 = o_w1 + (int64_t)d * f, o_w2 = o_b1 + f, o_b2 = o_w2 + (int64_t)f * d;
+  const float std_w = 0.02f, std_r = 0.02f / sqrtf(2.0f * L_total);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t off = i % pl;
+    const int64_t gidx = first_layer * pl + i;
+    float val;
+    if ((off >= o_wqkv && off < o_bqkv) || (off >= o_w1 && off < o_b1) || (off >= o_wo && off < o_bo) ||
+        (off >= o_w2 && off < o_b2)) {
+      const uint64_t h = splitmix64(seed ^ splitmix64((uint64_t)gidx));
+      const float u1 = ((h >> 40) + 1.0f) * (1.0f / 16777217.0f);
+      const float u2 = ((h & 0xffffffull) + 0.5f) * (1.0f / 16777216.0f);
+      const float z = sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+      const bool resid = (off >= o_wo && off < o_bo) || (off >= o_w2 && off < o_b2);
+      val = z * (resid ? std_r : std_w);
+    } else if ((off >= o_ln1w && off < o_ln1b) || (off >= o_ln2w && off < o_ln2b)) {
+      val = 1.0f;
+    } else {
+      val = 0.0f;
+    }
+    out[i] = val;
+  }
+}
+
+void init_params_device(float* out, int64_t n_layers, int d, int ffn_mult, int L_total, int64_t first_layer,
+                        uint64_t seed, cudaStream_t st) {
+  const int64_t f = (int64_t)ffn_mult * d;
+  const int64_t pl = (4 + 2LL * ffn_mult) * d * d + 13LL * d;
+  const int64_t n = n_layers * pl;
+  if (n <= 0) return;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  init_kernel<<<grid, 256, 0, st>>>(out, n, pl, d, (int)f, L_total, first_layer, seed);
+}
+
+// =============================================================== pipeline flags
+__global__ void wait_flag_kernel(const volatile unsigned long long* flag, unsigned long long target) {
+  unsigned long long v;
+  while (true) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= target) break;
+    __nanosleep(200);
+  }
+}
+void wait_flag(const volatile unsigned long long* flag, unsigned long long target, cudaStream_t st) {
+  wait_flag_kernel<<<1, 1, 0, st>>>(flag, target);
+}
+__global__ void set_flag_kernel(unsigned long long* flag, unsigned long long value) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+}
+void set_flag(unsigned long long* flag, unsigned long long value, cudaStream_t st) {
+  set_flag_kernel<<<1, 1, 0, st>>>(flag, value);
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace lga

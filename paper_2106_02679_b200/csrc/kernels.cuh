@@ -1,0 +1,125 @@
+// kernels.cuh -- host-side launchers of every device kernel of the LGA step.
+//
+// One layer (reading A-1), per token row x in R^d:
+//   a = LN1(x); qkv = a Wqkv + bqkv; o = causal-softmax-attention(q, k, v); h1 = x + o Wo + bo
+//   c = LN2(h1); u = c W1 + b1; g = GELU(u); y = h1 + g W2 + b2
+// Storage element type E is fp32 (parity mode) or bf16 (the paper's 16-bit compute,
+// P:85); accumulation is always fp32.
+#pragma once
+
+#include "common.cuh"
+
+namespace lga {
+
+// ------------------------------------------------------------------ GEMM
+// C[m][n] = sum_k A(m,k) * B(n,k), then the epilogue.
+//   A(m,k) = A[m*lda + k] if a_kmajor else A[k*lda + m]
+//   B(n,k) = B[n*ldb + k] if b_kmajor else B[k*ldb + n]
+// Forward  Y = X W      : A = X (K-major), B(n,k) = W[k][n] (MN-major)
+// dgrad    dX = dY W^T  : A = dY (K-major), B(n,k) = W[n][k] (K-major)
+// wgrad    dW = X^T dY  : A(m,k) = X[k][m] (MN-major), B(n,k) = dY[k][n] (MN-major)
+enum EpiKind : int {
+  EPI_STORE = 0,      // out = acc (+bias[n]) (+res[m][n]) (+acc_in[m][n])
+  EPI_GELU_FWD = 1,   // u = acc + bias[n] -> aux (E); out = GELU(u) (E)
+  EPI_GELU_BWD = 2,   // out = acc * GELU'(aux[m][n])   (aux holds u; out may alias aux)
+};
+
+struct Epi {
+  int kind = EPI_STORE;
+  const void* bias = nullptr; DT bias_dt = DT::F32;   // per column n
+  const float* res = nullptr; int64_t ldr = 0;         // fp32 residual
+  const float* acc_in = nullptr; int64_t ldacc = 0;    // fp32 accumulator added (gradient accumulation)
+  void* aux = nullptr; int64_t ldaux = 0; DT aux_dt = DT::F32;
+  void* out = nullptr; int64_t ldo = 0; DT out_dt = DT::F32;
+};
+
+struct GemmArgs {
+  int M = 0, N = 0, K = 0;
+  const void* A = nullptr; int64_t lda = 0; bool a_kmajor = true;
+  const void* B = nullptr; int64_t ldb = 0; bool b_kmajor = true;
+  Epi epi;
+  int split_k = 1;            // tensor-core path: >1 = deterministic split over K (needs workspace)
+  float* splitk_ws = nullptr; // [split_k][M][N] fp32
+};
+
+void gemm_f32_simt(const GemmArgs& g, cudaStream_t st);       // fp32 operands, CUDA cores
+cudaError_t gemm_bf16_tc(const GemmArgs& g, cudaStream_t st); // bf16 operands, tcgen05 + TMA
+int num_sms();
+
+// ------------------------------------------------------------------ attention
+// Per (sequence, head): S = q k^T * scale (+ causal mask), P = softmax(S), o = P v
+// (O3), saving lse = log-sum-exp of each score row; backward recomputes P from lse
+// (O5): dP = dO v^T, dS = P (dP - Dsum), dq = dS k * scale, dk = dS^T q * scale, dv = P^T dO
+// with Dsum_i = rowsum(dO_i * o_i).
+struct AttnArgs {
+  int nseq = 0, seq = 0, heads = 0, dh = 0, d = 0;
+  bool causal = true;
+  float scale = 1.f;
+  const void* qkv = nullptr;  // [nseq*seq][3d]  q | k | v, head h at column h*dh of each
+  void* o = nullptr;          // [nseq*seq][d]
+  float* lse = nullptr;       // [nseq][heads][seq]
+  const void* dO = nullptr;   // [nseq*seq][d]
+  float* dsum = nullptr;      // [nseq][heads][seq]
+  void* dqkv = nullptr;       // [nseq*seq][3d]
+};
+void attn_fwd_f32(const AttnArgs& a, cudaStream_t st);
+void attn_bwd_f32(const AttnArgs& a, cudaStream_t st);
+void attn_fwd_bf16(const AttnArgs& a, cudaStream_t st);
+void attn_bwd_bf16(const AttnArgs& a, cudaStream_t st);
+
+// ------------------------------------------------------------------ LayerNorm
+// y = (x - mu) * rstd * gamma + beta, biased variance (reading A-1).  x fp32 [rows][d];
+// y in E; stats[r] = (mu, rstd).
+void ln_fwd(const float* x, const void* gamma, const void* beta, DT pdt, void* y, DT ydt,
+            float2* stats, int rows, int d, float eps, cudaStream_t st);
+// dx = rstd (dxhat - mean(dxhat) - xhat mean(dxhat xhat)) + resid, dxhat = dout * gamma (O5);
+// writes dx (fp32) and optionally dx_e (E copy), and deterministic column partials
+// partial[blk][0][:] = sum dout*xhat, partial[blk][1][:] = sum dout over the block's rows.
+// Returns the number of row blocks (partial rows).
+int ln_bwd(const float* dout, const float* x, const float2* stats, const void* gamma, DT pdt,
+           const float* resid, float* dx, void* dx_e, DT edt, float* partial, int rows, int d,
+           cudaStream_t st);
+int ln_bwd_blocks(int rows);
+
+// ------------------------------------------------------------------ column sums (bias grads)
+// partial[blk][n] = sum over the block's rows of X[r][n]   (fixed row blocks, deterministic)
+int colsum_partial(const void* X, DT xdt, int64_t ldx, int rows, int n, float* partial, cudaStream_t st);
+int colsum_blocks(int rows);
+// Gradient write modes of the layer's gradient buffers (reading A-3, DESIGN.md "Gradient
+// accumulation"): v = sum_k partial[k][n]*ssel (fixed order), then
+//   acc_in == nullptr: out[n] = v ; else out[n] = acc_in[n] + v ;  out stored as out_dt.
+void colsum_finish(const float* partial, int nblk, int64_t pstride, int n, const float* acc_in,
+                   void* out, DT out_dt, cudaStream_t st);
+
+// ------------------------------------------------------------------ loss
+// dY = (y - T) / numel_mb; sumsq partial per block (double).  n = total elements.
+void mse_fwd_bwd(const float* y, const float* T, float* dY, double* partial, int64_t n,
+                 float inv_numel_mb, cudaStream_t st);
+int mse_blocks(int64_t n);
+// out[0] = 0.5/numel_mb * sum(partial)  (sum over this rank's micro-batches of their losses)
+void mse_finish(const double* partial, int nblk, double scale, double* out, cudaStream_t st);
+
+// ------------------------------------------------------------------ AdamW (torch semantics, A-4)
+// g = gin[i] * gscale; theta = theta*(1-lr*wd); m,v update; theta -= lr*mhat/(sqrt(vhat)+eps);
+// param_out (E) = theta; keep (fp32, optional) = g.
+void adamw(const void* gin, DT gdt, float gscale, float* master, float* m, float* v,
+           void* param_out, DT pdt, float* keep, int64_t n, float lr, float beta1, float beta2,
+           float eps, float wd, float bc1, float bc2, cudaStream_t st);
+
+// STANDARD schedule: acc[i] = (first ? 0 : acc[i]) + g[i]   (per-micro-batch reduced shard)
+void shard_accumulate(const void* g, DT gdt, float* acc, int64_t n, bool first, cudaStream_t st);
+
+// ------------------------------------------------------------------ misc
+void cast_f32(const float* x, void* y, DT ydt, int64_t n, cudaStream_t st);
+void copy_to_f32(const void* x, DT xdt, float* y, int64_t n, cudaStream_t st);
+void fill_f32(float* p, float v, int64_t n, cudaStream_t st);
+// Seeded on-device init ("train" recipe): per element normal(0, std) for weights, 1 for LN
+// gains, 0 otherwise.  kind[i] is derived from the canonical layout (layer-local offset).
+void init_params_device(float* out, int64_t n_layers, int d, int ffn_mult, int L_total,
+                        int64_t first_layer, uint64_t seed, cudaStream_t st);
+// Spin until *flag >= target (system-scope acquire); used for pipeline receives.
+void wait_flag(const volatile unsigned long long* flag, unsigned long long target, cudaStream_t st);
+// *flag = value (system-scope release) after all prior work on the stream.
+void set_flag(unsigned long long* flag, unsigned long long value, cudaStream_t st);
+
+}  // namespace lga

@@ -1,0 +1,1079 @@
+// lga_host.cpp -- the C ABI (include/lga.h), the per-rank arena, the layer executor and the
+// per-layer scheduler of the layered-gradient-accumulation step.
+//
+// Schedule:
+//   s_comp  : layer compute, all micro-batches of a layer before the next layer
+//   s_comm  : all-gather of layer l+1 ("Restore(i+1)") while s_comp runs layer l; in backward,
+//             reduce-scatter + AdamW of layer l ("Reduce(i)") while s_comp runs layer l-1
+//             (mixed buffering: 2 parameter slots, 1 fp32 accumulation buffer)
+//   pipeline: layer i on stage i mod P; the FFN2 epilogue of layer i writes x_{i+1}
+//             straight into stage (i+1) mod P's checkpoint buffer over NVLink (CUDA IPC), the
+//             LN1 backward of layer i writes dX_i into stage (i-1) mod P's gradient buffer,
+//             and a system-scope flag tells the receiver.
+#include "../../include/lga.h"
+#include "kernels.cuh"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace lga {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+
+static lga_status set_err(lga_status s, const char* file, int line, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  char full[1200];
+  snprintf(full, sizeof(full), "%s:%d: %s", file, line, buf);
+  g_last_error = full;
+  return s;
+}
+#define ERR(s, ...) set_err((s), __FILE__, __LINE__, __VA_ARGS__)
+
+struct StatusError {
+  lga_status s;
+};
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      ERR(LGA_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_));                       \
+      throw StatusError{LGA_ERR_CUDA};                                                  \
+    }                                                                                   \
+  } while (0)
+#define NK(call)                                                                        \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess) {                                                            \
+      ERR(LGA_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_));                       \
+      throw StatusError{LGA_ERR_NCCL};                                                  \
+    }                                                                                   \
+  } while (0)
+#define KCHECK() CK(cudaGetLastError())
+
+// ------------------------------------------------------------------ configuration
+struct Cfg {
+  int L, d, H, dh, s, b, N, D, P, f, M, c, Lloc;
+  int64_t pl, plpad, S;
+  bool bf16, layered, causal;
+  DT E, G;      // compute storage type; reduce-scatter / gradient staging type
+  float lr, b1, b2, eps, wd, ln_eps;
+  bool retain, no_comm;
+  // canonical offsets
+  int64_t o_ln1w, o_ln1b, o_wqkv, o_bqkv, o_wo, o_bo, o_ln2w, o_ln2b, o_w1, o_b1, o_w2, o_b2;
+};
+
+static lga_status validate(const lga_config* c, int world, Cfg* out) {
+  if (!c) return ERR(LGA_ERR_INVALID_ARG, "cfg is NULL");
+  if (c->abi_version != LGA_ABI_VERSION) return ERR(LGA_ERR_INVALID_ARG, "abi_version %u != %u", c->abi_version, LGA_ABI_VERSION);
+  if (c->layers <= 0 || c->d_model <= 0 || c->heads <= 0 || c->seq_len <= 0 || c->micro_batch <= 0 || c->n_micro <= 0 ||
+      c->dp <= 0 || c->pp <= 0)
+    return ERR(LGA_ERR_INVALID_ARG, "non-positive dimension");
+  if (c->d_model % c->heads) return ERR(LGA_ERR_INVALID_ARG, "d_model %% heads != 0");
+  if (c->ffn_mult != 4) return ERR(LGA_ERR_UNSUPPORTED, "ffn_mult must be 4 (P:440)");
+  if (c->layers % c->pp) return ERR(LGA_ERR_INVALID_ARG, "layers %% pp != 0 (reading A-11)");
+  if (c->pp > 1 && c->n_micro < c->pp) return ERR(LGA_ERR_INVALID_ARG, "n_micro < pp (reading A-11)");
+  if (world != c->dp * c->pp) return ERR(LGA_ERR_INVALID_ARG, "world %d != dp*pp %d", world, c->dp * c->pp);
+  if (c->schedule != LGA_LAYERED && c->schedule != LGA_STANDARD) return ERR(LGA_ERR_INVALID_ARG, "bad schedule");
+  if (c->schedule == LGA_STANDARD && c->pp != 1) return ERR(LGA_ERR_INVALID_ARG, "STANDARD requires pp == 1");
+  if (c->precision != LGA_FP32 && c->precision != LGA_BF16) return ERR(LGA_ERR_INVALID_ARG, "bad precision");
+  const int dh = c->d_model / c->heads;
+  if (c->precision == LGA_BF16 && (c->d_model % 64 || (dh != 64 && dh != 128)))
+    return ERR(LGA_ERR_UNSUPPORTED, "bf16 needs d %% 64 == 0 and head size 64 or 128 (got d=%d dh=%d)", c->d_model, dh);
+  if (c->precision == LGA_FP32 && dh > 128) return ERR(LGA_ERR_UNSUPPORTED, "head size > 128");
+  const int cmax = c->pp > 1 ? c->n_micro / c->pp : c->n_micro;
+  if (c->chunk < 0 || c->chunk > cmax) return ERR(LGA_ERR_INVALID_ARG, "chunk %d not in [0, %d]", c->chunk, cmax);
+  if (c->chunk > 0 && c->n_micro % c->chunk) return ERR(LGA_ERR_INVALID_ARG, "n_micro %% chunk != 0");
+  if (!(c->lr >= 0.f) || !(c->beta1 >= 0.f && c->beta1 < 1.f) || !(c->beta2 >= 0.f && c->beta2 < 1.f) || !(c->adam_eps > 0.f) ||
+      !(c->ln_eps > 0.f))
+    return ERR(LGA_ERR_INVALID_ARG, "bad optimizer / LayerNorm hyper-parameter");
+  if ((int64_t)c->micro_batch * c->seq_len * c->n_micro > (int64_t)1 << 30) return ERR(LGA_ERR_UNSUPPORTED, "batch too large");
+
+  Cfg g{};
+  g.L = c->layers; g.d = c->d_model; g.H = c->heads; g.dh = dh; g.s = c->seq_len; g.b = c->micro_batch;
+  g.N = c->n_micro; g.D = c->dp; g.P = c->pp; g.f = 4 * g.d; g.M = g.b * g.s; g.Lloc = g.L / g.P;
+  // default chunk: all micro-batches of a layer in one launch (P=1); one micro-batch per launch
+  // under the pipeline so that the next stage can start early (reading A-13)
+  g.c = c->chunk > 0 ? c->chunk : (g.P > 1 ? 1 : g.N);
+  if (c->schedule == LGA_STANDARD) g.c = 1;
+  g.pl = 12LL * g.d * g.d + 13LL * g.d;
+  const int64_t q = 64LL * g.D;
+  g.plpad = (g.pl + q - 1) / q * q;
+  g.S = g.plpad / g.D;
+  g.bf16 = c->precision == LGA_BF16;
+  g.layered = c->schedule == LGA_LAYERED;
+  g.causal = c->causal != 0;
+  g.E = g.bf16 ? DT::BF16 : DT::F32;
+  g.G = (g.bf16 && g.D > 1) ? DT::BF16 : DT::F32;   // 16-bit reduction only when there is a reduction (A-7)
+  g.lr = c->lr; g.b1 = c->beta1; g.b2 = c->beta2; g.eps = c->adam_eps; g.wd = c->weight_decay; g.ln_eps = c->ln_eps;
+  g.retain = c->retain_grads != 0;
+  g.no_comm = (c->flags & LGA_FLAG_NO_COMM) != 0;
+  const int64_t d = g.d, f = g.f;
+  g.o_ln1w = 0; g.o_ln1b = d; g.o_wqkv = 2 * d; g.o_bqkv = g.o_wqkv + 3 * d * d; g.o_wo = g.o_bqkv + 3 * d;
+  g.o_bo = g.o_wo + d * d; g.o_ln2w = g.o_bo + d; g.o_ln2b = g.o_ln2w + d; g.o_w1 = g.o_ln2b + d;
+  g.o_b1 = g.o_w1 + d * f; g.o_w2 = g.o_b1 + f; g.o_b2 = g.o_w2 + f * d;
+  if (g.o_b2 + d != g.pl) return ERR(LGA_ERR_INVALID_ARG, "internal layout error");
+  *out = g;
+  return LGA_OK;
+}
+
+// ------------------------------------------------------------------ arena (one allocation, M10 / P:96)
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, used = 0;
+  bool planning = true;
+  template <typename T>
+  T* take(size_t count) {
+    size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+    T* p = planning ? nullptr : reinterpret_cast<T*>(base + used);
+    used += bytes;
+    return p;
+  }
+  void* take_bytes(size_t bytes) { return take<char>(bytes); }
+};
+
+struct PeerInfo {
+  cudaIpcMemHandle_t handle;
+  uint64_t off_ckpt, off_dY, off_flags;
+  uint64_t pad[5];
+};
+static_assert(sizeof(PeerInfo) % 16 == 0, "PeerInfo size");
+
+}  // namespace lga
+
+using namespace lga;
+
+struct lga_handle {
+  Cfg c{};
+  int rank = 0, world = 1, stage = 0, replica = 0, dev = 0;
+  bool bad = false;
+  cudaStream_t user = nullptr, s_comp = nullptr, s_comm = nullptr;
+  ncclComm_t world_comm = nullptr, dp_comm = nullptr;
+  Arena arena;
+  // training state, per local layer j: [Lloc][S]
+  float *master = nullptr, *mom = nullptr, *var = nullptr, *gkeep = nullptr, *gshard_acc = nullptr;
+  void* pshard = nullptr;
+  void* slot[2] = {nullptr, nullptr};
+  float* gacc = nullptr;
+  void* gstage[2] = {nullptr, nullptr};
+  // activations
+  float* ckpt = nullptr;  // [Lloc][N][M][d]
+  float* yout = nullptr;  // [N][M][d] on the stage owning layer L-1
+  float* dY = nullptr;    // [N][M][d]
+  float* dscratch = nullptr;  // [c][M][d] sink for dX of layer 0
+  // chunk workspace
+  void *a = nullptr, *qkv = nullptr, *o = nullptr, *cn = nullptr, *u = nullptr, *g = nullptr, *dYe = nullptr,
+       *dh1e = nullptr, *dO = nullptr, *dqkv = nullptr;
+  float *h1 = nullptr, *dC = nullptr, *dh1 = nullptr, *lse = nullptr, *dsum = nullptr, *partial = nullptr;
+  float2 *st1 = nullptr, *st2 = nullptr;
+  double *mse_partial = nullptr, *loss_dev = nullptr, *loss_host = nullptr;
+  float *xin = nullptr, *tin = nullptr;  // device copies for lga_step_host
+  unsigned long long* flags = nullptr;   // [0] fwd receive count, [1] bwd receive count
+  // pipeline peers
+  char* peer_next_base = nullptr;  // stage (s+1) mod P of my replica
+  char* peer_prev_base = nullptr;  // stage (s-1) mod P
+  float *next_ckpt = nullptr, *prev_dY = nullptr;
+  unsigned long long *next_flags = nullptr, *prev_flags = nullptr;
+  unsigned long long sent_fwd = 0, sent_bwd = 0, recv_fwd = 0, recv_bwd = 0;
+  int64_t partial_floats = 0;
+  // events
+  cudaEvent_t ev_in = nullptr, ev_ag[2] = {}, ev_slot_free[2] = {}, ev_grad[2] = {}, ev_adam[2] = {}, ev_comm_end = nullptr,
+              ev_comp_end = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_fwd_end = nullptr;
+  std::vector<cudaEvent_t> ev_wait0, ev_wait1;   // stall accounting pairs (s_comp)
+  std::vector<int> wait_kind;
+  int n_wait = 0;
+  int64_t t = 0;  // AdamW step counter
+  lga_comm_stats last{}, total{};
+};
+
+namespace lga {
+
+static int64_t local_to_global(const lga_handle* h, int j) { return (int64_t)h->stage + (int64_t)j * h->c.P; }
+static bool owns_last(const lga_handle* h) { return (h->c.L - 1) % h->c.P == h->stage; }
+static ncclDataType_t nccl_dt(DT t) { return t == DT::F32 ? ncclFloat32 : ncclBfloat16; }
+
+static char* eoff(void* p, DT t, int64_t i) { return static_cast<char*>(p) + i * (int64_t)dt_size(t); }
+
+static void plan_arena(lga_handle* h) {
+  Arena& A = h->arena;
+  const Cfg& c = h->c;
+  const int64_t S = c.S, Ll = c.Lloc, T = (int64_t)c.c * c.M, d = c.d, f = c.f;
+  const size_t e = dt_size(c.E);
+  A.used = 0;
+  h->master = A.take<float>(Ll * S);
+  h->mom = A.take<float>(Ll * S);
+  h->var = A.take<float>(Ll * S);
+  h->pshard = A.take_bytes(Ll * S * e);
+  h->gkeep = c.retain ? A.take<float>(Ll * S) : nullptr;
+  h->gshard_acc = c.layered ? nullptr : A.take<float>(Ll * S);
+  if (c.D > 1) {
+    h->slot[0] = A.take_bytes(c.plpad * e);
+    h->slot[1] = A.take_bytes(c.plpad * e);
+  }
+  h->gacc = A.take<float>(c.plpad);
+  h->gstage[0] = A.take_bytes(c.plpad * dt_size(c.G));
+  h->gstage[1] = A.take_bytes(c.plpad * dt_size(c.G));
+  const int64_t act = (int64_t)c.N * c.M * d;
+  h->ckpt = A.take<float>(Ll * act);
+  h->yout = A.take<float>(act);
+  h->dY = A.take<float>(act);
+  h->dscratch = A.take<float>(T * d);
+  h->a = A.take_bytes(T * d * e);
+  h->qkv = A.take_bytes(T * 3 * d * e);
+  h->o = A.take_bytes(T * d * e);
+  h->cn = A.take_bytes(T * d * e);
+  h->u = A.take_bytes(T * f * e);
+  h->g = A.take_bytes(T * f * e);
+  h->dYe = A.take_bytes(T * d * e);
+  h->dh1e = A.take_bytes(T * d * e);
+  h->dO = A.take_bytes(T * d * e);
+  h->dqkv = A.take_bytes(T * 3 * d * e);
+  h->h1 = A.take<float>(T * d);
+  h->dC = A.take<float>(T * d);
+  h->dh1 = A.take<float>(T * d);
+  h->lse = A.take<float>((int64_t)c.c * c.b * c.H * c.s);
+  h->dsum = A.take<float>((int64_t)c.c * c.b * c.H * c.s);
+  h->st1 = A.take<float2>(T);
+  h->st2 = A.take<float2>(T);
+  const int64_t pcol = (int64_t)colsum_blocks((int)T) * f;
+  const int64_t pln = (int64_t)ln_bwd_blocks((int)T) * 2 * d;
+  h->partial_floats = std::max(pcol, pln);
+  h->partial = A.take<float>(h->partial_floats);
+  h->mse_partial = A.take<double>(mse_blocks(act) + 64);
+  h->loss_dev = A.take<double>(c.N + 8);
+  h->xin = A.take<float>(act);
+  h->tin = A.take<float>(act);
+  h->flags = A.take<unsigned long long>(8);
+}
+
+// ------------------------------------------------------------------ GEMM dispatch
+static void gemm(lga_handle* h, GemmArgs g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0) return;
+  if (h->c.bf16) {
+    CK(gemm_bf16_tc(g, st));
+  } else {
+    gemm_f32_simt(g, st);
+  }
+  KCHECK();
+}
+
+// Gradient write mode of one chunk (reading A-3, subsystem (2)): where the chunk's gradient goes.
+struct GradDst {
+  const float* acc_in;  // fp32 accumulator to add (nullptr on the first chunk)
+  void* out;            // fp32 accumulator (not last) or the staging buffer (last)
+  DT out_dt;
+};
+static GradDst grad_dst(lga_handle* h, int chunk_idx, int nchunks, int gb, int64_t off) {
+  const bool first = chunk_idx == 0, last = chunk_idx == nchunks - 1;
+  GradDst r;
+  r.acc_in = first ? nullptr : h->gacc + off;
+  if (last) {
+    r.out = eoff(h->gstage[gb], h->c.G, off);
+    r.out_dt = h->c.G;
+  } else {
+    r.out = h->gacc + off;
+    r.out_dt = DT::F32;
+  }
+  return r;
+}
+
+// ------------------------------------------------------------------ layer executor
+// Forward of local layer j over micro-batches [m0, m0+c) (module docstring of kernels.cuh).
+// x_in: [c][M][d] fp32; y_out: fp32 destination or nullptr (recompute: FFN2 not needed).
+static void layer_fwd(lga_handle* h, const void* W, const float* x_in, float* y_out, cudaStream_t st) {
+  const Cfg& c = h->c;
+  const int T = c.c * c.M;
+  const int d = c.d;
+  const DT E = c.E;
+  ln_fwd(x_in, eoff((void*)W, E, c.o_ln1w), eoff((void*)W, E, c.o_ln1b), E, h->a, E, h->st1, T, d, c.ln_eps, st);
+  KCHECK();
+  {  // qkv = a Wqkv + bqkv
+    GemmArgs g;
+    g.M = T; g.N = 3 * d; g.K = d;
+    g.A = h->a; g.lda = d; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_wqkv); g.ldb = 3 * d; g.b_kmajor = false;
+    g.epi.kind = EPI_STORE; g.epi.bias = eoff((void*)W, E, c.o_bqkv); g.epi.bias_dt = E;
+    g.epi.out = h->qkv; g.epi.ldo = 3 * d; g.epi.out_dt = E;
+    gemm(h, g, st);
+  }
+  {  // o = attention(q, k, v)
+    AttnArgs a;
+    a.nseq = c.c * c.b; a.seq = c.s; a.heads = c.H; a.dh = c.dh; a.d = d; a.causal = c.causal;
+    a.scale = 1.0f / sqrtf((float)c.dh);
+    a.qkv = h->qkv; a.o = h->o; a.lse = h->lse;
+    if (c.bf16) attn_fwd_bf16(a, st); else attn_fwd_f32(a, st);
+    KCHECK();
+  }
+  {  // h1 = x + o Wo + bo
+    GemmArgs g;
+    g.M = T; g.N = d; g.K = d;
+    g.A = h->o; g.lda = d; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_wo); g.ldb = d; g.b_kmajor = false;
+    g.epi.kind = EPI_STORE; g.epi.bias = eoff((void*)W, E, c.o_bo); g.epi.bias_dt = E;
+    g.epi.res = x_in; g.epi.ldr = d;
+    g.epi.out = h->h1; g.epi.ldo = d; g.epi.out_dt = DT::F32;
+    gemm(h, g, st);
+  }
+  ln_fwd(h->h1, eoff((void*)W, E, c.o_ln2w), eoff((void*)W, E, c.o_ln2b), E, h->cn, E, h->st2, T, d, c.ln_eps, st);
+  KCHECK();
+  {  // u = c W1 + b1 ; g = GELU(u)
+    GemmArgs g;
+    g.M = T; g.N = c.f; g.K = d;
+    g.A = h->cn; g.lda = d; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_w1); g.ldb = c.f; g.b_kmajor = false;
+    g.epi.kind = EPI_GELU_FWD; g.epi.bias = eoff((void*)W, E, c.o_b1); g.epi.bias_dt = E;
+    g.epi.aux = h->u; g.epi.ldaux = c.f; g.epi.aux_dt = E;
+    g.epi.out = h->g; g.epi.ldo = c.f; g.epi.out_dt = E;
+    gemm(h, g, st);
+  }
+  if (y_out) {  // y = h1 + g W2 + b2
+    GemmArgs g;
+    g.M = T; g.N = d; g.K = c.f;
+    g.A = h->g; g.lda = c.f; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_w2); g.ldb = d; g.b_kmajor = false;
+    g.epi.kind = EPI_STORE; g.epi.bias = eoff((void*)W, E, c.o_b2); g.epi.bias_dt = E;
+    g.epi.res = h->h1; g.epi.ldr = d;
+    g.epi.out = y_out; g.epi.ldo = d; g.epi.out_dt = DT::F32;
+    gemm(h, g, st);
+  }
+}
+
+// wgrad: dW[i][j] (+)= sum_t X[t][i] dYm[t][j]  -> region at `off` with leading dim n
+static void wgrad(lga_handle* h, const void* X, int64_t ldx, const void* Dy, int64_t ldy, int m, int n, int T,
+                  const GradDst& dst, int64_t /*off*/, cudaStream_t st) {
+  GemmArgs g;
+  g.M = m; g.N = n; g.K = T;
+  g.A = X; g.lda = ldx; g.a_kmajor = false;
+  g.B = Dy; g.ldb = ldy; g.b_kmajor = false;
+  g.epi.kind = EPI_STORE;
+  g.epi.acc_in = dst.acc_in; g.epi.ldacc = n;
+  g.epi.out = dst.out; g.epi.ldo = n; g.epi.out_dt = dst.out_dt;
+  gemm(h, g, st);
+}
+
+static void bias_grad(lga_handle* h, const void* X, DT xdt, int64_t ldx, int n, int T, const GradDst& dst, cudaStream_t st) {
+  const int nblk = colsum_partial(X, xdt, ldx, T, n, h->partial, st);
+  KCHECK();
+  colsum_finish(h->partial, nblk, n, n, dst.acc_in, dst.out, dst.out_dt, st);
+  KCHECK();
+}
+
+// Backward of local layer j over one chunk; the layer's intermediates are in the workspace
+// (recomputed just before).  dY: fp32 [c][M][d] gradient of the layer output, read;
+// dx_out: where dX goes (in place over dY, the previous stage's buffer, or a scratch sink).
+static void layer_bwd(lga_handle* h, const void* W, const float* x_in, const float* dY, float* dx_out,
+                      int chunk_idx, int nchunks, int gb, cudaStream_t st) {
+  const Cfg& c = h->c;
+  const int T = c.c * c.M;
+  const int d = c.d, f = c.f;
+  const DT E = c.E;
+  const void* dYe = dY;
+  if (c.bf16) {
+    cast_f32(dY, h->dYe, E, (int64_t)T * d, st);
+    KCHECK();
+    dYe = h->dYe;
+  }
+  auto dst = [&](int64_t off) { return grad_dst(h, chunk_idx, nchunks, gb, off); };
+  // ---- FFN2: y = h1 + g W2 + b2
+  wgrad(h, h->g, f, dYe, d, f, d, T, dst(c.o_w2), c.o_w2, st);
+  bias_grad(h, dY, DT::F32, d, d, T, dst(c.o_b2), st);
+  {  // dU = (dY W2^T) * GELU'(u), written over u
+    GemmArgs g;
+    g.M = T; g.N = f; g.K = d;
+    g.A = dYe; g.lda = d; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_w2); g.ldb = d; g.b_kmajor = true;
+    g.epi.kind = EPI_GELU_BWD; g.epi.aux = h->u; g.epi.ldaux = f; g.epi.aux_dt = E;
+    g.epi.out = h->u; g.epi.ldo = f; g.epi.out_dt = E;
+    gemm(h, g, st);
+  }
+  void* dU = h->u;
+  // ---- FFN1: u = c W1 + b1
+  wgrad(h, h->cn, d, dU, f, d, f, T, dst(c.o_w1), c.o_w1, st);
+  bias_grad(h, dU, E, f, f, T, dst(c.o_b1), st);
+  {  // dC = dU W1^T
+    GemmArgs g;
+    g.M = T; g.N = d; g.K = f;
+    g.A = dU; g.lda = f; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_w1); g.ldb = f; g.b_kmajor = true;
+    g.epi.out = h->dC; g.epi.ldo = d; g.epi.out_dt = DT::F32;
+    gemm(h, g, st);
+  }
+  // ---- LN2 backward + residual: dh1 = dY + LN2'(dC)
+  {
+    const int nblk = ln_bwd(h->dC, h->h1, h->st2, eoff((void*)W, E, c.o_ln2w), E, dY, h->dh1, c.bf16 ? h->dh1e : nullptr, E,
+                            h->partial, T, d, st);
+    KCHECK();
+    GradDst gw = dst(c.o_ln2w), gbias = dst(c.o_ln2b);
+    colsum_finish(h->partial, nblk, 2LL * d, d, gw.acc_in, gw.out, gw.out_dt, st);
+    colsum_finish(h->partial + d, nblk, 2LL * d, d, gbias.acc_in, gbias.out, gbias.out_dt, st);
+    KCHECK();
+  }
+  const void* dh1e = c.bf16 ? (const void*)h->dh1e : (const void*)h->dh1;
+  // ---- O projection: h1 = x + o Wo + bo
+  wgrad(h, h->o, d, dh1e, d, d, d, T, dst(c.o_wo), c.o_wo, st);
+  bias_grad(h, h->dh1, DT::F32, d, d, T, dst(c.o_bo), st);
+  {  // dO = dh1 Wo^T
+    GemmArgs g;
+    g.M = T; g.N = d; g.K = d;
+    g.A = dh1e; g.lda = d; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_wo); g.ldb = d; g.b_kmajor = true;
+    g.epi.out = h->dO; g.epi.ldo = d; g.epi.out_dt = E;
+    gemm(h, g, st);
+  }
+  {  // attention backward -> dqkv
+    AttnArgs a;
+    a.nseq = c.c * c.b; a.seq = c.s; a.heads = c.H; a.dh = c.dh; a.d = d; a.causal = c.causal;
+    a.scale = 1.0f / sqrtf((float)c.dh);
+    a.qkv = h->qkv; a.o = h->o; a.lse = h->lse; a.dO = h->dO; a.dsum = h->dsum; a.dqkv = h->dqkv;
+    if (c.bf16) attn_bwd_bf16(a, st); else attn_bwd_f32(a, st);
+    KCHECK();
+  }
+  // ---- QKV: qkv = a Wqkv + bqkv
+  wgrad(h, h->a, d, h->dqkv, 3 * d, d, 3 * d, T, dst(c.o_wqkv), c.o_wqkv, st);
+  bias_grad(h, h->dqkv, E, 3 * d, 3 * d, T, dst(c.o_bqkv), st);
+  {  // dA = dqkv Wqkv^T  (into dC, free now)
+    GemmArgs g;
+    g.M = T; g.N = d; g.K = 3 * d;
+    g.A = h->dqkv; g.lda = 3 * d; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_wqkv); g.ldb = 3 * d; g.b_kmajor = true;
+    g.epi.out = h->dC; g.epi.ldo = d; g.epi.out_dt = DT::F32;
+    gemm(h, g, st);
+  }
+  // ---- LN1 backward + residual: dX = dh1 + LN1'(dA)
+  {
+    const int nblk = ln_bwd(h->dC, x_in, h->st1, eoff((void*)W, E, c.o_ln1w), E, h->dh1, dx_out, nullptr, E, h->partial, T,
+                            d, st);
+    KCHECK();
+    GradDst gw = dst(c.o_ln1w), gbias = dst(c.o_ln1b);
+    colsum_finish(h->partial, nblk, 2LL * d, d, gw.acc_in, gw.out, gw.out_dt, st);
+    colsum_finish(h->partial + d, nblk, 2LL * d, d, gbias.acc_in, gbias.out, gbias.out_dt, st);
+    KCHECK();
+  }
+}
+
+// ------------------------------------------------------------------ scheduler helpers
+static void count_wait(lga_handle* h, cudaEvent_t ev, int kind) {
+  // stall accounting: event pair around the compute stream's wait on a comm event (BJ metric)
+  if (h->n_wait >= (int)h->ev_wait0.size()) {
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    h->ev_wait0.push_back(a);
+    h->ev_wait1.push_back(b);
+    h->wait_kind.push_back(kind);
+  }
+  h->wait_kind[h->n_wait] = kind;
+  CK(cudaEventRecord(h->ev_wait0[h->n_wait], h->s_comp));
+  if (ev) CK(cudaStreamWaitEvent(h->s_comp, ev, 0));
+  return;
+}
+static void count_wait_end(lga_handle* h) {
+  CK(cudaEventRecord(h->ev_wait1[h->n_wait], h->s_comp));
+  h->n_wait++;
+}
+
+static const void* layer_weights(lga_handle* h, int j, int slot) {
+  if (h->c.D > 1) return h->slot[slot];
+  return eoff(h->pshard, h->c.E, (int64_t)j * h->c.S);
+}
+
+static void all_gather(lga_handle* h, int j, int slot) {
+  const Cfg& c = h->c;
+  if (c.D <= 1) return;
+  h->last.ag_calls++;
+  h->last.ag_bytes += (uint64_t)(c.D - 1) * c.S * dt_size(c.E);
+  if (c.no_comm) return;
+  NK(ncclAllGather(eoff(h->pshard, c.E, (int64_t)j * c.S), h->slot[slot], (size_t)c.S, nccl_dt(c.E), h->dp_comm, h->s_comm));
+}
+
+// AdamW on this rank's shard of local layer j (update "as soon as possible", A-12)
+static void adam_layer(lga_handle* h, int j, const void* g, DT gdt) {
+  const Cfg& c = h->c;
+  const float bc1 = 1.0f - powf(c.b1, (float)h->t), bc2 = 1.0f - powf(c.b2, (float)h->t);
+  const float gscale = 1.0f / ((float)c.D * (float)c.N);   // gradient of the mean loss (A-3)
+  const int64_t off = (int64_t)j * c.S;
+  adamw(g, gdt, gscale, h->master + off, h->mom + off, h->var + off, eoff(h->pshard, c.E, off), c.E,
+        c.retain ? h->gkeep + off : nullptr, c.S, c.lr, c.b1, c.b2, c.eps, c.wd, bc1, bc2, h->s_comm);
+  KCHECK();
+}
+
+// reduce-scatter of the staged gradient in place (once per layer per step); returns the shard
+static void* reduce_scatter(lga_handle* h, int gb) {
+  const Cfg& c = h->c;
+  void* gs = h->gstage[gb];
+  void* shard_g = eoff(gs, c.G, (int64_t)h->replica * c.S);
+  if (c.D > 1) {
+    h->last.rs_calls++;
+    h->last.rs_bytes += (uint64_t)(c.D - 1) * c.S * dt_size(c.G);
+    if (!c.no_comm)
+      NK(ncclReduceScatter(gs, shard_g, (size_t)c.S, nccl_dt(c.G), ncclSum, h->dp_comm, h->s_comm));
+  }
+  return shard_g;
+}
+
+static float* ckpt_ptr(lga_handle* h, int j, int m) {
+  const Cfg& c = h->c;
+  return h->ckpt + ((int64_t)j * c.N + m) * (int64_t)c.M * c.d;
+}
+static float* act_ptr(float* base, const Cfg& c, int m) { return base + (int64_t)m * c.M * c.d; }
+
+// ------------------------------------------------------------------ the step (LAYERED, any D, any P)
+static void step_layered(lga_handle* h, const float* x, const float* T) {
+  const Cfg& c = h->c;
+  const int nchunks = c.N / c.c;
+  const bool last_stage = owns_last(h);
+  const int64_t mb = (int64_t)c.M * c.d;
+  int agk = 0;  // running all-gather index: slot = agk % 2
+  // ---------------- forward: layer-major over all micro-batches
+  if (c.D > 1) {
+    CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[0], 0));
+    all_gather(h, 0, 0);
+    CK(cudaEventRecord(h->ev_ag[0], h->s_comm));
+  }
+  for (int j = 0; j < c.Lloc; ++j, ++agk) {
+    const int sl = agk % 2;
+    const int64_t i = local_to_global(h, j);
+    if (c.D > 1 && j + 1 < c.Lloc) {  // prefetch Restore(i+P) while computing layer i
+      CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[(agk + 1) % 2], 0));
+      all_gather(h, j + 1, (agk + 1) % 2);
+      CK(cudaEventRecord(h->ev_ag[(agk + 1) % 2], h->s_comm));
+    }
+    if (c.D > 1) {
+      count_wait(h, h->ev_ag[sl], 0);
+      count_wait_end(h);
+    }
+    const void* W = layer_weights(h, j, sl);
+    for (int k = 0; k < nchunks; ++k) {
+      const int m0 = k * c.c;
+      const float* xin;
+      if (i == 0) {
+        xin = x + m0 * mb;
+      } else {
+        xin = ckpt_ptr(h, j, m0);
+        if (c.P > 1) {  // pipeline receive: x_i[m0..m0+c) from stage (i-1) mod P
+          h->recv_fwd += c.c;
+          h->last.p2p_recv_calls += c.c;
+          h->last.p2p_recv_bytes += (uint64_t)c.c * mb * 4;
+          if (!c.no_comm) {
+            count_wait(h, nullptr, 1);
+            wait_flag(h->flags + 0, h->recv_fwd, h->s_comp);
+            KCHECK();
+            count_wait_end(h);
+          }
+        }
+      }
+      if (i == 0 && c.P == 1) {
+        // layer 0 input is the caller's x; keep a checkpoint pointer to it (no copy)
+      }
+      float* yo;
+      if (i == c.L - 1) {
+        yo = act_ptr(h->yout, c, m0);
+      } else if (c.P == 1) {
+        yo = ckpt_ptr(h, j + 1, m0);
+      } else {  // write x_{i+1} straight into the next stage's checkpoint buffer (fused p2p)
+        const int jn = (int)((i + 1) / c.P);
+        yo = c.no_comm ? h->dscratch : h->next_ckpt + ((int64_t)jn * c.N + m0) * mb;
+      }
+      layer_fwd(h, W, xin, yo, h->s_comp);
+      h->last.fwd_units += c.c;
+      if (c.P > 1 && i < c.L - 1) {
+        h->sent_fwd += c.c;
+        h->last.p2p_send_calls += c.c;
+        h->last.p2p_send_bytes += (uint64_t)c.c * mb * 4;
+        if (!c.no_comm) {
+          set_flag(h->next_flags + 0, h->sent_fwd, h->s_comp);
+          KCHECK();
+        }
+      }
+      if (i == c.L - 1) {  // loss of this chunk + seed gradient
+        const int64_t n = (int64_t)c.c * mb;
+        mse_fwd_bwd(act_ptr(h->yout, c, m0), T + m0 * mb, act_ptr(h->dY, c, m0), h->mse_partial + 0, n,
+                    1.0f / (float)mb, h->s_comp);
+        KCHECK();
+        // this chunk's sum of micro-batch losses -> loss_dev[1 + k] (summed in fixed order at the end)
+        mse_finish(h->mse_partial, mse_blocks(n), 0.5 / (double)mb, h->loss_dev + 1 + k, h->s_comp);
+        KCHECK();
+      }
+    }
+    CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
+  }
+  CK(cudaEventRecord(h->ev_fwd_end, h->s_comp));
+  // ---------------- backward: layer-major, recompute + backward over all micro-batches
+  if (c.D > 1) {
+    CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[agk % 2], 0));
+    all_gather(h, c.Lloc - 1, agk % 2);
+    CK(cudaEventRecord(h->ev_ag[agk % 2], h->s_comm));
+  }
+  for (int j = c.Lloc - 1; j >= 0; --j, ++agk) {
+    const int sl = agk % 2;
+    const int64_t i = local_to_global(h, j);
+    const int gb = j % 2;
+    if (c.D > 1 && j - 1 >= 0) {
+      CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[(agk + 1) % 2], 0));
+      all_gather(h, j - 1, (agk + 1) % 2);
+      CK(cudaEventRecord(h->ev_ag[(agk + 1) % 2], h->s_comm));
+    }
+    if (c.D > 1) {
+      count_wait(h, h->ev_ag[sl], 0);
+      count_wait_end(h);
+    }
+    CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));   // staging buffer gb free again
+    const void* W = layer_weights(h, j, sl);
+    for (int k = 0; k < nchunks; ++k) {
+      const int m0 = k * c.c;
+      const float* xin = (i == 0) ? x + m0 * mb : ckpt_ptr(h, j, m0);
+      float* dYc = act_ptr(h->dY, c, m0);
+      if (c.P > 1 && i < c.L - 1) {  // receive dY_i[m0..) from stage (i+1) mod P
+        h->recv_bwd += c.c;
+        h->last.p2p_recv_calls += c.c;
+        h->last.p2p_recv_bytes += (uint64_t)c.c * mb * 4;
+        if (!c.no_comm) {
+          count_wait(h, nullptr, 1);
+          wait_flag(h->flags + 1, h->recv_bwd, h->s_comp);
+          KCHECK();
+          count_wait_end(h);
+        }
+      }
+      layer_fwd(h, W, xin, nullptr, h->s_comp);   // recompute
+      h->last.recompute_units += c.c;
+      float* dx;
+      if (i == 0) dx = h->dscratch;
+      else if (c.P == 1) dx = dYc;
+      else dx = c.no_comm ? h->dscratch : h->prev_dY + m0 * mb;
+      layer_bwd(h, W, xin, dYc, dx, k, nchunks, gb, h->s_comp);
+      h->last.bwd_units += c.c;
+      if (c.P > 1 && i > 0) {
+        h->sent_bwd += c.c;
+        h->last.p2p_send_calls += c.c;
+        h->last.p2p_send_bytes += (uint64_t)c.c * mb * 4;
+        if (!c.no_comm) {
+          set_flag(h->prev_flags + 1, h->sent_bwd, h->s_comp);
+          KCHECK();
+        }
+      }
+    }
+    CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
+    CK(cudaEventRecord(h->ev_grad[gb], h->s_comp));
+    CK(cudaStreamWaitEvent(h->s_comm, h->ev_grad[gb], 0));
+    void* shard_g = reduce_scatter(h, gb);
+    adam_layer(h, j, shard_g, c.G);
+    CK(cudaEventRecord(h->ev_adam[gb], h->s_comm));
+  }
+  (void)last_stage;
+}
+
+// ------------------------------------------------------------------ STANDARD (comparison, P = 1)
+// for each micro-batch: for l: AG(l); fwd(l, m); loss(m); for l desc: AG(l); recompute+bwd(l, m);
+// RS(l) -> shard, accumulate on the shard; AdamW after the last micro-batch.
+static void step_standard(lga_handle* h, const float* x, const float* T) {
+  const Cfg& c = h->c;
+  const int64_t mb = (int64_t)c.M * c.d;
+  int agk = 0;
+  for (int m = 0; m < c.N; ++m) {
+    for (int j = 0; j < c.L; ++j, ++agk) {
+      const int sl = agk % 2;
+      if (c.D > 1) {
+        CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[sl], 0));
+        all_gather(h, j, sl);
+        CK(cudaEventRecord(h->ev_ag[sl], h->s_comm));
+        count_wait(h, h->ev_ag[sl], 0);
+        count_wait_end(h);
+      }
+      const float* xin = j == 0 ? x + m * mb : ckpt_ptr(h, j, m);
+      float* yo = j == c.L - 1 ? act_ptr(h->yout, c, m) : ckpt_ptr(h, j + 1, m);
+      layer_fwd(h, layer_weights(h, j, sl), xin, yo, h->s_comp);
+      h->last.fwd_units++;
+      CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
+    }
+    mse_fwd_bwd(act_ptr(h->yout, c, m), T + m * mb, act_ptr(h->dY, c, m), h->mse_partial, mb, 1.0f / (float)mb, h->s_comp);
+    KCHECK();
+    mse_finish(h->mse_partial, mse_blocks(mb), 0.5 / (double)mb, h->loss_dev + 1 + m, h->s_comp);
+    KCHECK();
+    for (int j = c.L - 1; j >= 0; --j, ++agk) {
+      const int sl = agk % 2;
+      const int gb = j % 2;
+      if (c.D > 1) {
+        CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[sl], 0));
+        all_gather(h, j, sl);
+        CK(cudaEventRecord(h->ev_ag[sl], h->s_comm));
+        count_wait(h, h->ev_ag[sl], 0);
+        count_wait_end(h);
+      }
+      CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));
+      const void* W = layer_weights(h, j, sl);
+      const float* xin = j == 0 ? x + m * mb : ckpt_ptr(h, j, m);
+      float* dYc = act_ptr(h->dY, c, m);
+      layer_fwd(h, W, xin, nullptr, h->s_comp);
+      h->last.recompute_units++;
+      layer_bwd(h, W, xin, dYc, j == 0 ? h->dscratch : dYc, 0, 1, gb, h->s_comp);
+      h->last.bwd_units++;
+      CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
+      CK(cudaEventRecord(h->ev_grad[gb], h->s_comp));
+      CK(cudaStreamWaitEvent(h->s_comm, h->ev_grad[gb], 0));
+      // reduce-scatter this micro-batch's gradient, accumulate it on the shard (fixed order over m)
+      void* shard_g = reduce_scatter(h, gb);
+      float* acc = h->gshard_acc + (int64_t)j * c.S;
+      shard_accumulate(shard_g, c.G, acc, c.S, m == 0, h->s_comm);
+      KCHECK();
+      if (m == c.N - 1) adam_layer(h, j, acc, DT::F32);
+      CK(cudaEventRecord(h->ev_adam[gb], h->s_comm));
+    }
+  }
+}
+
+}  // namespace lga
+
+// ================================================================== C ABI
+using namespace lga;
+
+#define ABI_TRY try {
+#define ABI_CATCH                                      \
+  }                                                    \
+  catch (const StatusError& e) {                       \
+    if (h) h->bad = true;                              \
+    return e.s;                                        \
+  }                                                    \
+  catch (...) {                                        \
+    if (h) h->bad = true;                              \
+    return ERR(LGA_ERR_CUDA, "unexpected exception");  \
+  }
+
+extern "C" {
+
+uint32_t lga_abi_version(void) { return LGA_ABI_VERSION; }
+
+const char* lga_status_string(lga_status s) {
+  switch (s) {
+    case LGA_OK: return "LGA_OK";
+    case LGA_ERR_INVALID_ARG: return "LGA_ERR_INVALID_ARG";
+    case LGA_ERR_UNSUPPORTED: return "LGA_ERR_UNSUPPORTED";
+    case LGA_ERR_OUT_OF_MEMORY: return "LGA_ERR_OUT_OF_MEMORY";
+    case LGA_ERR_CUDA: return "LGA_ERR_CUDA";
+    case LGA_ERR_NCCL: return "LGA_ERR_NCCL";
+    case LGA_ERR_SIZE_MISMATCH: return "LGA_ERR_SIZE_MISMATCH";
+    case LGA_ERR_BAD_STATE: return "LGA_ERR_BAD_STATE";
+  }
+  return "LGA_ERR_UNKNOWN";
+}
+
+const char* lga_last_error(void) { return g_last_error.c_str(); }
+
+lga_status lga_param_count(const lga_config* cfg, uint64_t* per_layer, uint64_t* total) {
+  if (!cfg) return ERR(LGA_ERR_INVALID_ARG, "cfg is NULL");
+  if (cfg->d_model <= 0 || cfg->layers <= 0) return ERR(LGA_ERR_INVALID_ARG, "non-positive dimension");
+  const uint64_t d = (uint64_t)cfg->d_model, n = (uint64_t)(cfg->ffn_mult > 0 ? cfg->ffn_mult : 4);
+  const uint64_t pl = (4 + 2 * n) * d * d + 13 * d;
+  if (per_layer) *per_layer = pl;
+  if (total) *total = pl * (uint64_t)cfg->layers;
+  return LGA_OK;
+}
+
+lga_status lga_nccl_unique_id(uint8_t* out) {
+  if (!out) return ERR(LGA_ERR_INVALID_ARG, "out is NULL");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return ERR(LGA_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == LGA_NCCL_ID_BYTES, "nccl id size");
+  memcpy(out, &id, sizeof(id));
+  return LGA_OK;
+}
+
+static void free_handle(lga_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->dev);
+  if (h->s_comp) cudaStreamSynchronize(h->s_comp);
+  if (h->s_comm) cudaStreamSynchronize(h->s_comm);
+  if (h->peer_next_base) cudaIpcCloseMemHandle(h->peer_next_base);
+  if (h->peer_prev_base && h->peer_prev_base != h->peer_next_base) cudaIpcCloseMemHandle(h->peer_prev_base);
+  if (h->dp_comm) ncclCommDestroy(h->dp_comm);
+  if (h->world_comm) ncclCommDestroy(h->world_comm);
+  cudaEvent_t evs[] = {h->ev_in, h->ev_ag[0], h->ev_ag[1], h->ev_slot_free[0], h->ev_slot_free[1], h->ev_grad[0],
+                       h->ev_grad[1], h->ev_adam[0], h->ev_adam[1], h->ev_comm_end, h->ev_comp_end, h->ev_t0, h->ev_t1,
+                       h->ev_fwd_end};
+  for (auto e : evs)
+    if (e) cudaEventDestroy(e);
+  for (auto e : h->ev_wait0) cudaEventDestroy(e);
+  for (auto e : h->ev_wait1) cudaEventDestroy(e);
+  if (h->s_comp) cudaStreamDestroy(h->s_comp);
+  if (h->s_comm) cudaStreamDestroy(h->s_comm);
+  if (h->arena.base) cudaFree(h->arena.base);
+  if (h->loss_host) cudaFreeHost(h->loss_host);
+  delete h;
+}
+
+lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t device, const uint8_t* nccl_id,
+                    uintptr_t cuda_stream, const float* init_params, uint64_t seed, lga_handle** out) {
+  if (!out) return ERR(LGA_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  Cfg c;
+  lga_status s = validate(cfg, world, &c);
+  if (s != LGA_OK) return s;
+  if (rank < 0 || rank >= world) return ERR(LGA_ERR_INVALID_ARG, "rank %d out of [0, %d)", rank, world);
+  if (world > 1 && !nccl_id) return ERR(LGA_ERR_INVALID_ARG, "nccl_id is NULL with world %d", world);
+  lga_handle* h = new lga_handle();
+  h->c = c;
+  h->rank = rank;
+  h->world = world;
+  h->dev = device;
+  h->stage = rank % c.P;
+  h->replica = rank / c.P;
+  h->user = reinterpret_cast<cudaStream_t>(cuda_stream);
+  ABI_TRY
+  CK(cudaSetDevice(device));
+  int prio_lo = 0, prio_hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CK(cudaStreamCreateWithPriority(&h->s_comp, cudaStreamNonBlocking, prio_lo));
+  CK(cudaStreamCreateWithPriority(&h->s_comm, cudaStreamNonBlocking, prio_hi));   // comm first
+  cudaEvent_t* evs[] = {&h->ev_in, &h->ev_ag[0], &h->ev_ag[1], &h->ev_slot_free[0], &h->ev_slot_free[1], &h->ev_grad[0],
+                        &h->ev_grad[1], &h->ev_adam[0], &h->ev_adam[1], &h->ev_comm_end, &h->ev_comp_end};
+  for (auto e : evs) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  CK(cudaEventCreate(&h->ev_t0));
+  CK(cudaEventCreate(&h->ev_t1));
+  CK(cudaEventCreate(&h->ev_fwd_end));
+  // arena: plan, allocate once, carve
+  h->arena.planning = true;
+  plan_arena(h);
+  const size_t need = h->arena.used + 4096;
+  cudaError_t ae = cudaMalloc(&h->arena.base, need);
+  if (ae != cudaSuccess) {
+    cudaGetLastError();
+    free_handle(h);
+    return ERR(LGA_ERR_OUT_OF_MEMORY, "arena of %zu bytes: %s", need, cudaGetErrorString(ae));
+  }
+  h->arena.cap = need;
+  h->arena.planning = false;
+  plan_arena(h);
+  CK(cudaMemsetAsync(h->arena.base, 0, need, h->s_comp));
+  CK(cudaMallocHost(&h->loss_host, 8 * sizeof(double)));
+  // communicators: world (loss all-reduce, handle exchange) and the stage's DP group
+  if (world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof(id));
+    NK(ncclCommInitRank(&h->world_comm, world, id, rank));
+    if (c.D > 1) {
+      NK(ncclCommSplit(h->world_comm, h->stage, h->replica, &h->dp_comm, nullptr));
+    }
+  }
+  // parameters: fp32 master shard of each local layer (A-10: contiguous 1/D slice of the padded layer)
+  const int64_t Ll = c.Lloc;
+  {
+    std::vector<float> tmp;
+    float* dev_full = nullptr;
+    if (!init_params) CK(cudaMalloc(&dev_full, (size_t)c.pl * sizeof(float)));
+    for (int j = 0; j < Ll; ++j) {
+      const int64_t gl = local_to_global(h, j);
+      const int64_t lo = (int64_t)h->replica * c.S, hi = std::min<int64_t>(lo + c.S, c.pl);
+      float* dst = h->master + (int64_t)j * c.S;
+      if (init_params) {
+        if (hi > lo)
+          CK(cudaMemcpyAsync(dst, init_params + gl * c.pl + lo, (size_t)(hi - lo) * sizeof(float), cudaMemcpyHostToDevice,
+                             h->s_comp));
+      } else {
+        init_params_device(dev_full, 1, c.d, 4, c.L, gl, seed, h->s_comp);
+        KCHECK();
+        if (hi > lo)
+          CK(cudaMemcpyAsync(dst, dev_full + lo, (size_t)(hi - lo) * sizeof(float), cudaMemcpyDeviceToDevice, h->s_comp));
+      }
+    }
+    CK(cudaStreamSynchronize(h->s_comp));
+    if (dev_full) CK(cudaFree(dev_full));
+    cast_f32(h->master, h->pshard, c.E, Ll * c.S, h->s_comp);
+    KCHECK();
+  }
+  // pipeline peers: exchange IPC handles over the world communicator
+  if (c.P > 1) {
+    PeerInfo me{};
+    CK(cudaIpcGetMemHandle(&me.handle, h->arena.base));
+    me.off_ckpt = (uint64_t)((char*)h->ckpt - h->arena.base);
+    me.off_dY = (uint64_t)((char*)h->dY - h->arena.base);
+    me.off_flags = (uint64_t)((char*)h->flags - h->arena.base);
+    PeerInfo* dev_info = nullptr;
+    CK(cudaMalloc(&dev_info, sizeof(PeerInfo) * (world + 1)));
+    CK(cudaMemcpy(dev_info + world, &me, sizeof(me), cudaMemcpyHostToDevice));
+    NK(ncclAllGather(dev_info + world, dev_info, sizeof(PeerInfo), ncclUint8, h->world_comm, h->s_comp));
+    std::vector<PeerInfo> all(world);
+    CK(cudaMemcpyAsync(all.data(), dev_info, sizeof(PeerInfo) * world, cudaMemcpyDeviceToHost, h->s_comp));
+    CK(cudaStreamSynchronize(h->s_comp));
+    CK(cudaFree(dev_info));
+    const int next = h->replica * c.P + (h->stage + 1) % c.P;
+    const int prev = h->replica * c.P + (h->stage + c.P - 1) % c.P;
+    void* pn = nullptr;
+    CK(cudaIpcOpenMemHandle(&pn, all[next].handle, cudaIpcMemLazyEnablePeerAccess));
+    h->peer_next_base = (char*)pn;
+    if (prev == next) {
+      h->peer_prev_base = h->peer_next_base;
+    } else {
+      void* pp = nullptr;
+      CK(cudaIpcOpenMemHandle(&pp, all[prev].handle, cudaIpcMemLazyEnablePeerAccess));
+      h->peer_prev_base = (char*)pp;
+    }
+    h->next_ckpt = (float*)(h->peer_next_base + all[next].off_ckpt);
+    h->next_flags = (unsigned long long*)(h->peer_next_base + all[next].off_flags);
+    h->prev_dY = (float*)(h->peer_prev_base + all[prev].off_dY);
+    h->prev_flags = (unsigned long long*)(h->peer_prev_base + all[prev].off_flags);
+  }
+  CK(cudaStreamSynchronize(h->s_comp));
+  // both "staging buffer free" events start completed
+  CK(cudaEventRecord(h->ev_adam[0], h->s_comm));
+  CK(cudaEventRecord(h->ev_adam[1], h->s_comm));
+  CK(cudaEventRecord(h->ev_slot_free[0], h->s_comp));
+  CK(cudaEventRecord(h->ev_slot_free[1], h->s_comp));
+  if (world > 1) {  // all ranks' arenas are initialised before anyone writes into a peer
+    double* tmp = h->loss_dev;
+    NK(ncclAllReduce(tmp, tmp, 1, ncclFloat64, ncclSum, h->world_comm, h->s_comp));
+    CK(cudaStreamSynchronize(h->s_comp));
+  }
+  *out = h;
+  return LGA_OK;
+  ABI_CATCH
+}
+
+static lga_status run_step(lga_handle* h, const float* x, const float* T, double* loss_out, bool host_inputs) {
+  if (!h) return ERR(LGA_ERR_INVALID_ARG, "handle is NULL");
+  if (h->bad) return ERR(LGA_ERR_BAD_STATE, "handle latched after an earlier CUDA/NCCL error");
+  const Cfg& c = h->c;
+  const bool need_x = h->stage == 0, need_t = owns_last(h);
+  if ((need_x && !x) || (need_t && !T)) return ERR(LGA_ERR_INVALID_ARG, "x / target NULL on a stage that reads it");
+  ABI_TRY
+  CK(cudaSetDevice(h->dev));
+  h->last = lga_comm_stats{};
+  h->n_wait = 0;
+  h->t += 1;
+  CK(cudaEventRecord(h->ev_t0, h->user));
+  CK(cudaEventRecord(h->ev_in, h->user));
+  CK(cudaStreamWaitEvent(h->s_comp, h->ev_in, 0));
+  CK(cudaStreamWaitEvent(h->s_comm, h->ev_in, 0));
+  const int64_t act = (int64_t)c.N * c.M * c.d;
+  if (host_inputs) {
+    if (need_x) CK(cudaMemcpyAsync(h->xin, x, act * sizeof(float), cudaMemcpyHostToDevice, h->s_comp));
+    if (need_t) CK(cudaMemcpyAsync(h->tin, T, act * sizeof(float), cudaMemcpyHostToDevice, h->s_comp));
+    x = need_x ? h->xin : nullptr;
+    T = need_t ? h->tin : nullptr;
+  }
+  CK(cudaMemsetAsync(h->loss_dev, 0, (c.N + 8) * sizeof(double), h->s_comp));
+  CK(cudaEventRecord(h->ev_fwd_end, h->s_comp));   // re-recorded at the forward/backward boundary (LAYERED)
+  if (c.layered) step_layered(h, x, T);
+  else step_standard(h, x, T);
+  // global loss: sum of this rank's micro-batch losses (slots 1..N), all-reduced, / (D N)
+  mse_finish(h->loss_dev + 1, c.N, 1.0, h->loss_dev, h->s_comp);
+  KCHECK();
+  h->last.allreduce_calls = 1;
+  if (h->world > 1 && !c.no_comm) NK(ncclAllReduce(h->loss_dev, h->loss_dev, 1, ncclFloat64, ncclSum, h->world_comm, h->s_comp));
+  CK(cudaMemcpyAsync(h->loss_host, h->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, h->s_comp));
+  CK(cudaEventRecord(h->ev_comp_end, h->s_comp));
+  CK(cudaEventRecord(h->ev_comm_end, h->s_comm));
+  CK(cudaStreamWaitEvent(h->user, h->ev_comp_end, 0));
+  CK(cudaStreamWaitEvent(h->user, h->ev_comm_end, 0));
+  CK(cudaEventRecord(h->ev_t1, h->user));
+  h->last.steps = 1;
+  lga_comm_stats& tt = h->total;
+  tt.steps += 1;
+  tt.ag_calls += h->last.ag_calls; tt.rs_calls += h->last.rs_calls; tt.p2p_send_calls += h->last.p2p_send_calls;
+  tt.p2p_recv_calls += h->last.p2p_recv_calls; tt.allreduce_calls += h->last.allreduce_calls;
+  tt.ag_bytes += h->last.ag_bytes; tt.rs_bytes += h->last.rs_bytes; tt.p2p_send_bytes += h->last.p2p_send_bytes;
+  tt.p2p_recv_bytes += h->last.p2p_recv_bytes; tt.fwd_units += h->last.fwd_units; tt.bwd_units += h->last.bwd_units;
+  tt.recompute_units += h->last.recompute_units;
+  if (loss_out) {
+    CK(cudaEventSynchronize(h->ev_t1));
+    *loss_out = h->loss_host[0] / ((double)c.D * (double)c.N);
+  }
+  return LGA_OK;
+  ABI_CATCH
+}
+
+lga_status lga_step(lga_handle* h, const float* x, const float* target, double* loss_out) {
+  return run_step(h, x, target, loss_out, false);
+}
+
+lga_status lga_step_host(lga_handle* h, const float* x, const float* target, double* loss_out) {
+  return run_step(h, x, target, loss_out, true);
+}
+
+static lga_status gather_state(lga_handle* h, const float* src_shards, float* out, uint64_t n, int32_t on_device) {
+  if (!h) return ERR(LGA_ERR_INVALID_ARG, "handle is NULL");
+  if (h->bad) return ERR(LGA_ERR_BAD_STATE, "handle latched");
+  const Cfg& c = h->c;
+  const uint64_t expect = (uint64_t)c.Lloc * c.pl;
+  if (n != expect) return ERR(LGA_ERR_SIZE_MISMATCH, "n = %llu, expected %llu", (unsigned long long)n, (unsigned long long)expect);
+  if (!out) return ERR(LGA_ERR_INVALID_ARG, "out is NULL");
+  ABI_TRY
+  CK(cudaSetDevice(h->dev));
+  CK(cudaStreamSynchronize(h->s_comp));
+  CK(cudaStreamSynchronize(h->s_comm));
+  float* full = nullptr;
+  CK(cudaMalloc(&full, (size_t)c.Lloc * c.plpad * sizeof(float)));
+  for (int j = 0; j < c.Lloc; ++j) {
+    const float* shard = src_shards + (int64_t)j * c.S;
+    float* dst = full + (int64_t)j * c.plpad;
+    if (c.D > 1) {
+      NK(ncclAllGather(shard, dst, (size_t)c.S, ncclFloat32, h->dp_comm, h->s_comp));
+    } else {
+      CK(cudaMemcpyAsync(dst, shard, (size_t)c.S * sizeof(float), cudaMemcpyDeviceToDevice, h->s_comp));
+    }
+  }
+  for (int j = 0; j < c.Lloc; ++j) {
+    CK(cudaMemcpyAsync(out + (int64_t)j * c.pl, full + (int64_t)j * c.plpad, (size_t)c.pl * sizeof(float),
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->s_comp));
+  }
+  CK(cudaStreamSynchronize(h->s_comp));
+  CK(cudaFree(full));
+  return LGA_OK;
+  ABI_CATCH
+}
+
+lga_status lga_grads(lga_handle* h, float* out, uint64_t n, int32_t out_on_device) {
+  if (h && !h->c.retain) return ERR(LGA_ERR_INVALID_ARG, "retain_grads was 0 at lga_init");
+  return gather_state(h, h ? h->gkeep : nullptr, out, n, out_on_device);
+}
+
+lga_status lga_params(lga_handle* h, float* out, uint64_t n, int32_t out_on_device) {
+  return gather_state(h, h ? h->master : nullptr, out, n, out_on_device);
+}
+
+lga_status lga_comm_bytes(const lga_handle* h, lga_comm_stats* last_step, lga_comm_stats* total) {
+  if (!h) return ERR(LGA_ERR_INVALID_ARG, "handle is NULL");
+  if (last_step) *last_step = h->last;
+  if (total) *total = h->total;
+  return LGA_OK;
+}
+
+lga_status lga_layer_stage(const lga_handle* h, int32_t* stage_of_layer, int32_t n) {
+  if (!h || !stage_of_layer) return ERR(LGA_ERR_INVALID_ARG, "NULL argument");
+  if (n != h->c.L) return ERR(LGA_ERR_SIZE_MISMATCH, "n = %d, expected L = %d", n, h->c.L);
+  for (int i = 0; i < n; ++i) stage_of_layer[i] = i % h->c.P;
+  return LGA_OK;
+}
+
+lga_status lga_timing_last(lga_handle* h, lga_timing* out) {
+  if (!h || !out) return ERR(LGA_ERR_INVALID_ARG, "NULL argument");
+  if (h->bad) return ERR(LGA_ERR_BAD_STATE, "handle latched");
+  ABI_TRY
+  CK(cudaEventSynchronize(h->ev_t1));
+  lga_timing t{};
+  CK(cudaEventElapsedTime(&t.step_ms, h->ev_t0, h->ev_t1));
+  for (int k = 0; k < h->n_wait; ++k) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev_wait0[k], h->ev_wait1[k]));
+    if (h->wait_kind[k] == 0) t.comm_wait_ms += ms; else t.p2p_wait_ms += ms;
+  }
+  CK(cudaEventElapsedTime(&t.fwd_ms, h->ev_t0, h->ev_fwd_end));
+  CK(cudaEventElapsedTime(&t.bwd_ms, h->ev_fwd_end, h->ev_t1));
+  *out = t;
+  return LGA_OK;
+  ABI_CATCH
+}
+
+void lga_destroy(lga_handle* h) { free_handle(h); }
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+// test_hooks.cu -- extern "C" wrappers of single kernels for tests/ (include/lga_testing.h).
+#include "../../include/lga_testing.h"
+#include "kernels.cuh"
+
+#include <cmath>
+
+using namespace lga;
+
+extern "C" int lgatest_gemm(int path, int M, int N, int K, const void* A, int64_t lda, int a_kmajor, const void* B,
+                            int64_t ldb, int b_kmajor, int kind, const void* bias, int bias_dt, const float* res,
+                            const float* acc_in, void* aux, int aux_dt, void* out, int64_t ldo, int out_dt,
+                            uintptr_t stream) {
+  GemmArgs g;
+  g.M = M; g.N = N; g.K = K;
+  g.A = A; g.lda = lda; g.a_kmajor = a_kmajor != 0;
+  g.B = B; g.ldb = ldb; g.b_kmajor = b_kmajor != 0;
+  g.epi.kind = kind;
+  g.epi.bias = bias; g.epi.bias_dt = (DT)bias_dt;
+  g.epi.res = res; g.epi.ldr = ldo;
+  g.epi.acc_in = acc_in; g.epi.ldacc = ldo;
+  g.epi.aux = aux; g.epi.ldaux = ldo; g.epi.aux_dt = (DT)aux_dt;
+  g.epi.out = out; g.epi.ldo = ldo; g.epi.out_dt = (DT)out_dt;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (path == 0) {
+    gemm_f32_simt(g, st);
+    return (int)cudaGetLastError();
+  }
+  return (int)gemm_bf16_tc(g, st);
+}
+
+static AttnArgs mk(int nseq, int seq, int heads, int dh, int causal) {
+  AttnArgs a;
+  a.nseq = nseq; a.seq = seq; a.heads = heads; a.dh = dh; a.d = heads * dh; a.causal = causal != 0;
+  a.scale = 1.0f / sqrtf((float)dh);
+  return a;
+}
+
+extern "C" int lgatest_attn_fwd(int path, int nseq, int seq, int heads, int dh, int causal, const void* qkv, void* o,
+                                float* lse, uintptr_t stream) {
+  AttnArgs a = mk(nseq, seq, heads, dh, causal);
+  a.qkv = qkv; a.o = o; a.lse = lse;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (path == 0) attn_fwd_f32(a, st); else attn_fwd_bf16(a, st);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int lgatest_attn_bwd(int path, int nseq, int seq, int heads, int dh, int causal, const void* qkv,
+                                const void* o, const float* lse, const void* dO, float* dsum, void* dqkv,
+                                uintptr_t stream) {
+  AttnArgs a = mk(nseq, seq, heads, dh, causal);
+  a.qkv = qkv; a.o = (void*)o; a.lse = (float*)lse; a.dO = dO; a.dsum = dsum; a.dqkv = dqkv;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (path == 0) attn_bwd_f32(a, st); else attn_bwd_bf16(a, st);
+  return (int)cudaGetLastError();
+}

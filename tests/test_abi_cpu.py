@@ -1,0 +1,74 @@
+"""CPU-only checks of the boundary: liblga.so loads, exports every symbol include/lga.h
+declares, and its host-only entry points behave (no GPU compute is called here)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_symbols():
+    txt = open(os.path.join(ROOT, "include", "lga.h")).read()
+    return sorted(set(re.findall(r"^(?:const )?[a-z_0-9]+\*? *\*?(lga_[a-z_]+)\(", txt, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2106_02679_b200 import _abi
+    L = _abi.lib()
+    declared = _header_symbols()
+    assert "lga_init" in declared and "lga_step" in declared and "lga_grads" in declared and "lga_comm_bytes" in declared
+    for name in declared:
+        assert hasattr(L, name), name
+    assert sorted(_abi.EXPORTED) == declared
+
+
+def test_struct_layout_matches_header():
+    from paper_2106_02679_b200 import _abi
+    # lga_config: 1 uint32 + 13 int32 + 6 float + 1 int32 + 1 uint32 = 22 * 4 bytes
+    assert C.sizeof(_abi.lga_config) == 22 * 4
+    assert C.sizeof(_abi.lga_comm_stats) == 13 * 8
+    assert C.sizeof(_abi.lga_timing) == 5 * 4
+
+
+def test_param_count_host_only():
+    from paper_2106_02679_b200 import Config
+    assert Config(layers=2, d_model=4, heads=1, seq_len=32, micro_batch=1, n_micro=1).param_count() == (244, 488)
+    assert Config(layers=24, d_model=2048, heads=16, seq_len=2048, micro_batch=1, n_micro=16).param_count()[1] \
+        == 1_208_598_528
+
+
+def test_invalid_configs_rejected_without_side_effects():
+    from paper_2106_02679_b200 import Config, _abi
+    L = _abi.lib()
+    cases = [
+        (dict(d_model=65, heads=4), 1),                       # d % heads
+        (dict(layers=3, pp=2, dp=1), 1),                      # L % P
+        (dict(ffn_mult=3), 2),                                # n_I must be 4
+        (dict(precision=1, d_model=96, heads=3), 2),          # bf16 head size 32 unsupported
+        (dict(schedule=1, pp=2, layers=4, n_micro=4), 1),     # STANDARD needs P = 1
+        (dict(chunk=3), 1),                                   # N % chunk
+    ]
+    for kw, status in cases:
+        base = dict(layers=2, d_model=64, heads=4, seq_len=32, micro_batch=2, n_micro=4, precision=0)
+        base.update(kw)
+        cfg = Config(**base)
+        h = C.c_void_p()
+        world = cfg.dp * cfg.pp
+        nid = C.create_string_buffer(128) if world > 1 else None
+        st = L.lga_init(C.byref(cfg.to_c()), 0, world, 0, nid, None, None, 0, C.byref(h))
+        assert st == status, (kw, st, L.lga_last_error())
+        assert not h.value
+    # world mismatch
+    cfg = Config(layers=2, d_model=64, heads=4, seq_len=32, micro_batch=2, n_micro=4, dp=2)
+    h = C.c_void_p()
+    assert L.lga_init(C.byref(cfg.to_c()), 0, 3, 0, C.create_string_buffer(128), None, None, 0, C.byref(h)) == 1
+    assert b"world" in L.lga_last_error()
+
+
+def test_status_strings():
+    from paper_2106_02679_b200 import _abi
+    L = _abi.lib()
+    for k, v in _abi.STATUS.items():
+        assert L.lga_status_string(k).decode() == v

@@ -1,0 +1,160 @@
+"""Single-kernel numerics through the test hooks (include/lga_testing.h) against a plain
+PyTorch fp32 reference of the same op: the tcgen05 GEMM in every operand-major combination
+and epilogue, the SIMT fp32 GEMM, and attention forward / backward."""
+import ctypes as C
+import math
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2106_02679_b200 import _abi  # noqa: E402
+
+L = _abi.lib()
+L.lgatest_gemm.restype = C.c_int
+L.lgatest_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64,
+                           C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                           C.c_void_p, C.c_int64, C.c_int, C.c_void_p]
+L.lgatest_attn_fwd.restype = C.c_int
+L.lgatest_attn_fwd.argtypes = [C.c_int] * 6 + [C.c_void_p] * 3 + [C.c_void_p]
+L.lgatest_attn_bwd.restype = C.c_int
+L.lgatest_attn_bwd.argtypes = [C.c_int] * 6 + [C.c_void_p] * 6 + [C.c_void_p]
+
+
+def P(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def DT(t):
+    return 0 if t is None or t.dtype == torch.float32 else 1
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def gemm(path, A, a_kmajor, B, b_kmajor, M, N, K, out, kind=0, bias=None, res=None, acc_in=None, aux=None):
+    lda = A.shape[1]
+    ldb = B.shape[1]
+    r = L.lgatest_gemm(path, M, N, K, P(A), lda, int(a_kmajor), P(B), ldb, int(b_kmajor), kind, P(bias), DT(bias),
+                       P(res), P(acc_in), P(aux), DT(aux), P(out), out.shape[1], DT(out), stream())
+    assert r == 0, f"cuda error {r}"
+    torch.cuda.synchronize()
+
+
+def logical(A, kmajor):
+    """A(m,k) as a dense fp32 [M][K] tensor."""
+    return A.float() if kmajor else A.float().t()
+
+
+def relerr(a, b):
+    return ((a.double() - b.double()).norm() / b.double().norm()).item()
+
+
+SHAPES = [(128, 128, 64), (256, 512, 256), (200, 328, 136), (1000, 768, 768), (64, 2304, 4096), (4096, 256, 1000)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("amaj", [True, False])
+@pytest.mark.parametrize("bmaj", [True, False])
+def test_tc_gemm_store_f32(M, N, K, amaj, bmaj):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
+    A = torch.randn((M, K) if amaj else (K, M), device="cuda", generator=g).bfloat16()
+    B = torch.randn((N, K) if bmaj else (K, N), device="cuda", generator=g).bfloat16()
+    out = torch.full((M, N), float("nan"), device="cuda")
+    gemm(1, A, amaj, B, bmaj, M, N, K, out)
+    ref = logical(A, amaj) @ logical(B, bmaj).t()
+    assert relerr(out, ref) < 1e-5
+
+
+@pytest.mark.parametrize("kind", ["bias_bf16", "bias_res_acc", "gelu_fwd", "gelu_bwd"])
+def test_tc_gemm_epilogues(kind):
+    M, N, K = 520, 384, 192
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = torch.randn(K, N, device="cuda", generator=g).bfloat16()      # MN-major B (forward form)
+    bias = torch.randn(N, device="cuda", generator=g).bfloat16()
+    acc = A.float() @ B.float()
+    if kind == "bias_bf16":
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        gemm(1, A, True, B, False, M, N, K, out, bias=bias)
+        ref = acc + bias.float()
+        assert relerr(out.float(), ref) < 5e-3
+    elif kind == "bias_res_acc":
+        res = torch.randn(M, N, device="cuda", generator=g)
+        acc_in = torch.randn(M, N, device="cuda", generator=g)
+        out = torch.empty(M, N, device="cuda")
+        gemm(1, A, True, B, False, M, N, K, out, bias=bias, res=res, acc_in=acc_in)
+        ref = acc + bias.float() + res + acc_in
+        assert relerr(out, ref) < 1e-5
+    elif kind == "gelu_fwd":
+        u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        gemm(1, A, True, B, False, M, N, K, out, kind=1, bias=bias, aux=u)
+        uref = acc + bias.float()
+        assert relerr(u.float(), uref) < 5e-3
+        assert relerr(out.float(), torch.nn.functional.gelu(uref)) < 5e-3
+    else:
+        u = (torch.randn(M, N, device="cuda", generator=g) * 2).bfloat16()
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        gemm(1, A, True, B, False, M, N, K, out, kind=2, aux=u)
+        uf = u.float().requires_grad_(True)
+        gl = torch.autograd.grad(torch.nn.functional.gelu(uf).sum(), uf)[0]
+        assert relerr(out.float(), acc * gl) < 5e-3
+
+
+@pytest.mark.parametrize("amaj,bmaj", [(True, True), (True, False), (False, False)])
+def test_simt_gemm_f32(amaj, bmaj):
+    M, N, K = 131, 77, 93
+    g = torch.Generator(device="cuda").manual_seed(2)
+    A = torch.randn((M, K) if amaj else (K, M), device="cuda", generator=g)
+    B = torch.randn((N, K) if bmaj else (K, N), device="cuda", generator=g)
+    bias = torch.randn(N, device="cuda", generator=g)
+    out = torch.empty(M, N, device="cuda")
+    gemm(0, A, amaj, B, bmaj, M, N, K, out, bias=bias)
+    ref = logical(A, amaj) @ logical(B, bmaj).t() + bias
+    assert relerr(out, ref) < 1e-6
+
+
+def _attn_ref(qkv, nseq, s, H, dh, causal):
+    d = H * dh
+    x = qkv.float().view(nseq, s, 3, H, dh).permute(2, 0, 3, 1, 4)
+    q, k, v = x[0], x[1], x[2]
+    return q, k, v
+
+
+@pytest.mark.parametrize("path,dh,s,causal", [(0, 16, 37, 1), (0, 64, 128, 0), (1, 64, 256, 1), (1, 128, 200, 1),
+                                              (1, 128, 512, 0), (1, 64, 1024, 1)])
+def test_attention_fwd_bwd(path, dh, s, causal):
+    nseq, H = 2, 3
+    d = H * dh
+    dt = torch.float32 if path == 0 else torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(3)
+    qkv = torch.randn(nseq * s, 3 * d, device="cuda", generator=g).to(dt)
+    o = torch.empty(nseq * s, d, device="cuda", dtype=dt)
+    lse = torch.empty(nseq, H, s, device="cuda")
+    assert L.lgatest_attn_fwd(path, nseq, s, H, dh, causal, P(qkv), P(o), P(lse), stream()) == 0
+    q, k, v = _attn_ref(qkv, nseq, s, H, dh, causal)
+    q.requires_grad_(True); k.requires_grad_(True); v.requires_grad_(True)
+    ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=bool(causal))
+    ref_o = ref.permute(0, 2, 1, 3).reshape(nseq * s, d)
+    tol = 1e-5 if path == 0 else 1e-2
+    torch.cuda.synchronize()
+    assert relerr(o.float(), ref_o) < tol
+    S = (q @ k.transpose(-1, -2)) / math.sqrt(dh)
+    if causal:
+        S = S.masked_fill(torch.triu(torch.ones(s, s, device="cuda", dtype=torch.bool), 1), float("-inf"))
+    assert relerr(lse, torch.logsumexp(S, -1)) < (1e-6 if path == 0 else 1e-3)
+    dO = torch.randn(nseq * s, d, device="cuda", generator=g).to(dt)
+    dsum = torch.empty(nseq, H, s, device="cuda")
+    dqkv = torch.full((nseq * s, 3 * d), float("nan"), device="cuda", dtype=dt)
+    assert L.lgatest_attn_bwd(path, nseq, s, H, dh, causal, P(qkv), P(o), P(lse), P(dO), P(dsum), P(dqkv), stream()) == 0
+    torch.cuda.synchronize()
+    gq, gk, gv = torch.autograd.grad(ref, (q, k, v), dO.float().view(nseq, s, H, dh).permute(0, 2, 1, 3))
+    pack = lambda t: t.permute(0, 2, 1, 3).reshape(nseq * s, d)
+    got = dqkv.float().view(nseq * s, 3, d)
+    for i, r in enumerate((gq, gk, gv)):
+        assert relerr(got[:, i], pack(r)) < (1e-5 if path == 0 else 2e-2), i

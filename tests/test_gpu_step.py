@@ -1,0 +1,75 @@
+"""Parity of the CUDA step (through the C ABI) with the fp64 oracle, single GPU.
+
+fp32 mode: gradients and updated parameters within 1e-5 relative Frobenius (BASELINE.json
+north star), per layer and globally; counters exact."""
+import numpy as np
+import pytest
+
+import synth
+from gpu_util import oracle_run, per_layer_rel, rel
+from oracle import counters as oc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2106_02679_b200 import LGA_BF16, LGA_FP32, LGA_LAYERED, LGA_STANDARD, Config, Trainer  # noqa: E402
+
+
+def _run(sh, precision=LGA_FP32, schedule=LGA_LAYERED, chunk=0, causal=1, steps=1, lr=1e-3, wd=0.0, style="parity"):
+    init = synth.init_params(sh, style=style)
+    cfg = Config(layers=sh.layers, d_model=sh.d, heads=sh.heads, seq_len=sh.seq, micro_batch=sh.micro_batch,
+                 n_micro=sh.n_micro, precision=precision, schedule=schedule, chunk=chunk, causal=causal, lr=lr,
+                 weight_decay=wd, retain_grads=1)
+    tr = Trainer(cfg, rank=0, world=1, device=0, init_params=init)
+    batches = [synth.batch(sh, step=k) for k in range(steps)]
+    losses = []
+    for X, T in batches:
+        xt = torch.from_numpy(X[0]).cuda()
+        tt = torch.from_numpy(T[0]).cuda()
+        losses.append(tr.step(xt, tt))
+    out = dict(params=tr.params(), grads=tr.grads(), losses=losses, stats=tr.comm_stats()[0], stages=tr.layer_stage(),
+               timing=tr.timing())
+    tr.close()
+    ref_params, ref_losses, ref_grads = oracle_run(sh, init, batches, causal=causal, lr=lr, wd=wd)
+    return out, (ref_params, ref_losses, ref_grads, init)
+
+
+C1 = synth.Shape(layers=2, d=64, heads=4, seq=32, micro_batch=2, n_micro=4)
+
+
+@pytest.mark.parametrize("chunk", [0, 1, 2])
+def test_fp32_c1_layered_parity(chunk):
+    out, (rp, rl, rg, init) = _run(C1, chunk=chunk)
+    assert rel(out["grads"], rg) < 1e-5, per_layer_rel(out["grads"], rg, C1.layers)
+    assert max(per_layer_rel(out["grads"], rg, C1.layers)) < 1e-5
+    assert rel(out["params"], rp) < 1e-5
+    # the update itself, not just the parameters
+    assert rel(out["params"] - init, rp - init) < 1e-4
+    assert abs(out["losses"][0] - rl[0]) < 1e-6 * abs(rl[0])
+    c = oc.comm_counters(oc.StepShape(layers=2, d=64, seq=32, micro_batch=2, n_micro=4), param_bytes=4, grad_bytes=4)
+    for k, v in c.items():
+        assert out["stats"][k] == v, k
+    assert out["stages"] == [0, 0]
+
+
+def test_fp32_standard_schedule_parity():
+    out, (rp, rl, rg, _) = _run(C1, schedule=LGA_STANDARD)
+    assert rel(out["grads"], rg) < 1e-5
+    assert rel(out["params"], rp) < 1e-5
+
+
+def test_fp32_multi_step_weight_decay_noncausal():
+    sh = synth.Shape(layers=2, d=48, heads=3, seq=37, micro_batch=1, n_micro=3)   # ragged tiles, d_h = 16
+    out, (rp, rl, rg, _) = _run(sh, causal=0, steps=3, wd=0.1)
+    assert rel(out["grads"], rg) < 1e-5
+    assert rel(out["params"], rp) < 1e-5
+    np.testing.assert_allclose(out["losses"], rl, rtol=1e-5)
+
+
+def test_fp32_deterministic():
+    a, _ = _run(C1, chunk=2)
+    b, _ = _run(C1, chunk=2)
+    assert np.array_equal(a["grads"], b["grads"]) and np.array_equal(a["params"], b["params"])
