@@ -77,6 +77,8 @@ typedef enum { LGA_LAYERED = 0, LGA_STANDARD = 1 } lga_schedule;
 #define LGA_FLAG_NO_COMM   0x1u  /* debug A/B timing only: skip every collective and p2p
                                     transfer (results are then wrong); counters still count */
 #define LGA_FLAG_NO_GRAPH  0x2u  /* reserved */
+#define LGA_FLAG_PROFILE   0x4u  /* record CUDA events around every GEMM / attention / AdamW launch
+                                    (on the stream it is launched on) for lga_timing_last */
 
 typedef struct {
   uint32_t abi_version;    /* must be LGA_ABI_VERSION */
@@ -115,6 +117,14 @@ typedef struct {
   float comm_wait_ms;     /* sum of compute-stream stalls waiting on DP collectives */
   float p2p_wait_ms;      /* sum of compute-stream stalls waiting on pipeline receives */
   float fwd_ms, bwd_ms;   /* compute-stream time of the forward / backward passes */
+  /* Per kernel family, only with LGA_FLAG_PROFILE (else 0): summed device time of the
+   * launches, launch count, and the ALGORITHMIC work they did (GEMM: 2 M N K flops per
+   * launch; attention: 2 d_h s(s+1) per (sequence, head) forward for the causal triangle,
+   * 2x that backward; AdamW: bytes = (g + 3x4 read + 3x4 written + param) per element). */
+  float gemm_ms, attn_ms, adam_ms;
+  uint32_t gemm_launches, attn_launches, adam_launches;
+  double gemm_flop, attn_flop, adam_bytes;
+  uint64_t kernel_launches;  /* every kernel this library launched in the step (NCCL excluded) */
 } lga_timing;
 
 typedef struct lga_handle lga_handle;

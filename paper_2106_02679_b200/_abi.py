@@ -19,6 +19,7 @@ NCCL_ID_BYTES = 128
 LGA_FP32, LGA_BF16 = 0, 1
 LGA_LAYERED, LGA_STANDARD = 0, 1
 LGA_FLAG_NO_COMM = 0x1
+LGA_FLAG_PROFILE = 0x4
 
 STATUS = {0: "LGA_OK", 1: "LGA_ERR_INVALID_ARG", 2: "LGA_ERR_UNSUPPORTED", 3: "LGA_ERR_OUT_OF_MEMORY",
           4: "LGA_ERR_CUDA", 5: "LGA_ERR_NCCL", 6: "LGA_ERR_SIZE_MISMATCH", 7: "LGA_ERR_BAD_STATE"}
@@ -49,7 +50,11 @@ class lga_comm_stats(C.Structure):
 
 
 class lga_timing(C.Structure):
-    _fields_ = [(n, C.c_float) for n in ("step_ms", "comm_wait_ms", "p2p_wait_ms", "fwd_ms", "bwd_ms")]
+    _fields_ = ([(n, C.c_float) for n in ("step_ms", "comm_wait_ms", "p2p_wait_ms", "fwd_ms", "bwd_ms",
+                                          "gemm_ms", "attn_ms", "adam_ms")]
+                + [(n, C.c_uint32) for n in ("gemm_launches", "attn_launches", "adam_launches")]
+                + [(n, C.c_double) for n in ("gemm_flop", "attn_flop", "adam_bytes")]
+                + [("kernel_launches", C.c_uint64)])
 
     def as_dict(self):
         return {n: float(getattr(self, n)) for n, _ in self._fields_}

@@ -9,6 +9,10 @@
 
 namespace lga {
 
+// host-side count of kernels launched by this library (bench.py's gpu_launches)
+void note_launch();
+unsigned long long launch_count();
+
 enum class DT : int { F32 = 0, BF16 = 1 };
 
 __host__ __device__ inline size_t dt_size(DT t) { return t == DT::F32 ? 4 : 2; }

@@ -518,13 +518,13 @@ void run_fwd(const AttnArgs& a, cudaStream_t st) {
   static bool set = false;
   if (!set) { cudaFuncSetAttribute(fwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); set = true; }
   dim3 grid((a.seq + BQ - 1) / BQ, a.heads, a.nseq);
-  fwd_kernel<DH><<<grid, NT, smem, st>>>(a);
+  note_launch(), fwd_kernel<DH><<<grid, NT, smem, st>>>(a);
 }
 
 template <int DH>
 void run_bwd(const AttnArgs& a, cudaStream_t st) {
   const int64_t rows = (int64_t)a.nseq * a.seq * a.heads;
-  dsum_kernel<DH><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(a);
+  note_launch(), dsum_kernel<DH><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(a);
   const int smem_kv = (2 * BKV + 4 * BQ) * DH * 2 + 4 * BQ * 4;
   const int smem_q = (2 * BQ + 4 * BKV) * DH * 2;
   static bool set = false;
@@ -534,9 +534,9 @@ void run_bwd(const AttnArgs& a, cudaStream_t st) {
     set = true;
   }
   dim3 gk((a.seq + BKV - 1) / BKV, a.heads, a.nseq);
-  dkdv_kernel<DH><<<gk, NT, smem_kv, st>>>(a);
+  note_launch(), dkdv_kernel<DH><<<gk, NT, smem_kv, st>>>(a);
   dim3 gq((a.seq + BQ - 1) / BQ, a.heads, a.nseq);
-  dq_kernel<DH><<<gq, NT, smem_q, st>>>(a);
+  note_launch(), dq_kernel<DH><<<gq, NT, smem_q, st>>>(a);
 }
 
 }  // namespace fa

@@ -180,10 +180,10 @@ __global__ void __launch_bounds__(AQ) attn_dkdv_f32_kernel(AttnArgs a) {
 
 #define ATTN_DISPATCH(KERNEL, grid)                                                     \
   do {                                                                                  \
-    if (a.dh <= 16) KERNEL<16><<<grid, AQ, 0, st>>>(a);                                 \
-    else if (a.dh <= 32) KERNEL<32><<<grid, AQ, 0, st>>>(a);                            \
-    else if (a.dh <= 64) KERNEL<64><<<grid, AQ, 0, st>>>(a);                            \
-    else KERNEL<128><<<grid, AQ, 0, st>>>(a);                                           \
+    if (a.dh <= 16) note_launch(), KERNEL<16><<<grid, AQ, 0, st>>>(a);                                 \
+    else if (a.dh <= 32) note_launch(), KERNEL<32><<<grid, AQ, 0, st>>>(a);                            \
+    else if (a.dh <= 64) note_launch(), KERNEL<64><<<grid, AQ, 0, st>>>(a);                            \
+    else note_launch(), KERNEL<128><<<grid, AQ, 0, st>>>(a);                                           \
   } while (0)
 
 void attn_fwd_f32(const AttnArgs& a, cudaStream_t st) {
@@ -195,7 +195,7 @@ void attn_fwd_f32(const AttnArgs& a, cudaStream_t st) {
 void attn_bwd_f32(const AttnArgs& a, cudaStream_t st) {
   if (a.nseq <= 0) return;
   const int64_t rows = (int64_t)a.nseq * a.heads * a.seq;
-  attn_dsum_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(a);
+  note_launch(), attn_dsum_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(a);
   dim3 grid((a.seq + AQ - 1) / AQ, a.heads, a.nseq);
   ATTN_DISPATCH(attn_dq_f32_kernel, grid);
   ATTN_DISPATCH(attn_dkdv_f32_kernel, grid);

@@ -4,6 +4,7 @@
 // bitwise reproducible.
 #include "kernels.cuh"
 
+#include <atomic>
 #include <cmath>
 
 namespace lga {
@@ -51,7 +52,7 @@ void ln_fwd(const float* x, const void* gamma, const void* beta, DT pdt, void* y
   if (rows <= 0) return;
   const int bd = d >= 1024 ? 256 : (d >= 256 ? 128 : 64);
   const int vpt = (d + bd - 1) / bd;
-#define LNF(V) ln_fwd_kernel<V><<<rows, bd, 0, st>>>(x, gamma, beta, pdt, y, ydt, stats, d, eps)
+#define LNF(V) note_launch(), ln_fwd_kernel<V><<<rows, bd, 0, st>>>(x, gamma, beta, pdt, y, ydt, stats, d, eps)
   if (vpt <= 1) LNF(1); else if (vpt <= 2) LNF(2); else if (vpt <= 4) LNF(4);
   else if (vpt <= 8) LNF(8); else if (vpt <= 16) LNF(16); else LNF(32);
 #undef LNF
@@ -129,7 +130,7 @@ int ln_bwd(const float* dout, const float* x, const float2* stats, const void* g
   if (rows <= 0) return 0;
   const int bd = d >= 1024 ? 256 : (d >= 256 ? 128 : 64);
   const int vpt = (d + bd - 1) / bd;
-#define LNB(V) ln_bwd_kernel<V><<<nblk, bd, 0, st>>>(dout, x, stats, gamma, pdt, resid, dx, dx_e, edt, partial, rows, d)
+#define LNB(V) note_launch(), ln_bwd_kernel<V><<<nblk, bd, 0, st>>>(dout, x, stats, gamma, pdt, resid, dx, dx_e, edt, partial, rows, d)
   if (vpt <= 1) LNB(1); else if (vpt <= 2) LNB(2); else if (vpt <= 4) LNB(4);
   else if (vpt <= 8) LNB(8); else if (vpt <= 16) LNB(16); else LNB(32);
 #undef LNB
@@ -154,7 +155,7 @@ int colsum_partial(const void* X, DT xdt, int64_t ldx, int rows, int n, float* p
   const int nblk = colsum_blocks(rows);
   if (rows <= 0 || n <= 0) return 0;
   dim3 grid((n + 255) / 256, nblk);
-  colsum_partial_kernel<<<grid, 256, 0, st>>>(X, xdt, ldx, rows, n, partial);
+  note_launch(), colsum_partial_kernel<<<grid, 256, 0, st>>>(X, xdt, ldx, rows, n, partial);
   return nblk;
 }
 
@@ -171,7 +172,7 @@ __global__ void colsum_finish_kernel(const float* __restrict__ partial, int nblk
 void colsum_finish(const float* partial, int nblk, int64_t pstride, int n, const float* acc_in,
                    void* out, DT out_dt, cudaStream_t st) {
   if (n <= 0) return;
-  colsum_finish_kernel<<<(n + 255) / 256, 256, 0, st>>>(partial, nblk, pstride, n, acc_in, out, out_dt);
+  note_launch(), colsum_finish_kernel<<<(n + 255) / 256, 256, 0, st>>>(partial, nblk, pstride, n, acc_in, out, out_dt);
 }
 
 // =============================================================== MSE loss + seed gradient
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(MSE_THREADS) mse_kernel(const float* __restric
 void mse_fwd_bwd(const float* y, const float* T, float* dY, double* partial, int64_t n,
                  float inv_numel_mb, cudaStream_t st) {
   if (n <= 0) return;
-  mse_kernel<<<mse_blocks(n), MSE_THREADS, 0, st>>>(y, T, dY, partial, n, inv_numel_mb);
+  note_launch(), mse_kernel<<<mse_blocks(n), MSE_THREADS, 0, st>>>(y, T, dY, partial, n, inv_numel_mb);
 }
 
 __global__ void mse_finish_kernel(const double* partial, int nblk, double scale, double* out) {
@@ -218,7 +219,7 @@ __global__ void mse_finish_kernel(const double* partial, int nblk, double scale,
 }
 
 void mse_finish(const double* partial, int nblk, double scale, double* out, cudaStream_t st) {
-  mse_finish_kernel<<<1, 32, 0, st>>>(partial, nblk, scale, out);
+  note_launch(), mse_finish_kernel<<<1, 32, 0, st>>>(partial, nblk, scale, out);
 }
 
 // =============================================================== AdamW
@@ -249,7 +250,7 @@ void adamw(const void* gin, DT gdt, float gscale, float* master, float* m, float
            float eps, float wd, float bc1, float bc2, cudaStream_t st) {
   if (n <= 0) return;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
-#define AD(GE, PE) adamw_kernel<GE, PE><<<grid, 256, 0, st>>>((const GE*)gin, gscale, master, m, v, (PE*)param_out, keep, n, lr, beta1, beta2, eps, wd, bc1, bc2)
+#define AD(GE, PE) note_launch(), adamw_kernel<GE, PE><<<grid, 256, 0, st>>>((const GE*)gin, gscale, master, m, v, (PE*)param_out, keep, n, lr, beta1, beta2, eps, wd, bc1, bc2)
   if (gdt == DT::F32 && pdt == DT::F32) AD(float, float);
   else if (gdt == DT::F32) AD(float, __nv_bfloat16);
   else if (pdt == DT::F32) AD(__nv_bfloat16, float);
@@ -264,7 +265,7 @@ __global__ void shard_acc_kernel(const void* g, DT gdt, float* acc, int64_t n, b
 void shard_accumulate(const void* g, DT gdt, float* acc, int64_t n, bool first, cudaStream_t st) {
   if (n <= 0) return;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
-  shard_acc_kernel<<<grid, 256, 0, st>>>(g, gdt, acc, n, first);
+  note_launch(), shard_acc_kernel<<<grid, 256, 0, st>>>(g, gdt, acc, n, first);
 }
 
 // =============================================================== casts / fills
@@ -275,7 +276,7 @@ __global__ void cast_kernel(const float* __restrict__ x, void* y, DT ydt, int64_
 void cast_f32(const float* x, void* y, DT ydt, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
-  cast_kernel<<<grid, 256, 0, st>>>(x, y, ydt, n);
+  note_launch(), cast_kernel<<<grid, 256, 0, st>>>(x, y, ydt, n);
 }
 __global__ void to_f32_kernel(const void* x, DT xdt, float* y, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -284,7 +285,7 @@ __global__ void to_f32_kernel(const void* x, DT xdt, float* y, int64_t n) {
 void copy_to_f32(const void* x, DT xdt, float* y, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
-  to_f32_kernel<<<grid, 256, 0, st>>>(x, xdt, y, n);
+  note_launch(), to_f32_kernel<<<grid, 256, 0, st>>>(x, xdt, y, n);
 }
 __global__ void fill_kernel(float* p, float v, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
@@ -292,7 +293,7 @@ __global__ void fill_kernel(float* p, float v, int64_t n) {
 void fill_f32(float* p, float v, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
-  fill_kernel<<<grid, 256, 0, st>>>(p, v, n);
+  note_launch(), fill_kernel<<<grid, 256, 0, st>>>(p, v, n);
 }
 
 // =============================================================== seeded device init
@@ -339,7 +340,7 @@ void init_params_device(float* out, int64_t n_layers, int d, int ffn_mult, int L
   const int64_t n = n_layers * pl;
   if (n <= 0) return;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
-  init_kernel<<<grid, 256, 0, st>>>(out, n, pl, d, (int)f, L_total, first_layer, seed);
+  note_launch(), init_kernel<<<grid, 256, 0, st>>>(out, n, pl, d, (int)f, L_total, first_layer, seed);
 }
 
 // =============================================================== pipeline flags
@@ -352,15 +353,19 @@ __global__ void wait_flag_kernel(const volatile unsigned long long* flag, unsign
   }
 }
 void wait_flag(const volatile unsigned long long* flag, unsigned long long target, cudaStream_t st) {
-  wait_flag_kernel<<<1, 1, 0, st>>>(flag, target);
+  note_launch(), wait_flag_kernel<<<1, 1, 0, st>>>(flag, target);
 }
 __global__ void set_flag_kernel(unsigned long long* flag, unsigned long long value) {
   __threadfence_system();
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
 }
 void set_flag(unsigned long long* flag, unsigned long long value, cudaStream_t st) {
-  set_flag_kernel<<<1, 1, 0, st>>>(flag, value);
+  note_launch(), set_flag_kernel<<<1, 1, 0, st>>>(flag, value);
 }
+
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 int num_sms() {
   static int n = 0;

@@ -69,7 +69,7 @@ struct Cfg {
   bool bf16, layered, causal;
   DT E, G;      // compute storage type; reduce-scatter / gradient staging type
   float lr, b1, b2, eps, wd, ln_eps;
-  bool retain, no_comm;
+  bool retain, no_comm, profile;
   // canonical offsets
   int64_t o_ln1w, o_ln1b, o_wqkv, o_bqkv, o_wo, o_bo, o_ln2w, o_ln2b, o_w1, o_b1, o_w2, o_b2;
 };
@@ -119,6 +119,7 @@ static lga_status validate(const lga_config* c, int world, Cfg* out) {
   g.lr = c->lr; g.b1 = c->beta1; g.b2 = c->beta2; g.eps = c->adam_eps; g.wd = c->weight_decay; g.ln_eps = c->ln_eps;
   g.retain = c->retain_grads != 0;
   g.no_comm = (c->flags & LGA_FLAG_NO_COMM) != 0;
+  g.profile = (c->flags & LGA_FLAG_PROFILE) != 0;
   const int64_t d = g.d, f = g.f;
   g.o_ln1w = 0; g.o_ln1b = d; g.o_wqkv = 2 * d; g.o_bqkv = g.o_wqkv + 3 * d * d; g.o_wo = g.o_bqkv + 3 * d;
   g.o_bo = g.o_wo + d * d; g.o_ln2w = g.o_bo + d; g.o_ln2b = g.o_ln2w + d; g.o_w1 = g.o_ln2b + d;
@@ -193,6 +194,12 @@ struct lga_handle {
   std::vector<cudaEvent_t> ev_wait0, ev_wait1;   // stall accounting pairs (s_comp)
   std::vector<int> wait_kind;
   int n_wait = 0;
+  // per-family profiling (LGA_FLAG_PROFILE): event pairs on the launching stream
+  std::vector<cudaEvent_t> prof0, prof1;
+  std::vector<int> prof_fam;
+  std::vector<double> prof_work;
+  int n_prof = 0;
+  unsigned long long launches_at_start = 0, launches_last = 0;
   int64_t t = 0;  // AdamW step counter
   lga_comm_stats last{}, total{};
 };
@@ -257,15 +264,47 @@ static void plan_arena(lga_handle* h) {
   h->flags = A.take<unsigned long long>(8);
 }
 
+// ------------------------------------------------------------------ profiling
+enum { FAM_GEMM = 0, FAM_ATTN = 1, FAM_ADAM = 2 };
+static int prof_begin(lga_handle* h, cudaStream_t st) {
+  if (!h->c.profile) return -1;
+  if (h->n_prof >= (int)h->prof0.size()) {
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    h->prof0.push_back(a);
+    h->prof1.push_back(b);
+    h->prof_fam.push_back(0);
+    h->prof_work.push_back(0.0);
+  }
+  CK(cudaEventRecord(h->prof0[h->n_prof], st));
+  return h->n_prof++;
+}
+static void prof_end(lga_handle* h, int idx, cudaStream_t st, int fam, double work) {
+  if (idx < 0) return;
+  CK(cudaEventRecord(h->prof1[idx], st));
+  h->prof_fam[idx] = fam;
+  h->prof_work[idx] = work;
+}
+
 // ------------------------------------------------------------------ GEMM dispatch
 static void gemm(lga_handle* h, GemmArgs g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
+  const int p = prof_begin(h, st);
   if (h->c.bf16) {
     CK(gemm_bf16_tc(g, st));
   } else {
     gemm_f32_simt(g, st);
   }
   KCHECK();
+  prof_end(h, p, st, FAM_GEMM, 2.0 * g.M * (double)g.N * g.K);
+}
+
+// algorithmic attention flops of one forward over nseq sequences (causal triangle incl. diagonal)
+static double attn_flops_fwd(const Cfg& c, int nseq) {
+  const double s = c.s;
+  const double pairs = c.causal ? s * (s + 1) / 2 : s * s;
+  return 4.0 * c.dh * pairs * c.H * nseq;
 }
 
 // Gradient write mode of one chunk (reading A-3, subsystem (2)): where the chunk's gradient goes.
@@ -312,8 +351,10 @@ static void layer_fwd(lga_handle* h, const void* W, const float* x_in, float* y_
     a.nseq = c.c * c.b; a.seq = c.s; a.heads = c.H; a.dh = c.dh; a.d = d; a.causal = c.causal;
     a.scale = 1.0f / sqrtf((float)c.dh);
     a.qkv = h->qkv; a.o = h->o; a.lse = h->lse;
+    const int p = prof_begin(h, st);
     if (c.bf16) attn_fwd_bf16(a, st); else attn_fwd_f32(a, st);
     KCHECK();
+    prof_end(h, p, st, FAM_ATTN, attn_flops_fwd(c, a.nseq));
   }
   {  // h1 = x + o Wo + bo
     GemmArgs g;
@@ -436,8 +477,10 @@ static void layer_bwd(lga_handle* h, const void* W, const float* x_in, const flo
     a.nseq = c.c * c.b; a.seq = c.s; a.heads = c.H; a.dh = c.dh; a.d = d; a.causal = c.causal;
     a.scale = 1.0f / sqrtf((float)c.dh);
     a.qkv = h->qkv; a.o = h->o; a.lse = h->lse; a.dO = h->dO; a.dsum = h->dsum; a.dqkv = h->dqkv;
+    const int p = prof_begin(h, st);
     if (c.bf16) attn_bwd_bf16(a, st); else attn_bwd_f32(a, st);
     KCHECK();
+    prof_end(h, p, st, FAM_ATTN, 2.0 * attn_flops_fwd(c, a.nseq));
   }
   // ---- QKV: qkv = a Wqkv + bqkv
   wgrad(h, h->a, d, h->dqkv, 3 * d, d, 3 * d, T, dst(c.o_wqkv), c.o_wqkv, st);
@@ -503,9 +546,12 @@ static void adam_layer(lga_handle* h, int j, const void* g, DT gdt) {
   const float bc1 = 1.0f - powf(c.b1, (float)h->t), bc2 = 1.0f - powf(c.b2, (float)h->t);
   const float gscale = 1.0f / ((float)c.D * (float)c.N);   // gradient of the mean loss (A-3)
   const int64_t off = (int64_t)j * c.S;
+  const int p = prof_begin(h, h->s_comm);
   adamw(g, gdt, gscale, h->master + off, h->mom + off, h->var + off, eoff(h->pshard, c.E, off), c.E,
         c.retain ? h->gkeep + off : nullptr, c.S, c.lr, c.b1, c.b2, c.eps, c.wd, bc1, bc2, h->s_comm);
   KCHECK();
+  const double per = (double)dt_size(gdt) + 24.0 + (double)dt_size(c.E) + (c.retain ? 4.0 : 0.0);
+  prof_end(h, p, h->s_comm, FAM_ADAM, per * (double)c.S);
 }
 
 // reduce-scatter of the staged gradient in place (once per layer per step); returns the shard
@@ -949,6 +995,8 @@ static lga_status run_step(lga_handle* h, const float* x, const float* T, double
   CK(cudaSetDevice(h->dev));
   h->last = lga_comm_stats{};
   h->n_wait = 0;
+  h->n_prof = 0;
+  h->launches_at_start = launch_count();
   h->t += 1;
   CK(cudaEventRecord(h->ev_t0, h->user));
   CK(cudaEventRecord(h->ev_in, h->user));
@@ -976,6 +1024,7 @@ static lga_status run_step(lga_handle* h, const float* x, const float* T, double
   CK(cudaStreamWaitEvent(h->user, h->ev_comp_end, 0));
   CK(cudaStreamWaitEvent(h->user, h->ev_comm_end, 0));
   CK(cudaEventRecord(h->ev_t1, h->user));
+  h->launches_last = launch_count() - h->launches_at_start;
   h->last.steps = 1;
   lga_comm_stats& tt = h->total;
   tt.steps += 1;
@@ -1069,6 +1118,16 @@ lga_status lga_timing_last(lga_handle* h, lga_timing* out) {
   }
   CK(cudaEventElapsedTime(&t.fwd_ms, h->ev_t0, h->ev_fwd_end));
   CK(cudaEventElapsedTime(&t.bwd_ms, h->ev_fwd_end, h->ev_t1));
+  for (int k = 0; k < h->n_prof; ++k) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->prof0[k], h->prof1[k]));
+    switch (h->prof_fam[k]) {
+      case FAM_GEMM: t.gemm_ms += ms; t.gemm_launches++; t.gemm_flop += h->prof_work[k]; break;
+      case FAM_ATTN: t.attn_ms += ms; t.attn_launches++; t.attn_flop += h->prof_work[k]; break;
+      default: t.adam_ms += ms; t.adam_launches++; t.adam_bytes += h->prof_work[k]; break;
+    }
+  }
+  t.kernel_launches = h->launches_last;
   *out = t;
   return LGA_OK;
   ABI_CATCH
