@@ -541,7 +541,7 @@ void run_bwd(const AttnArgs& a, cudaStream_t st) {
 
 }  // namespace fa
 
-void attn_fwd_bf16(const AttnArgs& a, cudaStream_t st) {
+void attn_fwd_bf16_mma(const AttnArgs& a, cudaStream_t st) {
   if (a.nseq <= 0) return;
   if (a.dh == 64) fa::run_fwd<64>(a, st);
   else fa::run_fwd<128>(a, st);

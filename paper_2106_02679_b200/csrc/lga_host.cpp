@@ -352,7 +352,7 @@ static void layer_fwd(lga_handle* h, const void* W, const float* x_in, float* y_
     a.scale = 1.0f / sqrtf((float)c.dh);
     a.qkv = h->qkv; a.o = h->o; a.lse = h->lse;
     const int p = prof_begin(h, st);
-    if (c.bf16) attn_fwd_bf16(a, st); else attn_fwd_f32(a, st);
+    if (c.bf16) CK(attn_fwd_bf16(a, st)); else attn_fwd_f32(a, st);
     KCHECK();
     prof_end(h, p, st, FAM_ATTN, attn_flops_fwd(c, a.nseq));
   }

@@ -40,7 +40,14 @@ extern "C" int lgatest_attn_fwd(int path, int nseq, int seq, int heads, int dh, 
   AttnArgs a = mk(nseq, seq, heads, dh, causal);
   a.qkv = qkv; a.o = o; a.lse = lse;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (path == 0) attn_fwd_f32(a, st); else attn_fwd_bf16(a, st);
+  if (path == 0) {
+    attn_fwd_f32(a, st);
+  } else if (path == 1) {
+    const cudaError_t e = attn_fwd_bf16(a, st);
+    if (e != cudaSuccess) return (int)e;
+  } else {
+    attn_fwd_bf16_mma(a, st);
+  }
   return (int)cudaGetLastError();
 }
 

@@ -1,0 +1,90 @@
+"""Multi-GPU parity and exact counters (one process per GPU, torchrun): ZeRO-partitioned data
+parallelism (D = 2, 4) and the modular pipeline (P = 2, D x P = 4), against the fp64 oracle.
+
+Skipped unless the box has enough GPUs (gpurun --gpus N)."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import synth
+from gpu_util import oracle_run, per_layer_rel, rel
+from oracle import counters as oc
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+torch = pytest.importorskip("torch")
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+HERE = os.path.dirname(os.path.abspath(__file__))
+_port = [29611]
+
+
+def _launch(tmp_path, sh, precision=0, schedule=0, chunk=0, steps=1):
+    world = sh.dp * sh.pp
+    if NGPU < world:
+        pytest.skip(f"needs {world} GPUs, have {NGPU}")
+    _port[0] += 1
+    shape = json.dumps(dict(layers=sh.layers, d=sh.d, heads=sh.heads, seq=sh.seq, micro_batch=sh.micro_batch,
+                            n_micro=sh.n_micro, dp=sh.dp, pp=sh.pp))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={_port[0]}", os.path.join(HERE, "dist_worker.py"),
+           "--out", str(tmp_path), "--shape", shape, "--precision", str(precision), "--schedule", str(schedule),
+           "--chunk", str(chunk), "--steps", str(steps)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return [dict(np.load(os.path.join(tmp_path, f"rank{k}.npz"))) for k in range(world)]
+
+
+def _check(outs, sh, tol, steps=1, schedule="layered", elem=4):
+    batches = [synth.batch(sh, step=k) for k in range(steps)]
+    init = synth.init_params(sh, style="parity")
+    rp, rl, rg = oracle_run(sh, init, batches, lr=1e-3)
+    pl = sh.d * sh.d * 12 + 13 * sh.d
+    for o in outs:
+        stage = int(o["stage"])
+        layers = oc.local_layers(stage, sh.layers, sh.pp)
+        sel = np.concatenate([np.arange(i * pl, (i + 1) * pl) for i in layers])
+        g, p = o["grads"], o["params"]
+        assert rel(g, rg[sel]) < tol, (stage, per_layer_rel(g, rg[sel], len(layers)))
+        assert rel(p, rp[sel]) < tol
+        np.testing.assert_allclose(o["losses"], rl, rtol=max(tol, 1e-6))
+        assert list(o["stages"]) == [oc.stage_of_layer(i, sh.pp) for i in range(sh.layers)]
+        last = json.loads(str(o["last"]))
+        ref = oc.comm_counters(oc.StepShape(layers=sh.layers, d=sh.d, seq=sh.seq, micro_batch=sh.micro_batch,
+                                            n_micro=sh.n_micro, dp=sh.dp, pp=sh.pp),
+                               stage=stage, schedule=schedule, param_bytes=elem, grad_bytes=elem)
+        for k, v in ref.items():
+            assert last[k] == v, (k, last[k], v, stage)
+
+
+@pytest.mark.parametrize("dp", [2, 4])
+def test_dp_fp32_layered(tmp_path, dp):
+    sh = synth.Shape(layers=4, d=64, heads=4, seq=32, micro_batch=2, n_micro=4, dp=dp)
+    _check(_launch(tmp_path, sh), sh, 1e-5)
+
+
+def test_dp2_fp32_standard(tmp_path):
+    sh = synth.Shape(layers=2, d=64, heads=4, seq=32, micro_batch=2, n_micro=3, dp=2)
+    _check(_launch(tmp_path, sh, schedule=1), sh, 1e-5, schedule="standard")
+
+
+def test_dp2_fp32_two_steps_chunked(tmp_path):
+    sh = synth.Shape(layers=2, d=64, heads=4, seq=32, micro_batch=2, n_micro=4, dp=2)
+    _check(_launch(tmp_path, sh, chunk=2, steps=2), sh, 1e-5, steps=2)
+
+
+def test_pp2_fp32_modular_pipeline(tmp_path):
+    sh = synth.Shape(layers=4, d=64, heads=4, seq=32, micro_batch=2, n_micro=4, dp=1, pp=2)
+    _check(_launch(tmp_path, sh), sh, 1e-5)
+
+
+def test_pp2_dp2_fp32(tmp_path):
+    sh = synth.Shape(layers=4, d=64, heads=4, seq=32, micro_batch=2, n_micro=4, dp=2, pp=2)
+    _check(_launch(tmp_path, sh), sh, 1e-5)
+
+
+def test_dp2_bf16(tmp_path):
+    sh = synth.Shape(layers=2, d=256, heads=2, seq=128, micro_batch=1, n_micro=4, dp=2)
+    _check(_launch(tmp_path, sh, precision=1), sh, 2e-2, elem=2)

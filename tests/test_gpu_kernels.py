@@ -126,7 +126,7 @@ def _attn_ref(qkv, nseq, s, H, dh, causal):
     return q, k, v
 
 
-@pytest.mark.parametrize("path,dh,s,causal", [(0, 16, 37, 1), (0, 64, 128, 0), (1, 64, 256, 1), (1, 128, 200, 1),
+@pytest.mark.parametrize("path,dh,s,causal", [(0, 16, 37, 1), (0, 64, 128, 0), (1, 64, 256, 1), (1, 128, 200, 1), (2, 128, 200, 1), (2, 64, 300, 0), (1, 64, 300, 0),
                                               (1, 128, 512, 0), (1, 64, 1024, 1)])
 def test_attention_fwd_bwd(path, dh, s, causal):
     nseq, H = 2, 3

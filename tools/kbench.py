@@ -1,0 +1,110 @@
+"""Per-kernel micro-benchmarks through the test hooks (include/lga_testing.h), CUDA-event timed.
+
+    python tools/kbench.py [attn] [gemm] [--dh 128 --seq 2048 --nseq 16 --heads 16]
+
+Prints one line per kernel: shape, ms per launch, achieved TFLOP/s (algorithmic flops).
+Development tool; bench.py is the measurement of record.
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2106_02679_b200 import _abi  # noqa: E402
+
+L = _abi.lib()
+L.lgatest_gemm.restype = C.c_int
+L.lgatest_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64,
+                           C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                           C.c_void_p, C.c_int64, C.c_int, C.c_void_p]
+L.lgatest_attn_fwd.restype = C.c_int
+L.lgatest_attn_fwd.argtypes = [C.c_int] * 6 + [C.c_void_p] * 3 + [C.c_void_p]
+L.lgatest_attn_bwd.restype = C.c_int
+L.lgatest_attn_bwd.argtypes = [C.c_int] * 6 + [C.c_void_p] * 6 + [C.c_void_p]
+
+
+def P(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def timeit(fn, iters=10, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def attn(args):
+    nseq, s, H, dh = args.nseq, args.seq, args.heads, args.dh
+    d = H * dh
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    qkv = torch.randn(nseq * s, 3 * d, device="cuda").bfloat16()
+    o = torch.empty(nseq * s, d, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(nseq, H, s, device="cuda")
+    dO = torch.randn(nseq * s, d, device="cuda").bfloat16()
+    dsum = torch.empty(nseq, H, s, device="cuda")
+    dqkv = torch.empty_like(qkv)
+    flops = 4.0 * dh * (s * (s + 1) / 2) * H * nseq
+    for path, name in ((1, "fwd tcgen05"), (2, "fwd mma.sync")):
+        ms = timeit(lambda: L.lgatest_attn_fwd(path, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), st))
+        print(f"attn {name:14s} nseq={nseq} s={s} H={H} dh={dh}: {ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s")
+    L.lgatest_attn_fwd(1, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), st)
+    ms = timeit(lambda: L.lgatest_attn_bwd(1, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), P(dO), P(dsum), P(dqkv), st))
+    print(f"attn {'bwd':14s} nseq={nseq} s={s} H={H} dh={dh}: {ms:.3f} ms  {2 * flops / ms / 1e9:.1f} TFLOP/s (algorithmic 2x fwd)")
+
+
+def gemm(args):
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    T, d = args.tokens, args.d
+    f = 4 * d
+    cases = [
+        ("qkv fwd   ", T, 3 * d, d, True, False, 1, "bias_bf16"),
+        ("oproj fwd ", T, d, d, True, False, 0, "bias_res_f32"),
+        ("ffn1 fwd  ", T, f, d, True, False, 1, "gelu"),
+        ("ffn2 fwd  ", T, d, f, True, False, 0, "bias_res_f32"),
+        ("ffn2 dgrad", T, f, d, True, True, 1, "gelu_bwd"),
+        ("ffn1 dgrad", T, d, f, True, True, 0, "f32"),
+        ("w1 wgrad  ", d, f, T, False, False, 0, "acc"),
+        ("wqkv wgrad", d, 3 * d, T, False, False, 0, "acc"),
+        ("wo wgrad  ", d, d, T, False, False, 0, "acc"),
+    ]
+    for name, M, N, K, ak, bk, outbf, kind in cases:
+        A = torch.randn((M, K) if ak else (K, M), device="cuda").bfloat16()
+        B = torch.randn((N, K) if bk else (K, N), device="cuda").bfloat16()
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16 if outbf else torch.float32)
+        bias = torch.randn(N, device="cuda").bfloat16() if kind in ("bias_bf16", "bias_res_f32", "gelu") else None
+        res = torch.randn(M, N, device="cuda") if kind == "bias_res_f32" else None
+        acc = torch.randn(M, N, device="cuda") if kind == "acc" else None
+        aux = torch.randn(M, N, device="cuda").bfloat16() if kind in ("gelu", "gelu_bwd") else None
+        ek = 1 if kind == "gelu" else (2 if kind == "gelu_bwd" else 0)
+        dt = lambda t: 0 if t is None or t.dtype == torch.float32 else 1
+        fn = lambda: L.lgatest_gemm(1, M, N, K, P(A), A.shape[1], int(ak), P(B), B.shape[1], int(bk), ek, P(bias), dt(bias),
+                                    P(res), P(acc), P(aux), dt(aux), P(out), N, dt(out), st)
+        assert fn() == 0
+        ms = timeit(fn)
+        print(f"gemm {name} M={M} N={N} K={K} {kind:12s}: {ms:.3f} ms  {2.0 * M * N * K / ms / 1e9:.1f} TFLOP/s")
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("what", nargs="*", default=["attn", "gemm"])
+    ap.add_argument("--dh", type=int, default=128)
+    ap.add_argument("--seq", type=int, default=2048)
+    ap.add_argument("--nseq", type=int, default=16)
+    ap.add_argument("--heads", type=int, default=16)
+    ap.add_argument("--tokens", type=int, default=32768)
+    ap.add_argument("--d", type=int, default=2048)
+    a = ap.parse_args()
+    if "attn" in a.what:
+        attn(a)
+    if "gemm" in a.what:
+        gemm(a)
