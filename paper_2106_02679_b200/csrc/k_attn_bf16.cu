@@ -547,7 +547,7 @@ void attn_fwd_bf16_mma(const AttnArgs& a, cudaStream_t st) {
   else fa::run_fwd<128>(a, st);
 }
 
-void attn_bwd_bf16(const AttnArgs& a, cudaStream_t st) {
+void attn_bwd_bf16_mma(const AttnArgs& a, cudaStream_t st) {
   if (a.nseq <= 0) return;
   if (a.dh == 64) fa::run_bwd<64>(a, st);
   else fa::run_bwd<128>(a, st);

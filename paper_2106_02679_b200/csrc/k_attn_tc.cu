@@ -234,39 +234,10 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
   }
 }
 
-static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
-}
-
-// 3-D map over packed qkv: dim0 = 3d columns, dim1 = positions in a sequence, dim2 = sequences;
-// a [128 x 64] box never crosses a sequence (rows past the end are zero-filled).
-static cudaError_t qkv_map(CUtensorMap* m, const AttnArgs& a) {
-  auto enc = get_encode();
-  if (!enc) return cudaErrorNotSupported;
-  const uint64_t ld = 3ull * a.d;
-  cuuint64_t dims[3] = {ld, (cuuint64_t)a.seq, (cuuint64_t)a.nseq};
-  cuuint64_t strides[2] = {ld * 2, ld * 2 * (uint64_t)a.seq};
-  cuuint32_t box[3] = {64, 128, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.qkv), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
-}
-
 template <int DH>
 static cudaError_t run_fwd(const AttnArgs& a, cudaStream_t st) {
   CUtensorMap tm;
-  cudaError_t e = qkv_map(&tm, a);
+  cudaError_t e = map3d_bf16(&tm, a.qkv, 3ull * a.d, a.seq, a.nseq, 128);
   if (e != cudaSuccess) return e;
   static bool set = false;
   if (!set) {

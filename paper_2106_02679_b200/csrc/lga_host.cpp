@@ -478,7 +478,7 @@ static void layer_bwd(lga_handle* h, const void* W, const float* x_in, const flo
     a.scale = 1.0f / sqrtf((float)c.dh);
     a.qkv = h->qkv; a.o = h->o; a.lse = h->lse; a.dO = h->dO; a.dsum = h->dsum; a.dqkv = h->dqkv;
     const int p = prof_begin(h, st);
-    if (c.bf16) attn_bwd_bf16(a, st); else attn_bwd_f32(a, st);
+    if (c.bf16) CK(attn_bwd_bf16(a, st)); else attn_bwd_f32(a, st);
     KCHECK();
     prof_end(h, p, st, FAM_ATTN, 2.0 * attn_flops_fwd(c, a.nseq));
   }

@@ -4,7 +4,11 @@
 #pragma once
 
 #include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
 #include <cstdint>
+#include <mutex>
 
 namespace lga {
 namespace tcu {
@@ -142,6 +146,44 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // (TMA CU_TENSOR_MAP_SWIZZLE_128B == UMMA SWIZZLE_128B; the tile base must be 1024-byte aligned)
 __device__ __forceinline__ uint32_t sw128(int row, int chunk) {
   return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+// ---- host: tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry point; no -lcuda)
+inline PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 3-D bf16 map over a [nseq][seq][cols] activation: box = 64 columns x box_rows positions x 1 sequence,
+// 128B swizzle; boxes never cross a sequence (positions past seq are zero-filled).
+inline cudaError_t map3d_bf16(CUtensorMap* m, const void* ptr, uint64_t cols, uint64_t seq, uint64_t nseq,
+                              uint32_t box_rows) {
+  auto enc = tmap_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((cols * 2) & 15)) return cudaErrorMisalignedAddress;
+  cuuint64_t dims[3] = {cols, seq, nseq};
+  cuuint64_t strides[2] = {cols * 2, cols * 2 * seq};
+  cuuint32_t box[3] = {64, box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// 1-D bulk copy global -> shared completing on an mbarrier (bytes % 16 == 0, both 16-byte aligned)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 }  // namespace tcu

@@ -57,6 +57,13 @@ extern "C" int lgatest_attn_bwd(int path, int nseq, int seq, int heads, int dh, 
   AttnArgs a = mk(nseq, seq, heads, dh, causal);
   a.qkv = qkv; a.o = (void*)o; a.lse = (float*)lse; a.dO = dO; a.dsum = dsum; a.dqkv = dqkv;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (path == 0) attn_bwd_f32(a, st); else attn_bwd_bf16(a, st);
+  if (path == 0) {
+    attn_bwd_f32(a, st);
+  } else if (path == 1) {
+    const cudaError_t e = attn_bwd_bf16(a, st);
+    if (e != cudaSuccess) return (int)e;
+  } else {
+    attn_bwd_bf16_mma(a, st);
+  }
   return (int)cudaGetLastError();
 }
