@@ -21,7 +21,10 @@ namespace fat {
 
 using namespace tcu;
 
-constexpr int BQ = 128, BKV = 128, NT = 256;
+constexpr int BQ = 128, BKV = 128;
+constexpr int SM_WARPS = 8;                    // softmax warps: 2 per TMEM lane quadrant, 64 key columns each
+constexpr int NT = (4 + SM_WARPS) * 32;
+constexpr int SM_THREADS = SM_WARPS * 32;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_THRESHOLD = 8.0f;   // log2 units
 
@@ -33,7 +36,8 @@ struct FwdSmem {
   static constexpr int K_OFF = Q_OFF + TILE;        // 2 stages
   static constexpr int V_OFF = K_OFF + 2 * TILE;    // 2 stages
   static constexpr int P_OFF = V_OFF + 2 * TILE;    // [128][128] bf16 = 2 sub-tiles
-  static constexpr int BAR_OFF = P_OFF + 2 * SUB;
+  static constexpr int RED_OFF = P_OFF + 2 * SUB;   // [2 tile parity][2 halves][128 rows] row maxima + [2][128] sums
+  static constexpr int BAR_OFF = RED_OFF + 6 * 128 * 4;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
@@ -65,7 +69,7 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 14; ++i) {
       const bool by_softmax = (&bars[i] == s_empty) || (&bars[i] == s_empty + 1) || (&bars[i] == p_full);
-      mbar_init(&bars[i], by_softmax ? 128 : 1);   // softmax threads arrive individually
+      mbar_init(&bars[i], by_softmax ? SM_THREADS : 1);   // softmax threads arrive individually
     }
     mbar_fence_init();
     prefetch_tmap(&tm);
@@ -135,43 +139,46 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
         }
       }
     }
-  } else if (warp >= 4) {  // ===== softmax + epilogue, one query row per thread
+  } else if (warp >= 4) {  // ===== softmax + epilogue: one query row per thread pair (two column halves)
     const int qd = warp & 3;
+    const int hf = (warp - 4) >> 2;            // key-column half / O-column half this warp owns
     const int r = qd * 32 + lane;
     const int q = q0 + r;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const float sl2 = a.scale * LOG2E;
-    uint8_t* sP = smem + SM::P_OFF;
+    uint8_t* sP = smem + SM::P_OFF + hf * SM::SUB;   // this half's [128][64] P sub-tile
+    float* red = reinterpret_cast<float*>(smem + SM::RED_OFF);   // [2 parity][2 halves][128]
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
       const int b = j & 1;
       mbar_wait(&s_full[b], (j >> 1) & 1);
       fence_after();
-      float sv[BKV];
-#pragma unroll
-      for (int c = 0; c < BKV / 32; ++c) {
-        float t[32];
-        tmem_ld32(t_s[b] + lane_off + c * 32, t);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = t[i];
-      }
+      uint32_t raw[2][32];
+      tmem_ld32_nowait(t_s[b] + lane_off + hf * 64, raw[0]);
+      tmem_ld32_nowait(t_s[b] + lane_off + hf * 64 + 32, raw[1]);
+      tmem_wait_ld();
       fence_before();
       mbar_arrive(&s_empty[b]);
-      const int k0 = j * BKV;
+      const int k0 = j * BKV + hf * 64;
+      float sv[64];
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < BKV; ++c) {
+      for (int c = 0; c < 64; ++c) {
         const int kj = k0 + c;
-        float v = sv[c] * sl2;
+        float v = __uint_as_float(raw[c >> 5][c & 31]) * sl2;
         if (kj >= s || (a.causal && kj > q)) v = -INFINITY;
         sv[c] = v;
         mx = fmaxf(mx, v);
       }
+      // row max over both halves: exchange through shared memory (buffer parity j&1 avoids a WAR race)
+      red[((j & 1) * 2 + hf) * 128 + r] = mx;
+      asm volatile("bar.sync 1, %0;" ::"n"(SM_THREADS) : "memory");
+      mx = fmaxf(mx, red[((j & 1) * 2 + (hf ^ 1)) * 128 + r]);
       const float m_new = (mx > m_used + RESCALE_THRESHOLD) ? mx : m_used;
       float rs = 0.f;
-      uint32_t pk[BKV / 2];
+      uint32_t pk[32];
 #pragma unroll
-      for (int c = 0; c < BKV; c += 2) {
+      for (int c = 0; c < 64; c += 2) {
         const float p0 = m_new == -INFINITY ? 0.f : exp2f(sv[c] - m_new);
         const float p1 = m_new == -INFINITY ? 0.f : exp2f(sv[c + 1] - m_new);
         rs += p0 + p1;
@@ -182,10 +189,10 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
         fence_after();
       }
       float scale = 1.f;
-      if (m_new != m_used && m_used != -INFINITY) {
+      if (m_new != m_used && m_used != -INFINITY) {   // lazy rescale of this half's O columns
         scale = exp2f(m_used - m_new);
 #pragma unroll 1
-        for (int c = 0; c < DH / 32; ++c) {
+        for (int c = hf * (DH / 64); c < (hf + 1) * (DH / 64); ++c) {
           float t[32];
           tmem_ld32(t_o + lane_off + c * 32, t);
 #pragma unroll
@@ -193,12 +200,11 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
           tmem_st32(t_o + lane_off + c * 32, t);
         }
       }
-      l = l * scale + rs;
+      l = l * scale + rs;   // partial row sum over this half's keys
       m_used = m_new;
-      // P row r -> shared memory, K-major SW128 layout ([128][64] sub-tiles of 64 keys)
 #pragma unroll
-      for (int ch = 0; ch < BKV / 8; ++ch) {
-        const uint32_t addr = smem_u32(sP + (ch >> 3) * SM::SUB) + sw128(r, ch & 7);
+      for (int ch = 0; ch < 8; ++ch) {
+        const uint32_t addr = smem_u32(sP) + sw128(r, ch);
         asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[ch * 4]), "r"(pk[ch * 4 + 1]),
                      "r"(pk[ch * 4 + 2]), "r"(pk[ch * 4 + 3])
                      : "memory");
@@ -207,13 +213,16 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
       fence_before();
       mbar_arrive(p_full);
     }
-    // epilogue: O / l -> bf16 global, lse
+    // epilogue: l = sum of both halves; O / l -> bf16 global (each half writes its O columns), lse
+    red[4 * 128 + hf * 128 + r] = l;
+    asm volatile("bar.sync 1, %0;" ::"n"(SM_THREADS) : "memory");
+    l += red[4 * 128 + (hf ^ 1) * 128 + r];
     mbar_wait(o_done, (nkv - 1) & 1);
     fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     __nv_bfloat16* og = static_cast<__nv_bfloat16*>(a.o) + ((int64_t)sq * s + q) * d + h * DH;
 #pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
+    for (int c = hf * (DH / 64); c < (hf + 1) * (DH / 64); ++c) {
       float t[32];
       tmem_ld32(t_o + lane_off + c * 32, t);
       if (q < s) {
@@ -224,7 +233,7 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
                               pack_bf16x2(t[8 * i + 4] * inv, t[8 * i + 5] * inv), pack_bf16x2(t[8 * i + 6] * inv, t[8 * i + 7] * inv));
       }
     }
-    if (q < s) a.lse[((int64_t)sq * a.heads + h) * s + q] = (m_used + log2f(l)) * 0.6931471805599453f;
+    if (q < s && hf == 0) a.lse[((int64_t)sq * a.heads + h) * s + q] = (m_used + log2f(l)) * 0.6931471805599453f;
   }
   fence_before();
   __syncthreads();

@@ -18,7 +18,9 @@ namespace fatb {
 
 using namespace tcu;
 
-constexpr int NT = 256;
+constexpr int EW_WARPS = 8;                 // element-wise warps: 2 per TMEM lane quadrant
+constexpr int EW_THREADS = EW_WARPS * 32;
+constexpr int NT = (4 + EW_WARPS) * 32;
 constexpr float LOG2E = 1.4426950408889634f;
 
 // rowsum(dO * o) per (sequence, head, position); one warp per row
@@ -40,25 +42,15 @@ __global__ void dsum_kernel(AttnArgs a) {
   if (l == 0) a.dsum[((tok / a.seq) * a.heads + h) * a.seq + tok % a.seq] = acc;
 }
 
-__device__ __forceinline__ void st_row_bf16(uint8_t* tile, int r, const uint32_t (&pk)[32]) {
-  // 64 bf16 (= 8 chunks of 16 B) of row r of a [128][64] K-major SW128 tile
+// 32 bf16 (4 chunks of 16 B, chunk indices 4*half .. 4*half+3) of row r of a [128][64] K-major SW128 tile
+__device__ __forceinline__ void st_half_row_bf16(uint8_t* tile, int r, int half, const uint32_t (&pk)[16]) {
 #pragma unroll
-  for (int ch = 0; ch < 8; ++ch) {
-    const uint32_t addr = smem_u32(tile) + sw128(r, ch);
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[ch * 4]), "r"(pk[ch * 4 + 1]),
-                 "r"(pk[ch * 4 + 2]), "r"(pk[ch * 4 + 3])
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t addr = smem_u32(tile) + sw128(r, half * 4 + i);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[i * 4]), "r"(pk[i * 4 + 1]),
+                 "r"(pk[i * 4 + 2]), "r"(pk[i * 4 + 3])
                  : "memory");
   }
-}
-
-__device__ __forceinline__ void ld_row64(uint32_t taddr, float (&v)[64]) {
-  float t[32];
-  tmem_ld32(taddr, t);
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = t[i];
-  tmem_ld32(taddr + 32, t);
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[32 + i] = t[i];
 }
 
 // TMEM row -> bf16 global row.  tcgen05.ld is warp-collective: every lane executes it, only
@@ -127,7 +119,7 @@ __global__ void __launch_bounds__(NT, 1)
   const int64_t rb = ((int64_t)sq * a.heads + h) * s;   // row base of lse / dsum
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < 11; ++i) mbar_init(&bars[i], (i == 7 || i == 8 || i == 9) ? 128 : 1);
+    for (int i = 0; i < 11; ++i) mbar_init(&bars[i], (i == 7 || i == 8 || i == 9) ? EW_THREADS : 1);
     mbar_fence_init();
     prefetch_tmap(&tm_kv);
     prefetch_tmap(&tm_q);
@@ -203,11 +195,13 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
     }
-  } else if (warp >= 4) {  // ===== element-wise: one key row per thread
+  } else if (warp >= 4) {  // ===== element-wise: one key row per thread pair (two query-column halves)
     const int qd = warp & 3;
+    const int hf = (warp - 4) >> 2;
     const int r = qd * 32 + lane;
+    const int tid = threadIdx.x - 128;
     const int kj = k0 + r;
-    const uint32_t lo = (uint32_t)(qd * 32) << 16;
+    const uint32_t lrow = (uint32_t)(qd * 32) << 16;
     const float sl2 = a.scale * LOG2E;
     uint8_t* sPt = smem + SM::PT_OFF;
     uint8_t* sDSt = smem + SM::DST_OFF;
@@ -216,31 +210,32 @@ __global__ void __launch_bounds__(NT, 1)
       const int q0 = (qstart + i) * QB;
       mbar_wait(&s_full[b], (i >> 1) & 1);
       fence_after();
-      float sv[64], dp[64];
-      ld_row64(t_st[b] + lo, sv);
-      ld_row64(t_dpt[b] + lo, dp);
+      uint32_t rsv[32], rdp[32];
+      tmem_ld32_nowait(t_st[b] + lrow + hf * 32, rsv);
+      tmem_ld32_nowait(t_dpt[b] + lrow + hf * 32, rdp);
+      tmem_wait_ld();
       fence_before();
       mbar_arrive(&s_empty[b]);
-      // lse (log2 units) and dsum of this query tile -> shared memory, loaded by the 128 element-wise threads
-      {
-        const int t = r & 63, q = q0 + t;
+      // lse (log2 units) and dsum of this query tile -> shared memory
+      if (tid < 128) {
+        const int t = tid & 63, q = q0 + t;
         float v = 0.f;
-        if (q < s) v = r < 64 ? a.lse[rb + q] * LOG2E : a.dsum[rb + q];
-        (r < 64 ? lse_s : dsum_s)[st * 64 + t] = v;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q < s) v = tid < 64 ? a.lse[rb + q] * LOG2E : a.dsum[rb + q];
+        (tid < 64 ? lse_s : dsum_s)[st * 64 + t] = v;
       }
-      const float* ls = lse_s + st * 64;
-      const float* ds_ = dsum_s + st * 64;
-      uint32_t pp[32], pd[32];
+      asm volatile("bar.sync 1, %0;" ::"n"(EW_THREADS) : "memory");
+      const float* ls = lse_s + st * 64 + hf * 32;
+      const float* ds_ = dsum_s + st * 64 + hf * 32;
+      uint32_t pp[16], pd[16];
 #pragma unroll
-      for (int c = 0; c < 64; c += 2) {
+      for (int c = 0; c < 32; c += 2) {
         float p[2], g[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int q = q0 + c + e;
+          const int q = q0 + hf * 32 + c + e;
           const bool valid = q < s && kj < s && (!a.causal || kj <= q);
-          p[e] = valid ? exp2f(sv[c + e] * sl2 - ls[c + e]) : 0.f;
-          g[e] = p[e] * (dp[c + e] - ds_[c + e]) * a.scale;
+          p[e] = valid ? exp2f(__uint_as_float(rsv[c + e]) * sl2 - ls[c + e]) : 0.f;
+          g[e] = p[e] * (__uint_as_float(rdp[c + e]) - ds_[c + e]) * a.scale;
         }
         pp[c / 2] = pack_bf16x2(p[0], p[1]);
         pd[c / 2] = pack_bf16x2(g[0], g[1]);
@@ -249,17 +244,17 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_wait(g_done, (i - 1) & 1);   // previous dV/dK MMAs done: P^T / dS^T buffers free
         fence_after();
       }
-      st_row_bf16(sPt, r, pp);
-      st_row_bf16(sDSt, r, pd);
+      st_half_row_bf16(sPt, r, hf, pp);
+      st_half_row_bf16(sDSt, r, hf, pd);
       fence_proxy_async();
       fence_before();
       mbar_arrive(p_full);
     }
     mbar_wait(g_done, (nq - 1) & 1);
     fence_after();
-    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + kj) * 3 * d + h * DH;
-    store_row_bf16_global(out + d, t_dk + lo, DH, 1.f, kj < s);
-    store_row_bf16_global(out + 2 * d, t_dv + lo, DH, 1.f, kj < s);
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + kj) * 3 * d + h * DH + hf * (DH / 2);
+    store_row_bf16_global(out + d, t_dk + lrow + hf * (DH / 2), DH / 2, 1.f, kj < s);
+    store_row_bf16_global(out + 2 * d, t_dv + lrow + hf * (DH / 2), DH / 2, 1.f, kj < s);
   }
   fence_before();
   __syncthreads();
@@ -315,7 +310,7 @@ __global__ void __launch_bounds__(NT, 1)
   const int nk = (kend + KB2 - 1) / KB2;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < 11; ++i) mbar_init(&bars[i], (i == 7 || i == 8 || i == 9) ? 128 : 1);
+    for (int i = 0; i < 11; ++i) mbar_init(&bars[i], (i == 7 || i == 8 || i == 9) ? EW_THREADS : 1);
     mbar_fence_init();
     prefetch_tmap(&tm_q);
     prefetch_tmap(&tm_g);
@@ -386,11 +381,12 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
     }
-  } else if (warp >= 4) {  // ===== element-wise: one query row per thread
+  } else if (warp >= 4) {  // ===== element-wise: one query row per thread pair (two key-column halves)
     const int qd = warp & 3;
+    const int hf = (warp - 4) >> 2;
     const int r = qd * 32 + lane;
     const int q = q0 + r;
-    const uint32_t lo = (uint32_t)(qd * 32) << 16;
+    const uint32_t lrow = (uint32_t)(qd * 32) << 16;
     const float sl2 = a.scale * LOG2E;
     const int64_t rb = ((int64_t)sq * a.heads + h) * s;
     const float lse2 = q < s ? a.lse[rb + q] * LOG2E : 0.f;
@@ -400,21 +396,22 @@ __global__ void __launch_bounds__(NT, 1)
       const int b = j & 1;
       mbar_wait(&s_full[b], (j >> 1) & 1);
       fence_after();
-      float sv[64], dp[64];
-      ld_row64(t_s[b] + lo, sv);
-      ld_row64(t_dp[b] + lo, dp);
+      uint32_t rsv[32], rdp[32];
+      tmem_ld32_nowait(t_s[b] + lrow + hf * 32, rsv);
+      tmem_ld32_nowait(t_dp[b] + lrow + hf * 32, rdp);
+      tmem_wait_ld();
       fence_before();
       mbar_arrive(&s_empty[b]);
-      uint32_t pd[32];
+      uint32_t pd[16];
 #pragma unroll
-      for (int c = 0; c < 64; c += 2) {
+      for (int c = 0; c < 32; c += 2) {
         float g[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int kj = j * KB2 + c + e;
+          const int kj = j * KB2 + hf * 32 + c + e;
           const bool valid = q < s && kj < s && (!a.causal || kj <= q);
-          const float p = valid ? exp2f(sv[c + e] * sl2 - lse2) : 0.f;
-          g[e] = p * (dp[c + e] - Dq) * a.scale;
+          const float p = valid ? exp2f(__uint_as_float(rsv[c + e]) * sl2 - lse2) : 0.f;
+          g[e] = p * (__uint_as_float(rdp[c + e]) - Dq) * a.scale;
         }
         pd[c / 2] = pack_bf16x2(g[0], g[1]);
       }
@@ -422,15 +419,15 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_wait(g_done, (j - 1) & 1);
         fence_after();
       }
-      st_row_bf16(sDS, r, pd);
+      st_half_row_bf16(sDS, r, hf, pd);
       fence_proxy_async();
       fence_before();
       mbar_arrive(p_full);
     }
     mbar_wait(g_done, (nk - 1) & 1);
     fence_after();
-    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + q) * 3 * d + h * DH;
-    store_row_bf16_global(out, t_dq + lo, DH, 1.f, q < s);
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + q) * 3 * d + h * DH + hf * (DH / 2);
+    store_row_bf16_global(out, t_dq + lrow + hf * (DH / 2), DH / 2, 1.f, q < s);
   }
   fence_before();
   __syncthreads();

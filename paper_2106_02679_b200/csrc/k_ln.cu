@@ -1,0 +1,272 @@
+// k_ln.cu -- LayerNorm forward / backward and the fixed-order column-sum finisher (HBM-bound).
+//
+// y = (x - mu) rstd gamma + beta, biased variance (reading A-1); backward (O5):
+//   dx = rstd (dxhat - mean(dxhat) - xhat mean(dxhat xhat)) + resid,  dxhat = dout gamma,
+//   dgamma = sum_rows dout xhat,  dbeta = sum_rows dout.
+// Row kernels: one warp per row, 128-bit loads, the row held in registers (d % 128 == 0), else one block
+// per row.  dgamma / dbeta: a separate column kernel writes per-block partials in a fixed row order; the
+// finisher sums the partials in a fixed order too -- no float atomics, bitwise reproducible.
+#include "kernels.cuh"
+
+namespace lga {
+
+__device__ __forceinline__ float4 ld4(const void* p, DT t, int64_t i) {
+  if (t == DT::F32) return *reinterpret_cast<const float4*>(static_cast<const float*>(p) + i);
+  const uint2 u = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(p) + i);
+  return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                     __uint_as_float(u.y & 0xFFFF0000u));
+}
+__device__ __forceinline__ void st4(void* p, DT t, int64_t i, float4 v) {
+  if (t == DT::F32) {
+    *reinterpret_cast<float4*>(static_cast<float*>(p) + i) = v;
+  } else {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p) + i) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+}
+
+// =============================================================== forward
+template <int NV>
+__global__ void __launch_bounds__(256) ln_fwd_warp(const float* __restrict__ x, const void* gamma, const void* beta,
+                                                   DT pdt, void* y, DT ydt, float2* __restrict__ stats, int rows,
+                                                   int d, float eps) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* xr = x + (int64_t)row * d;
+  float4 v[NV];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    v[k] = *reinterpret_cast<const float4*>(xr + lane * 4 + 128 * k);
+    s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  }
+  const float mean = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const float a = v[k].x - mean, b = v[k].y - mean, c = v[k].z - mean, e = v[k].w - mean;
+    q += (a * a + b * b) + (c * c + e * e);
+  }
+  const float rstd = rsqrtf(warp_sum(q) / d + eps);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = lane * 4 + 128 * k;
+    const float4 g = ld4(gamma, pdt, c), b = ld4(beta, pdt, c);
+    st4(y, ydt, (int64_t)row * d + c,
+        make_float4((v[k].x - mean) * rstd * g.x + b.x, (v[k].y - mean) * rstd * g.y + b.y,
+                    (v[k].z - mean) * rstd * g.z + b.z, (v[k].w - mean) * rstd * g.w + b.w));
+  }
+  if (lane == 0) stats[row] = make_float2(mean, rstd);
+}
+
+// generic d: block per row, VPT values per thread
+template <int VPT>
+__global__ void __launch_bounds__(256) ln_fwd_block(const float* __restrict__ x, const void* gamma, const void* beta,
+                                                    DT pdt, void* y, DT ydt, float2* __restrict__ stats, int d,
+                                                    float eps) {
+  __shared__ float red[64];
+  const int64_t row = blockIdx.x;
+  const float* xr = x + row * d;
+  float v[VPT];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    v[i] = c < d ? xr[c] : 0.f;
+    s += v[i];
+  }
+  const float mean = block_sum2(s, 0.f, red).x / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    const float t = c < d ? v[i] - mean : 0.f;
+    q += t * t;
+  }
+  const float rstd = rsqrtf(block_sum2(q, 0.f, red).x / d + eps);
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    if (c < d) st_elem(y, row * d + c, ydt, (v[i] - mean) * rstd * ld_elem(gamma, c, pdt) + ld_elem(beta, c, pdt));
+  }
+  if (threadIdx.x == 0) stats[row] = make_float2(mean, rstd);
+}
+
+void ln_fwd(const float* x, const void* gamma, const void* beta, DT pdt, void* y, DT ydt, float2* stats, int rows,
+            int d, float eps, cudaStream_t st) {
+  if (rows <= 0) return;
+  if (d % 128 == 0 && d <= 4096) {
+    const int nv = d / 128, grid = (rows + 7) / 8;
+#define LF(N) note_launch(), ln_fwd_warp<N><<<grid, 256, 0, st>>>(x, gamma, beta, pdt, y, ydt, stats, rows, d, eps)
+    switch (nv) {
+      case 1: LF(1); break; case 2: LF(2); break; case 3: LF(3); break; case 4: LF(4); break;
+      case 5: LF(5); break; case 6: LF(6); break; case 8: LF(8); break; case 12: LF(12); break;
+      case 16: LF(16); break; case 24: LF(24); break; case 32: LF(32); break;
+      default: goto generic;
+    }
+#undef LF
+    return;
+  }
+generic : {
+  const int bd = d >= 1024 ? 256 : (d >= 256 ? 128 : 64);
+  const int vpt = (d + bd - 1) / bd;
+#define LB(V) note_launch(), ln_fwd_block<V><<<rows, bd, 0, st>>>(x, gamma, beta, pdt, y, ydt, stats, d, eps)
+  if (vpt <= 1) LB(1); else if (vpt <= 2) LB(2); else if (vpt <= 4) LB(4);
+  else if (vpt <= 8) LB(8); else if (vpt <= 16) LB(16); else LB(32);
+#undef LB
+}
+}
+
+// =============================================================== backward: dx (rows)
+template <int NV>
+__global__ void __launch_bounds__(256) ln_bwd_warp(const float* __restrict__ dout, const float* __restrict__ x,
+                                                   const float2* __restrict__ stats, const void* gamma, DT pdt,
+                                                   const float* __restrict__ resid, float* __restrict__ dx,
+                                                   void* dx_e, DT edt, int rows, int d) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int64_t base = (int64_t)row * d;
+  const float2 sr = stats[row];
+  float4 xh[NV], gh[NV];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = lane * 4 + 128 * k;
+    const float4 xv = *reinterpret_cast<const float4*>(x + base + c);
+    const float4 go = *reinterpret_cast<const float4*>(dout + base + c);
+    const float4 g = ld4(gamma, pdt, c);
+    xh[k] = make_float4((xv.x - sr.x) * sr.y, (xv.y - sr.x) * sr.y, (xv.z - sr.x) * sr.y, (xv.w - sr.x) * sr.y);
+    gh[k] = make_float4(go.x * g.x, go.y * g.y, go.z * g.z, go.w * g.w);
+    s1 += (gh[k].x + gh[k].y) + (gh[k].z + gh[k].w);
+    s2 += (gh[k].x * xh[k].x + gh[k].y * xh[k].y) + (gh[k].z * xh[k].z + gh[k].w * xh[k].w);
+  }
+  const float m1 = warp_sum(s1) / d, m2 = warp_sum(s2) / d;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = lane * 4 + 128 * k;
+    float4 v = make_float4(sr.y * (gh[k].x - m1 - xh[k].x * m2), sr.y * (gh[k].y - m1 - xh[k].y * m2),
+                           sr.y * (gh[k].z - m1 - xh[k].z * m2), sr.y * (gh[k].w - m1 - xh[k].w * m2));
+    if (resid) {
+      const float4 r = *reinterpret_cast<const float4*>(resid + base + c);
+      v.x += r.x; v.y += r.y; v.z += r.z; v.w += r.w;
+    }
+    *reinterpret_cast<float4*>(dx + base + c) = v;
+    if (dx_e) st4(dx_e, edt, base + c, v);
+  }
+}
+
+template <int VPT>
+__global__ void __launch_bounds__(256) ln_bwd_block(const float* __restrict__ dout, const float* __restrict__ x,
+                                                    const float2* __restrict__ stats, const void* gamma, DT pdt,
+                                                    const float* __restrict__ resid, float* __restrict__ dx,
+                                                    void* dx_e, DT edt, int d) {
+  __shared__ float red[64];
+  const int64_t row = blockIdx.x, base = row * d;
+  const float2 sr = stats[row];
+  float xh[VPT], gh[VPT];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    xh[i] = c < d ? (x[base + c] - sr.x) * sr.y : 0.f;
+    gh[i] = c < d ? dout[base + c] * ld_elem(gamma, c, pdt) : 0.f;
+    s1 += gh[i];
+    s2 += gh[i] * xh[i];
+  }
+  const float2 s = block_sum2(s1, s2, red);
+  const float m1 = s.x / d, m2 = s.y / d;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    if (c < d) {
+      float v = sr.y * (gh[i] - m1 - xh[i] * m2);
+      if (resid) v += resid[base + c];
+      dx[base + c] = v;
+      if (dx_e) st_elem(dx_e, base + c, edt, v);
+    }
+  }
+}
+
+// =============================================================== backward: dgamma / dbeta column partials
+constexpr int LN_COL_ROWS = 64;
+int ln_bwd_blocks(int rows) { return (rows + LN_COL_ROWS - 1) / LN_COL_ROWS; }
+
+__global__ void __launch_bounds__(256) ln_col_partial(const float* __restrict__ dout, const float* __restrict__ x,
+                                                      const float2* __restrict__ stats, float* __restrict__ partial,
+                                                      int rows, int d) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= d) return;
+  const int r0 = blockIdx.y * LN_COL_ROWS, r1 = min(rows, r0 + LN_COL_ROWS);
+  float dg = 0.f, db = 0.f;
+#pragma unroll 4
+  for (int r = r0; r < r1; ++r) {
+    const float2 sr = stats[r];
+    const float go = dout[(int64_t)r * d + c];
+    dg += go * ((x[(int64_t)r * d + c] - sr.x) * sr.y);
+    db += go;
+  }
+  partial[(int64_t)blockIdx.y * 2 * d + c] = dg;
+  partial[(int64_t)blockIdx.y * 2 * d + d + c] = db;
+}
+
+int ln_bwd(const float* dout, const float* x, const float2* stats, const void* gamma, DT pdt, const float* resid,
+           float* dx, void* dx_e, DT edt, float* partial, int rows, int d, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  bool done = false;
+  if (d % 128 == 0 && d <= 4096) {
+    const int grid = (rows + 7) / 8;
+    done = true;
+#define LW(N) note_launch(), ln_bwd_warp<N><<<grid, 256, 0, st>>>(dout, x, stats, gamma, pdt, resid, dx, dx_e, edt, rows, d)
+    switch (d / 128) {
+      case 1: LW(1); break; case 2: LW(2); break; case 3: LW(3); break; case 4: LW(4); break;
+      case 5: LW(5); break; case 6: LW(6); break; case 8: LW(8); break; case 12: LW(12); break;
+      case 16: LW(16); break; case 24: LW(24); break; case 32: LW(32); break;
+      default: done = false;
+    }
+#undef LW
+  }
+  if (!done) {
+    const int bd = d >= 1024 ? 256 : (d >= 256 ? 128 : 64);
+    const int vpt = (d + bd - 1) / bd;
+#define LB(V) note_launch(), ln_bwd_block<V><<<rows, bd, 0, st>>>(dout, x, stats, gamma, pdt, resid, dx, dx_e, edt, d)
+    if (vpt <= 1) LB(1); else if (vpt <= 2) LB(2); else if (vpt <= 4) LB(4);
+    else if (vpt <= 8) LB(8); else if (vpt <= 16) LB(16); else LB(32);
+#undef LB
+  }
+  const int nblk = ln_bwd_blocks(rows);
+  dim3 grid((d + 255) / 256, nblk);
+  note_launch(), ln_col_partial<<<grid, 256, 0, st>>>(dout, x, stats, partial, rows, d);
+  return nblk;
+}
+
+// =============================================================== fixed-order finisher
+// out[n] = (acc_in ? acc_in[n] : 0) + sum_k partial[k*pstride + n].  Block = 8 row groups x 32 columns;
+// row group g sums partial rows g, g+8, ... in order; the 8 group sums are added in order g = 0..7.
+__global__ void __launch_bounds__(256) colsum_finish_kernel(const float* __restrict__ partial, int nblk,
+                                                            int64_t pstride, int n, const float* acc_in, void* out,
+                                                            DT out_dt) {
+  __shared__ float red[8][33];
+  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
+  float s = 0.f;
+  if (c < n)
+    for (int k = g; k < nblk; k += 8) s += partial[(int64_t)k * pstride + c];
+  red[g][cl] = s;
+  __syncthreads();
+  if (g == 0 && c < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i][cl];
+    if (acc_in) t += acc_in[c];
+    st_elem(out, c, out_dt, t);
+  }
+}
+
+void colsum_finish(const float* partial, int nblk, int64_t pstride, int n, const float* acc_in, void* out, DT out_dt,
+                   cudaStream_t st) {
+  if (n <= 0) return;
+  note_launch(), colsum_finish_kernel<<<(n + 31) / 32, 256, 0, st>>>(partial, nblk, pstride, n, acc_in, out, out_dt);
+}
+
+}  // namespace lga

@@ -9,134 +9,6 @@
 
 namespace lga {
 
-// =============================================================== LayerNorm forward
-// Block per row; VPT values per thread stay in registers (exact two-pass mean / variance).
-template <int VPT>
-__global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x, const void* gamma,
-                                                     const void* beta, DT pdt, void* y, DT ydt,
-                                                     float2* __restrict__ stats, int d, float eps) {
-  __shared__ float red[64];
-  const int64_t row = blockIdx.x;
-  const float* xr = x + row * d;
-  float v[VPT];
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int c = threadIdx.x + i * blockDim.x;
-    v[i] = c < d ? xr[c] : 0.f;
-    s += v[i];
-  }
-  const float mean = block_sum2(s, 0.f, red).x / d;
-  float q = 0.f;
-#pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int c = threadIdx.x + i * blockDim.x;
-    const float t = c < d ? v[i] - mean : 0.f;
-    q += t * t;
-  }
-  const float var = block_sum2(q, 0.f, red).x / d;
-  const float rstd = rsqrtf(var + eps);
-#pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int c = threadIdx.x + i * blockDim.x;
-    if (c < d) {
-      const float yv = (v[i] - mean) * rstd * ld_elem(gamma, c, pdt) + ld_elem(beta, c, pdt);
-      st_elem(y, row * d + c, ydt, yv);
-    }
-  }
-  if (threadIdx.x == 0) stats[row] = make_float2(mean, rstd);
-}
-
-void ln_fwd(const float* x, const void* gamma, const void* beta, DT pdt, void* y, DT ydt,
-            float2* stats, int rows, int d, float eps, cudaStream_t st) {
-  if (rows <= 0) return;
-  const int bd = d >= 1024 ? 256 : (d >= 256 ? 128 : 64);
-  const int vpt = (d + bd - 1) / bd;
-#define LNF(V) note_launch(), ln_fwd_kernel<V><<<rows, bd, 0, st>>>(x, gamma, beta, pdt, y, ydt, stats, d, eps)
-  if (vpt <= 1) LNF(1); else if (vpt <= 2) LNF(2); else if (vpt <= 4) LNF(4);
-  else if (vpt <= 8) LNF(8); else if (vpt <= 16) LNF(16); else LNF(32);
-#undef LNF
-}
-
-// =============================================================== LayerNorm backward
-// Block handles rows [blk*R, blk*R+R); per row two block reductions; the column partials of
-// dgamma / dbeta accumulate in registers across the block's rows (fixed order).
-constexpr int LN_BWD_ROWS = 32;
-
-int ln_bwd_blocks(int rows) { return (rows + LN_BWD_ROWS - 1) / LN_BWD_ROWS; }
-
-template <int VPT>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ dout, const float* __restrict__ x,
-                                                     const float2* __restrict__ stats, const void* gamma, DT pdt,
-                                                     const float* __restrict__ resid, float* dx, void* dx_e, DT edt,
-                                                     float* __restrict__ partial, int rows, int d) {
-  __shared__ float red[64];
-  float g[VPT], dg[VPT], db[VPT];
-#pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int c = threadIdx.x + i * blockDim.x;
-    g[i] = c < d ? ld_elem(gamma, c, pdt) : 0.f;
-    dg[i] = 0.f; db[i] = 0.f;
-  }
-  const int r0 = blockIdx.x * LN_BWD_ROWS;
-  const int r1 = min(rows, r0 + LN_BWD_ROWS);
-  for (int r = r0; r < r1; ++r) {
-    const float2 sr = stats[r];
-    const int64_t base = (int64_t)r * d;
-    float xh[VPT], dxh[VPT];
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-      const int c = threadIdx.x + i * blockDim.x;
-      if (c < d) {
-        const float go = dout[base + c];
-        xh[i] = (x[base + c] - sr.x) * sr.y;
-        dxh[i] = go * g[i];
-        dg[i] += go * xh[i];
-        db[i] += go;
-      } else {
-        xh[i] = 0.f; dxh[i] = 0.f;
-      }
-      s1 += dxh[i];
-      s2 += dxh[i] * xh[i];
-    }
-    const float2 s = block_sum2(s1, s2, red);
-    const float m1 = s.x / d, m2 = s.y / d;
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-      const int c = threadIdx.x + i * blockDim.x;
-      if (c < d) {
-        float v = sr.y * (dxh[i] - m1 - xh[i] * m2);
-        if (resid) v += resid[base + c];
-        dx[base + c] = v;
-        if (dx_e) st_elem(dx_e, base + c, edt, v);
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int c = threadIdx.x + i * blockDim.x;
-    if (c < d) {
-      partial[(int64_t)blockIdx.x * 2 * d + c] = dg[i];
-      partial[(int64_t)blockIdx.x * 2 * d + d + c] = db[i];
-    }
-  }
-}
-
-int ln_bwd(const float* dout, const float* x, const float2* stats, const void* gamma, DT pdt,
-           const float* resid, float* dx, void* dx_e, DT edt, float* partial, int rows, int d,
-           cudaStream_t st) {
-  const int nblk = ln_bwd_blocks(rows);
-  if (rows <= 0) return 0;
-  const int bd = d >= 1024 ? 256 : (d >= 256 ? 128 : 64);
-  const int vpt = (d + bd - 1) / bd;
-#define LNB(V) note_launch(), ln_bwd_kernel<V><<<nblk, bd, 0, st>>>(dout, x, stats, gamma, pdt, resid, dx, dx_e, edt, partial, rows, d)
-  if (vpt <= 1) LNB(1); else if (vpt <= 2) LNB(2); else if (vpt <= 4) LNB(4);
-  else if (vpt <= 8) LNB(8); else if (vpt <= 16) LNB(16); else LNB(32);
-#undef LNB
-  return nblk;
-}
-
 // =============================================================== column sums
 constexpr int COLSUM_ROWS = 64;
 int colsum_blocks(int rows) { return (rows + COLSUM_ROWS - 1) / COLSUM_ROWS; }
@@ -157,22 +29,6 @@ int colsum_partial(const void* X, DT xdt, int64_t ldx, int rows, int n, float* p
   dim3 grid((n + 255) / 256, nblk);
   note_launch(), colsum_partial_kernel<<<grid, 256, 0, st>>>(X, xdt, ldx, rows, n, partial);
   return nblk;
-}
-
-__global__ void colsum_finish_kernel(const float* __restrict__ partial, int nblk, int64_t pstride, int n,
-                                     const float* acc_in, void* out, DT out_dt) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  float s = 0.f;
-  for (int k = 0; k < nblk; ++k) s += partial[(int64_t)k * pstride + c];
-  if (acc_in) s += acc_in[c];
-  st_elem(out, c, out_dt, s);
-}
-
-void colsum_finish(const float* partial, int nblk, int64_t pstride, int n, const float* acc_in,
-                   void* out, DT out_dt, cudaStream_t st) {
-  if (n <= 0) return;
-  note_launch(), colsum_finish_kernel<<<(n + 255) / 256, 256, 0, st>>>(partial, nblk, pstride, n, acc_in, out, out_dt);
 }
 
 // =============================================================== MSE loss + seed gradient
