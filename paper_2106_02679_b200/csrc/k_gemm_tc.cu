@@ -1,11 +1,17 @@
 // k_gemm_tc.cu -- bf16 GEMM on the 5th-generation tensor cores, sm_100a:
-//   TMA (cp.async.bulk.tensor, 128B swizzle) -> shared memory ring (STAGES deep)
+//   TMA (cp.async.bulk.tensor, 128B swizzle) -> shared-memory ring (STAGES deep)
 //   -> tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN, K=16) issued by one thread, fp32 accumulators in TMEM
-//   -> tcgen05.ld by 4 epilogue warps -> fused epilogue (epilogue.cuh) -> global.
+//   -> tcgen05.ld by 8 epilogue warps -> fused epilogue (epilogue.cuh semantics) -> global.
 // Persistent, warp-specialised: warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 = TMEM allocator,
-// warps 4..7 = epilogue.  Two TMEM accumulator stages so that the epilogue of tile t overlaps the
-// MMAs of tile t+1.  Operands may be K-major or MN-major independently (UMMA descriptor major bit), so
-// forward (X W), dgrad (dY W^T) and wgrad (X^T dY) all read their operands in place -- no transposes.
+// warps 4..11 = epilogue (two per TMEM lane quadrant, each draining half of the tile's columns).  Two TMEM
+// accumulator stages so that the epilogue of tile t overlaps the MMAs of tile t+1.  Operands may be
+// K-major or MN-major independently (UMMA descriptor major bit), so forward (X W), dgrad (dY W^T) and
+// wgrad (X^T dY) all read their operands in place -- no transposes.
+//
+// Epilogue data path (TMA_EPI): each warp owns a 4 KB swizzled staging tile of 32 rows x 32 columns;
+// the residual / accumulator / GELU input is TMA-loaded into it, the results are written back in place
+// and TMA-stored (bulk groups), so global traffic moves in full coalesced boxes instead of one row per
+// thread.  Shapes whose leading dimensions are not 16-byte multiples use the direct per-row path.
 #include "epilogue.cuh"
 #include "tc_common.cuh"
 
@@ -19,21 +25,30 @@ constexpr int BM = 128;
 constexpr int BK = 64;           // 64 bf16 = 128 bytes = one swizzle span
 constexpr int UMMA_K = 16;
 constexpr int EPI_WARP0 = 4;
-constexpr int EPI_WARPS = 8;    // two warps per TMEM lane quadrant, each drains half of the tile's columns
+constexpr int EPI_WARPS = 8;
 constexpr int NUM_THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
+constexpr int EPI_TILE = 32;     // rows and columns of one epilogue staging box
+constexpr int STAGE_EPI = 4096;  // bytes of staging per epilogue warp
 
 template <int BN>
 struct Smem {
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int STAGES = 4;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;   // two accumulator stages
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
+  static constexpr int BAR_OFF = EPI_OFF + EPI_WARPS * STAGE_EPI;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;   // + barriers + alignment slack
 };
 
-// ---- vectorised epilogue of 32 consecutive columns of one row (falls back to scalar at edges)
+// Epilogue tensor maps (TMA path): out (g for GELU fwd), aux out (u for GELU fwd), and one input
+// (residual | accumulator | u for GELU bwd).
+struct EpiMaps {
+  CUtensorMap out, aux, in;
+};
+
+// ---- direct (per-row) epilogue of 32 consecutive columns of one row; also the fallback
 __device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 __device__ __forceinline__ void load32(const void* base, DT t, int64_t idx, float (&x)[32]) {
@@ -67,19 +82,13 @@ __device__ __forceinline__ void store32(void* base, DT t, int64_t idx, const flo
   } else {
     uint4* p = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(base) + idx);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      uint32_t w[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const __nv_bfloat162 b2 = __floats2bfloat162_rn(x[8 * i + 2 * j], x[8 * i + 2 * j + 1]);
-        w[j] = *reinterpret_cast<const uint32_t*>(&b2);
-      }
-      p[i] = make_uint4(w[0], w[1], w[2], w[3]);
-    }
+    for (int i = 0; i < 4; ++i)
+      p[i] = make_uint4(pack_bf16x2(x[8 * i], x[8 * i + 1]), pack_bf16x2(x[8 * i + 2], x[8 * i + 3]),
+                        pack_bf16x2(x[8 * i + 4], x[8 * i + 5]), pack_bf16x2(x[8 * i + 6], x[8 * i + 7]));
   }
 }
 
-__device__ __forceinline__ void epi_chunk(const Epi& e, int64_t m, int64_t n0, int nvalid, float (&v)[32]) {
+__device__ __forceinline__ void epi_chunk_direct(const Epi& e, int64_t m, int64_t n0, int nvalid, float (&v)[32]) {
   bool vec = nvalid == 32 && aligned16(static_cast<char*>(e.out) + (m * e.ldo + n0) * (int64_t)dt_size(e.out_dt));
   if (vec && e.kind == EPI_STORE) {
     if (e.bias) vec = aligned16(static_cast<const char*>(e.bias) + n0 * (int64_t)dt_size(e.bias_dt));
@@ -121,9 +130,48 @@ __device__ __forceinline__ void epi_chunk(const Epi& e, int64_t m, int64_t n0, i
   }
 }
 
-template <int BN, bool A_MN, bool B_MN>
+// ---- staged (TMA) epilogue: one row of a 32 x 32 swizzled staging box
+// fp32 box: 128-byte rows, 128B swizzle (16-byte chunk c of row r at c ^ (r & 7));
+// bf16 box: 64-byte rows, 64B swizzle (chunk c of row r at c ^ ((r >> 1) & 3)).
+__device__ __forceinline__ void stage_read_row(const uint8_t* buf, DT t, int r, float (&x)[32]) {
+  if (t == DT::F32) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float4 q = *reinterpret_cast<const float4*>(buf + r * 128 + ((c ^ (r & 7)) << 4));
+      x[4 * c] = q.x; x[4 * c + 1] = q.y; x[4 * c + 2] = q.z; x[4 * c + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 q = *reinterpret_cast<const uint4*>(buf + r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        x[8 * c + 2 * j] = __uint_as_float(w[j] << 16);
+        x[8 * c + 2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+      }
+    }
+  }
+}
+__device__ __forceinline__ void stage_write_row(uint8_t* buf, DT t, int r, const float (&x)[32]) {
+  if (t == DT::F32) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      *reinterpret_cast<float4*>(buf + r * 128 + ((c ^ (r & 7)) << 4)) =
+          make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      *reinterpret_cast<uint4*>(buf + r * 64 + ((c ^ ((r >> 1) & 3)) << 4)) =
+          make_uint4(pack_bf16x2(x[8 * c], x[8 * c + 1]), pack_bf16x2(x[8 * c + 2], x[8 * c + 3]),
+                     pack_bf16x2(x[8 * c + 4], x[8 * c + 5]), pack_bf16x2(x[8 * c + 6], x[8 * c + 7]));
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, bool TMA_EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs g) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ EpiMaps em, const GemmArgs g) {
   using SM = Smem<BN>;
   constexpr int STAGES = SM::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -132,7 +180,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ebar = tempty + 2;   // [EPI_WARPS] staging-load barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + EPI_WARPS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (g.M + BM - 1) / BM, num_n = (g.N + BN - 1) / BN;
@@ -143,6 +192,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS); }
+    for (int s = 0; s < EPI_WARPS; ++s) mbar_init(&ebar[s], 1);
     mbar_fence_init();
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
@@ -226,8 +276,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp >= EPI_WARP0) {  // ===== epilogue: TMEM -> registers -> fused epilogue -> global
+    const int ew = warp - EPI_WARP0;
     const int q = warp & 3;          // TMEM lane quadrant this warp may access
-    const int half = (warp - EPI_WARP0) >> 2;
+    const int half = ew >> 2;
+    const Epi& e = g.epi;
+    uint8_t* sbuf = smem + SM::EPI_OFF + ew * STAGE_EPI;
+    // staged-path roles of the single input box and the output box(es)
+    const bool has_in = TMA_EPI && (e.res || e.acc_in || e.kind == EPI_GELU_BWD);
+    const DT in_dt = e.kind == EPI_GELU_BWD ? e.aux_dt : DT::F32;
+    const uint32_t in_bytes = EPI_TILE * EPI_TILE * (uint32_t)dt_size(in_dt);
+    uint32_t ephase = 0;
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       int mb, nb;
@@ -236,22 +294,87 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[as], aphase);
       fence_after();
-      const int64_t m = (int64_t)mb * BM + q * 32 + lane;
+      const int m0w = mb * BM + q * 32;           // first row of this warp's 32-row strip
+      const int64_t m = m0w + lane;
       const uint32_t taddr = tmem_base + as * BN + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
       for (int ch = half * (BN / 64); ch < (half + 1) * (BN / 64); ++ch) {
+        const int n0 = nb * BN + ch * 32;
+        if (!TMA_EPI) {
+          float v[32];
+          tmem_ld32(taddr + ch * 32, v);
+          if (m < g.M && n0 < g.N) epi_chunk_direct(e, m, n0, (int)min(32, g.N - n0), v);
+          continue;
+        }
+        if (n0 >= g.N || m0w >= g.M) continue;   // whole box outside the matrix (warp-uniform)
+        // previous TMA store must have finished reading the staging box before it is reused
+        if (lane == 0) {
+          bulk_wait_read0();
+          if (has_in) {
+            mbar_expect_tx(&ebar[ew], in_bytes);
+            tma_load_2d(sbuf, &em.in, &ebar[ew], n0, m0w);
+          }
+        }
+        __syncwarp();
+        uint32_t raw[32];
+        tmem_ld32_nowait(taddr + ch * 32, raw);
+        tmem_wait_ld();
         float v[32];
-        tmem_ld32(taddr + ch * 32, v);
-        const int64_t n0 = (int64_t)nb * BN + ch * 32;
-        if (m < g.M && n0 < g.N) {
-          const int nvalid = (int)(g.N - n0 < 32 ? g.N - n0 : 32);
-          epi_chunk(g.epi, m, n0, nvalid, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]);
+        if (has_in) {
+          mbar_wait(&ebar[ew], ephase);
+          ephase ^= 1;
+        }
+        if (e.kind == EPI_STORE) {
+          if (e.bias) {
+            float b[32];
+            if (n0 + 32 <= g.N) load32(e.bias, e.bias_dt, n0, b);
+            else for (int i = 0; i < 32; ++i) b[i] = n0 + i < g.N ? ld_elem(e.bias, n0 + i, e.bias_dt) : 0.f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += b[i];
+          }
+          if (has_in) {
+            float x[32];
+            stage_read_row(sbuf, DT::F32, lane, x);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += x[i];
+          }
+          stage_write_row(sbuf, e.out_dt, lane, v);
+        } else if (e.kind == EPI_GELU_FWD) {
+          float b[32];
+          if (n0 + 32 <= g.N) load32(e.bias, e.bias_dt, n0, b);
+          else for (int i = 0; i < 32; ++i) b[i] = n0 + i < g.N ? ld_elem(e.bias, n0 + i, e.bias_dt) : 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += b[i];
+          stage_write_row(sbuf, e.aux_dt, lane, v);              // u  -> first 2 KB
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
+          stage_write_row(sbuf + 2048, e.out_dt, lane, v);       // g  -> second 2 KB
+        } else {  // EPI_GELU_BWD: u was TMA-loaded into the box; out overwrites it in place
+          float u[32];
+          stage_read_row(sbuf, in_dt, lane, u);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(u[i]);
+          stage_write_row(sbuf, e.out_dt, lane, v);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          if (e.kind == EPI_GELU_FWD) {
+            tma_store_2d(&em.aux, sbuf, n0, m0w);
+            tma_store_2d(&em.out, sbuf + 2048, n0, m0w);
+          } else {
+            tma_store_2d(&em.out, sbuf, n0, m0w);
+          }
+          bulk_commit();
         }
       }
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
     }
+    if (TMA_EPI && lane == 0) bulk_wait0();
   }
   fence_before();
   __syncthreads();
@@ -262,43 +385,79 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 // ------------------------------------------------------------------ host side
-// 2-D bf16 tensor map: dim0 (contiguous) = inner, dim1 = outer, row stride in elements.
-static cudaError_t make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
-                            uint32_t box_inner, uint32_t box_outer) {
+// 2-D tensor map: dim0 (contiguous) = inner, dim1 = outer, row stride in elements.
+static cudaError_t make_map(CUtensorMap* map, const void* ptr, DT dt, uint64_t inner, uint64_t outer, uint64_t ld,
+                            uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
   auto enc = tcu::tmap_encoder();
   if (!enc) return cudaErrorNotSupported;
-  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 2) & 15)) return cudaErrorMisalignedAddress;
+  const uint64_t es = dt_size(dt);
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * es) & 15)) return cudaErrorMisalignedAddress;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
+  cuuint64_t strides[1] = {ld * es};
   cuuint32_t box[2] = {box_inner, box_outer};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint32_t el[2] = {1, 1};
+  CUresult r = enc(map, dt == DT::F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// 32 x 32 staging-box map of an [M][N] epilogue tensor (f32: 128B swizzle, bf16: 64B swizzle)
+static bool box_map(CUtensorMap* m, const void* ptr, DT dt, int M, int N, int64_t ld) {
+  return make_map(m, ptr, dt, (uint64_t)N, (uint64_t)M, (uint64_t)ld, EPI_TILE, EPI_TILE,
+                  dt == DT::F32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B) == cudaSuccess;
+}
+
+// Build the staged-epilogue maps; false = shape / layout not eligible (use the direct path).
+static bool epi_maps(const GemmArgs& g, EpiMaps* em) {
+  const Epi& e = g.epi;
+  if (e.res && e.acc_in) return false;
+  if (!box_map(&em->out, e.out, e.out_dt, g.M, g.N, e.ldo)) return false;
+  em->aux = em->out;
+  em->in = em->out;
+  if (e.kind == EPI_GELU_FWD) {
+    if (e.aux_dt != DT::BF16 || e.out_dt != DT::BF16) return false;
+    if (!box_map(&em->aux, e.aux, e.aux_dt, g.M, g.N, e.ldaux)) return false;
+  } else if (e.kind == EPI_GELU_BWD) {
+    if (!box_map(&em->in, e.aux, e.aux_dt, g.M, g.N, e.ldaux)) return false;
+  } else if (e.res) {
+    if (!box_map(&em->in, e.res, DT::F32, g.M, g.N, e.ldr)) return false;
+  } else if (e.acc_in) {
+    if (!box_map(&em->in, e.acc_in, DT::F32, g.M, g.N, e.ldacc)) return false;
+  }
+  return true;
+}
+
+template <int BN, bool A_MN, bool B_MN, bool TMA_EPI>
+static cudaError_t launch_k(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const GemmArgs& g,
+                            cudaStream_t st) {
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, TMA_EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::TOTAL);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  const int grid = std::min(tiles, num_sms());
+  note_launch(), kern<<<grid, NUM_THREADS, Smem<BN>::TOTAL, st>>>(ta, tb, em, g);
+  return cudaGetLastError();
 }
 
 template <int BN, bool A_MN, bool B_MN>
 static cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
   CUtensorMap ta, tb;
   cudaError_t e;
-  if (!A_MN) e = make_map(&ta, g.A, g.K, g.M, g.lda, BK, BM);
-  else e = make_map(&ta, g.A, g.M, g.K, g.lda, 64, BK);
+  if (!A_MN) e = make_map(&ta, g.A, DT::BF16, g.K, g.M, g.lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+  else e = make_map(&ta, g.A, DT::BF16, g.M, g.K, g.lda, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B);
   if (e != cudaSuccess) return e;
-  if (!B_MN) e = make_map(&tb, g.B, g.K, g.N, g.ldb, BK, BN);
-  else e = make_map(&tb, g.B, g.N, g.K, g.ldb, 64, BK);
+  if (!B_MN) e = make_map(&tb, g.B, DT::BF16, g.K, g.N, g.ldb, BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+  else e = make_map(&tb, g.B, DT::BF16, g.N, g.K, g.ldb, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B);
   if (e != cudaSuccess) return e;
-  auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::TOTAL);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
-  const int grid = std::min(tiles, num_sms());
-  note_launch(), kern<<<grid, NUM_THREADS, Smem<BN>::TOTAL, st>>>(ta, tb, g);
-  return cudaGetLastError();
+  EpiMaps em;
+  if (epi_maps(g, &em)) return launch_k<BN, A_MN, B_MN, true>(ta, tb, em, g, st);
+  memset(&em, 0, sizeof(em));
+  return launch_k<BN, A_MN, B_MN, false>(ta, tb, em, g, st);
 }
 
 }  // namespace tc
