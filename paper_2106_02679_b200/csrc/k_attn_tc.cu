@@ -36,8 +36,8 @@ struct FwdSmem {
   static constexpr int K_OFF = Q_OFF + TILE;        // 2 stages
   static constexpr int V_OFF = K_OFF + 2 * TILE;    // 2 stages
   static constexpr int P_OFF = V_OFF + 2 * TILE;    // [128][128] bf16 = 2 sub-tiles
-  static constexpr int RED_OFF = P_OFF + 2 * SUB;   // [2 tile parity][2 halves][128 rows] row maxima + [2][128] sums
-  static constexpr int BAR_OFF = RED_OFF + 6 * 128 * 4;
+  static constexpr int RED_OFF = P_OFF + 2 * SUB;   // [2 halves][128 rows] maxima, then [2][128] sums
+  static constexpr int BAR_OFF = RED_OFF + 4 * 128 * 4;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
@@ -52,24 +52,34 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
   uint64_t* v_full = bars + 3;     // [2]
   uint64_t* kv_empty = bars + 5;   // [2]
   uint64_t* s_full = bars + 7;     // [2]
-  uint64_t* s_empty = bars + 9;    // [2]
-  uint64_t* p_full = bars + 11;
-  uint64_t* o_done = bars + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* s_empty = bars + 9;    // [2]   (SM_THREADS arrivals)
+  uint64_t* p_full = bars + 11;    // [2 halves] (SM_THREADS/2 arrivals each)
+  uint64_t* o_done = bars + 13;    // [2 halves]
+  uint64_t* q_empty = bars + 15;   // Q buffer free (all S MMAs of an item done)
+  uint64_t* o_free = bars + 16;    // O accumulators read by the epilogue (SM_THREADS arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqt = gridDim.x;
-  const int qt = a.causal ? nqt - 1 - (int)blockIdx.x : (int)blockIdx.x;   // heavy tiles first
-  const int h = blockIdx.y, sq = blockIdx.z;
   const int s = a.seq, d = a.d;
-  const int q0 = qt * BQ;
+  const int nqt = (s + BQ - 1) / BQ;
+  const int per_q = a.heads * a.nseq;
+  const int n_items = nqt * per_q;
   const int nkv_all = (s + BKV - 1) / BKV;
-  const int nkv = a.causal ? min(nkv_all, (q0 + BQ - 1) / BKV + 1) : nkv_all;
+  // work item t -> (query tile, head, sequence); causal: heaviest query tiles first
+  auto item = [&](int t, int& qt, int& h, int& sq, int& nkv) {
+    const int qi = t / per_q, rem = t % per_q;
+    qt = a.causal ? nqt - 1 - qi : qi;
+    h = rem % a.heads;
+    sq = rem / a.heads;
+    nkv = a.causal ? min(nkv_all, (qt * BQ + BQ - 1) / BKV + 1) : nkv_all;
+  };
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < 14; ++i) {
-      const bool by_softmax = (&bars[i] == s_empty) || (&bars[i] == s_empty + 1) || (&bars[i] == p_full);
-      mbar_init(&bars[i], by_softmax ? SM_THREADS : 1);   // softmax threads arrive individually
+    for (int i = 0; i < 17; ++i) {
+      uint32_t cnt = 1;
+      if (i == 9 || i == 10 || i == 16) cnt = SM_THREADS;
+      if (i == 11 || i == 12) cnt = SM_THREADS / 2;
+      mbar_init(&bars[i], cnt);   // softmax threads arrive individually
     }
     mbar_fence_init();
     prefetch_tmap(&tm);
@@ -80,25 +90,33 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
   fence_after();
   const uint32_t tbase = *tmem_slot;
   const uint32_t t_s[2] = {tbase, tbase + 128};
-  const uint32_t t_o = tbase + 256;
+  const uint32_t t_o[2] = {tbase + 256, tbase + 256 + DH};   // one O accumulator per key half (DH <= 128)
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer
-      mbar_expect_tx(q_full, SM::TILE);
-#pragma unroll
-      for (int i = 0; i < DH / 64; ++i) tma_load_3d(smem + SM::Q_OFF + i * SM::SUB, &tm, q_full, h * DH + 64 * i, q0, sq);
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&k_full[st], SM::TILE);
-#pragma unroll
-        for (int i = 0; i < DH / 64; ++i)
-          tma_load_3d(smem + SM::K_OFF + st * SM::TILE + i * SM::SUB, &tm, &k_full[st], d + h * DH + 64 * i, j * BKV, sq);
-        mbar_expect_tx(&v_full[st], SM::TILE);
+      int jt = 0;     // global KV tile counter (ring stage / phase)
+      int it = 0;
+      for (int t = blockIdx.x; t < n_items; t += gridDim.x, ++it) {
+        int qt, h, sq, nkv;
+        item(t, qt, h, sq, nkv);
+        mbar_wait(q_empty, (it & 1) ^ 1);
+        mbar_expect_tx(q_full, SM::TILE);
 #pragma unroll
         for (int i = 0; i < DH / 64; ++i)
-          tma_load_3d(smem + SM::V_OFF + st * SM::TILE + i * SM::SUB, &tm, &v_full[st], 2 * d + h * DH + 64 * i,
-                      j * BKV, sq);
+          tma_load_3d(smem + SM::Q_OFF + i * SM::SUB, &tm, q_full, h * DH + 64 * i, qt * BQ, sq);
+        for (int j = 0; j < nkv; ++j, ++jt) {
+          const int st = jt & 1;
+          mbar_wait(&kv_empty[st], ((jt >> 1) & 1) ^ 1);
+          mbar_expect_tx(&k_full[st], SM::TILE);
+#pragma unroll
+          for (int i = 0; i < DH / 64; ++i)
+            tma_load_3d(smem + SM::K_OFF + st * SM::TILE + i * SM::SUB, &tm, &k_full[st], d + h * DH + 64 * i, j * BKV, sq);
+          mbar_expect_tx(&v_full[st], SM::TILE);
+#pragma unroll
+          for (int i = 0; i < DH / 64; ++i)
+            tma_load_3d(smem + SM::V_OFF + st * SM::TILE + i * SM::SUB, &tm, &v_full[st], 2 * d + h * DH + 64 * i,
+                        j * BKV, sq);
+        }
       }
     }
   } else if (warp == 1) {
@@ -107,133 +125,167 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
       constexpr uint32_t idesc_o = make_idesc(128, DH, false, true);
       const uint32_t sQ = smem_u32(smem + SM::Q_OFF);
       const uint32_t sP = smem_u32(smem + SM::P_OFF);
-      mbar_wait(q_full, 0);
-      for (int j = 0; j <= nkv; ++j) {
-        if (j < nkv) {
-          const int st = j & 1, b = j & 1;
-          mbar_wait(&k_full[st], (j >> 1) & 1);
-          mbar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);
-          fence_after();
-          const uint32_t sK = smem_u32(smem + SM::K_OFF + st * SM::TILE);
+      int js = 0;   // global S / KV tile counter
+      int it = 0;
+      for (int t = blockIdx.x; t < n_items; t += gridDim.x, ++it) {
+        int qt, h, sq, nkv;
+        item(t, qt, h, sq, nkv);
+        mbar_wait(q_full, it & 1);
+        const int j0 = js;   // global index of this item's first tile
+        for (int j = 0; j <= nkv; ++j) {
+          if (j < nkv) {
+            const int g = j0 + j, st = g & 1, b = g & 1;
+            mbar_wait(&k_full[st], (g >> 1) & 1);
+            mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
+            fence_after();
+            const uint32_t sK = smem_u32(smem + SM::K_OFF + st * SM::TILE);
 #pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * SM::SUB + (kk & 3) * 32;
-            umma_f16(t_s[b], make_desc(sQ + off, 16, 1024), make_desc(sK + off, 16, 1024), idesc_s, kk > 0);
+            for (int kk = 0; kk < DH / 16; ++kk) {
+              const uint32_t off = (kk >> 2) * SM::SUB + (kk & 3) * 32;
+              umma_f16(t_s[b], make_desc(sQ + off, 16, 1024), make_desc(sK + off, 16, 1024), idesc_s, kk > 0);
+            }
+            umma_commit(&s_full[b]);
+            if (j == nkv - 1) umma_commit(q_empty);   // Q no longer needed by this item
           }
-          umma_commit(&s_full[b]);
-        }
-        if (j >= 1) {
-          const int jj = j - 1, st = jj & 1;
-          mbar_wait(p_full, jj & 1);
-          mbar_wait(&v_full[st], (jj >> 1) & 1);
-          fence_after();
-          const uint32_t sV = smem_u32(smem + SM::V_OFF + st * SM::TILE);
+          if (j >= 1) {
+            const int jj = j - 1, g = j0 + jj, st = g & 1;
+            if (jj == 0) mbar_wait(o_free, (it & 1) ^ 1);   // previous item's epilogue has read O
+            mbar_wait(&v_full[st], (g >> 1) & 1);
+            const uint32_t sV = smem_u32(smem + SM::V_OFF + st * SM::TILE);
 #pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk) {
-            const uint64_t ad = make_desc(sP + (kk >> 2) * SM::SUB + (kk & 3) * 32, 16, 1024);
-            const uint64_t bd = make_desc(sV + kk * 16 * 128, SM::SUB, 1024);   // MN-major: d_h blocks at 16 KB
-            umma_f16(t_o, ad, bd, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
+            for (int hh = 0; hh < 2; ++hh) {   // O_h += P_h V_h over keys 64h .. 64h+63
+              mbar_wait(&p_full[hh], g & 1);
+              fence_after();
+#pragma unroll
+              for (int kk = 4 * hh; kk < 4 * hh + 4; ++kk) {
+                const uint64_t ad = make_desc(sP + hh * SM::SUB + (kk & 3) * 32, 16, 1024);
+                const uint64_t bd = make_desc(sV + kk * 16 * 128, SM::SUB, 1024);   // MN-major: d_h blocks at 16 KB
+                umma_f16(t_o[hh], ad, bd, idesc_o, (jj > 0 || kk > 4 * hh) ? 1u : 0u);
+              }
+              umma_commit(&o_done[hh]);
+            }
+            umma_commit(&kv_empty[st]);
           }
-          umma_commit(o_done);
-          umma_commit(&kv_empty[st]);
         }
+        js += nkv;
       }
     }
-  } else if (warp >= 4) {  // ===== softmax + epilogue: one query row per thread pair (two column halves)
+  } else if (warp >= 4) {  // ===== softmax + epilogue: one query row and one key half per thread
     const int qd = warp & 3;
-    const int hf = (warp - 4) >> 2;            // key-column half / O-column half this warp owns
+    const int hf = (warp - 4) >> 2;            // key half of every tile this warp owns
     const int r = qd * 32 + lane;
-    const int q = q0 + r;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const float sl2 = a.scale * LOG2E;
     uint8_t* sP = smem + SM::P_OFF + hf * SM::SUB;   // this half's [128][64] P sub-tile
-    float* red = reinterpret_cast<float*>(smem + SM::RED_OFF);   // [2 parity][2 halves][128]
-    float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
-      fence_after();
-      uint32_t raw[2][32];
-      tmem_ld32_nowait(t_s[b] + lane_off + hf * 64, raw[0]);
-      tmem_ld32_nowait(t_s[b] + lane_off + hf * 64 + 32, raw[1]);
-      tmem_wait_ld();
-      fence_before();
-      mbar_arrive(&s_empty[b]);
-      const int k0 = j * BKV + hf * 64;
-      float sv[64];
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const int kj = k0 + c;
-        float v = __uint_as_float(raw[c >> 5][c & 31]) * sl2;
-        if (kj >= s || (a.causal && kj > q)) v = -INFINITY;
-        sv[c] = v;
-        mx = fmaxf(mx, v);
-      }
-      // row max over both halves: exchange through shared memory (buffer parity j&1 avoids a WAR race)
-      red[((j & 1) * 2 + hf) * 128 + r] = mx;
-      asm volatile("bar.sync 1, %0;" ::"n"(SM_THREADS) : "memory");
-      mx = fmaxf(mx, red[((j & 1) * 2 + (hf ^ 1)) * 128 + r]);
-      const float m_new = (mx > m_used + RESCALE_THRESHOLD) ? mx : m_used;
-      float rs = 0.f;
-      uint32_t pk[32];
-#pragma unroll
-      for (int c = 0; c < 64; c += 2) {
-        const float p0 = m_new == -INFINITY ? 0.f : exp2f(sv[c] - m_new);
-        const float p1 = m_new == -INFINITY ? 0.f : exp2f(sv[c + 1] - m_new);
-        rs += p0 + p1;
-        pk[c / 2] = pack_bf16x2(p0, p1);
-      }
-      if (j >= 1) {
-        mbar_wait(o_done, (j - 1) & 1);   // PV_{j-1} done: O stable, P buffer free
+    float* red = reinterpret_cast<float*>(smem + SM::RED_OFF);
+    int gt = 0;   // global tile counter
+    for (int t = blockIdx.x; t < n_items; t += gridDim.x) {
+      int qt, h, sq, nkv;
+      item(t, qt, h, sq, nkv);
+      const int q0 = qt * BQ, q = q0 + r;
+      float m_used = -INFINITY, l = 0.f;        // running max (log2 units) and sum of this half
+      for (int j = 0; j < nkv; ++j, ++gt) {
+        const int b = gt & 1;
+        mbar_wait(&s_full[b], (gt >> 1) & 1);
         fence_after();
-      }
-      float scale = 1.f;
-      if (m_new != m_used && m_used != -INFINITY) {   // lazy rescale of this half's O columns
-        scale = exp2f(m_used - m_new);
-#pragma unroll 1
-        for (int c = hf * (DH / 64); c < (hf + 1) * (DH / 64); ++c) {
-          float t[32];
-          tmem_ld32(t_o + lane_off + c * 32, t);
+        uint32_t raw[2][32];
+        tmem_ld32_nowait(t_s[b] + lane_off + hf * 64, raw[0]);
+        tmem_ld32_nowait(t_s[b] + lane_off + hf * 64 + 32, raw[1]);
+        tmem_wait_ld();
+        fence_before();
+        mbar_arrive(&s_empty[b]);
+        const int k0 = j * BKV + hf * 64;
+        // masking only where a key can be past the sequence end or after the query (uniform per warp)
+        const bool need_mask = (k0 + 64 > s) || (a.causal && k0 + 63 > q0 + qd * 32);
+        float sv[64];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) t[i] *= scale;
-          tmem_st32(t_o + lane_off + c * 32, t);
+        for (int c = 0; c < 64; ++c) sv[c] = __uint_as_float(raw[c >> 5][c & 31]);
+        if (need_mask) {
+          const int lim = a.causal ? min(s - 1, q) - k0 : s - 1 - k0;   // last unmasked column
+#pragma unroll
+          for (int c = 0; c < 64; ++c)
+            if (c > lim) sv[c] = -INFINITY;
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 64; ++c) mx = fmaxf(mx, sv[c]);
+        mx *= sl2;
+        const float m_new = (mx > m_used + RESCALE_THRESHOLD) ? mx : m_used;
+        const float moff = m_new == -INFINITY ? 0.f : -m_new;   // fully masked so far: every p is 2^-inf = 0
+        float rs = 0.f;
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {
+          const float p0 = ex2(fmaf(sv[c], sl2, moff));
+          const float p1 = ex2(fmaf(sv[c + 1], sl2, moff));
+          rs += p0 + p1;
+          pk[c / 2] = pack_bf16x2(p0, p1);
+        }
+        if (j >= 1) {
+          mbar_wait(&o_done[hf], (gt - 1) & 1);   // PV of the previous tile done: O_h stable, P_h buffer free
+          fence_after();
+        }
+        float scale = 1.f;
+        if (m_new != m_used && m_used != -INFINITY) {   // lazy rescale of this half's accumulator row
+          scale = ex2(m_used - m_new);
+#pragma unroll 1
+          for (int c = 0; c < DH / 32; ++c) {
+            float tt[32];
+            tmem_ld32(t_o[hf] + lane_off + c * 32, tt);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) tt[i] *= scale;
+            tmem_st32(t_o[hf] + lane_off + c * 32, tt);
+          }
+        }
+        l = l * scale + rs;
+        m_used = m_new;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          const uint32_t addr = smem_u32(sP) + sw128(r, ch);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[ch * 4]), "r"(pk[ch * 4 + 1]),
+                       "r"(pk[ch * 4 + 2]), "r"(pk[ch * 4 + 3])
+                       : "memory");
+        }
+        fence_proxy_async();
+        fence_before();
+        mbar_arrive(&p_full[hf]);
+      }
+      // epilogue: combine the halves, o = (2^(m0-m) O_0 + 2^(m1-m) O_1) / (2^(m0-m) l_0 + 2^(m1-m) l_1)
+      red[hf * 128 + r] = m_used;
+      red[256 + hf * 128 + r] = l;
+      asm volatile("bar.sync 1, %0;" ::"n"(SM_THREADS) : "memory");
+      const float m_o = red[(hf ^ 1) * 128 + r], l_o = red[256 + (hf ^ 1) * 128 + r];
+      asm volatile("bar.sync 1, %0;" ::"n"(SM_THREADS) : "memory");   // red reusable by the next item
+      const float m0 = hf == 0 ? m_used : m_o, m1 = hf == 0 ? m_o : m_used;
+      const float l0 = hf == 0 ? l : l_o, l1 = hf == 0 ? l_o : l;
+      const float mm = fmaxf(m0, m1);
+      const float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - mm), f1 = m1 == -INFINITY ? 0.f : ex2(m1 - mm);
+      const float lt = f0 * l0 + f1 * l1;
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      mbar_wait(&o_done[0], (gt - 1) & 1);
+      mbar_wait(&o_done[1], (gt - 1) & 1);
+      fence_after();
+      __nv_bfloat16* og = static_cast<__nv_bfloat16*>(a.o) + ((int64_t)sq * s + q) * d + h * DH;
+#pragma unroll 1
+      for (int c = hf * (DH / 64); c < (hf + 1) * (DH / 64); ++c) {   // this thread's half of the O columns
+        float t0[32], t1[32];
+        tmem_ld32(t_o[0] + lane_off + c * 32, t0);
+        tmem_ld32(t_o[1] + lane_off + c * 32, t1);
+        if (q < s) {
+          float tt[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) tt[i] = (f0 * t0[i] + f1 * t1[i]) * inv;
+          uint4* dst = reinterpret_cast<uint4*>(og + c * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(pack_bf16x2(tt[8 * i], tt[8 * i + 1]), pack_bf16x2(tt[8 * i + 2], tt[8 * i + 3]),
+                                pack_bf16x2(tt[8 * i + 4], tt[8 * i + 5]), pack_bf16x2(tt[8 * i + 6], tt[8 * i + 7]));
         }
       }
-      l = l * scale + rs;   // partial row sum over this half's keys
-      m_used = m_new;
-#pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        const uint32_t addr = smem_u32(sP) + sw128(r, ch);
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[ch * 4]), "r"(pk[ch * 4 + 1]),
-                     "r"(pk[ch * 4 + 2]), "r"(pk[ch * 4 + 3])
-                     : "memory");
-      }
-      fence_proxy_async();
+      if (q < s && hf == 0) a.lse[((int64_t)sq * a.heads + h) * s + q] = (mm + log2f(lt)) * 0.6931471805599453f;
       fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(o_free);
     }
-    // epilogue: l = sum of both halves; O / l -> bf16 global (each half writes its O columns), lse
-    red[4 * 128 + hf * 128 + r] = l;
-    asm volatile("bar.sync 1, %0;" ::"n"(SM_THREADS) : "memory");
-    l += red[4 * 128 + (hf ^ 1) * 128 + r];
-    mbar_wait(o_done, (nkv - 1) & 1);
-    fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* og = static_cast<__nv_bfloat16*>(a.o) + ((int64_t)sq * s + q) * d + h * DH;
-#pragma unroll 1
-    for (int c = hf * (DH / 64); c < (hf + 1) * (DH / 64); ++c) {
-      float t[32];
-      tmem_ld32(t_o + lane_off + c * 32, t);
-      if (q < s) {
-        uint4* dst = reinterpret_cast<uint4*>(og + c * 32);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dst[i] = make_uint4(pack_bf16x2(t[8 * i] * inv, t[8 * i + 1] * inv), pack_bf16x2(t[8 * i + 2] * inv, t[8 * i + 3] * inv),
-                              pack_bf16x2(t[8 * i + 4] * inv, t[8 * i + 5] * inv), pack_bf16x2(t[8 * i + 6] * inv, t[8 * i + 7] * inv));
-      }
-    }
-    if (q < s && hf == 0) a.lse[((int64_t)sq * a.heads + h) * s + q] = (m_used + log2f(l)) * 0.6931471805599453f;
   }
   fence_before();
   __syncthreads();
@@ -254,8 +306,8 @@ static cudaError_t run_fwd(const AttnArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     set = true;
   }
-  dim3 grid((a.seq + BQ - 1) / BQ, a.heads, a.nseq);
-  note_launch(), fwd_kernel<DH><<<grid, NT, FwdSmem<DH>::TOTAL, st>>>(tm, a);
+  const int items = ((a.seq + BQ - 1) / BQ) * a.heads * a.nseq;
+  note_launch(), fwd_kernel<DH><<<std::min(items, num_sms()), NT, FwdSmem<DH>::TOTAL, st>>>(tm, a);
   return cudaGetLastError();
 }
 

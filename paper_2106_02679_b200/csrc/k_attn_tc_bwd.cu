@@ -81,9 +81,10 @@ struct DkvSmem {
   static constexpr int QT = DH / 64 * SUB64;           // Q (or dO) tile [64][DH]
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = K_OFF + KT;
-  static constexpr int Q_OFF = V_OFF + KT;             // [2]
-  static constexpr int G_OFF = Q_OFF + 2 * QT;         // dO [2]
-  static constexpr int PT_OFF = G_OFF + 2 * QT;        // P^T [128][64]
+  static constexpr int NST = 3;                        // Q / dO ring depth
+  static constexpr int Q_OFF = V_OFF + KT;             // [NST]
+  static constexpr int G_OFF = Q_OFF + NST * QT;       // dO [NST]
+  static constexpr int PT_OFF = G_OFF + NST * QT;      // P^T [128][64]
   static constexpr int DST_OFF = PT_OFF + SUB128;      // dS^T [128][64]
   static constexpr int LD_OFF = DST_OFF + SUB128;      // lse[2][64], dsum[2][64] (floats)
   static constexpr int BAR_OFF = LD_OFF + 4 * 64 * 4;
@@ -98,14 +99,16 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+  constexpr int NST = SM::NST;
   uint64_t* kv_full = bars + 0;
-  uint64_t* q_full = bars + 1;   // [2]
-  uint64_t* q_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;   // [2]
-  uint64_t* s_empty = bars + 7;  // [2] (128 arrivals)
-  uint64_t* p_full = bars + 9;   // (128 arrivals)
-  uint64_t* g_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* q_full = bars + 1;              // [NST]
+  uint64_t* q_empty = q_full + NST;         // [NST]
+  uint64_t* s_full = q_empty + NST;         // [2]
+  uint64_t* s_empty = s_full + 2;           // [2] (EW_THREADS arrivals)
+  uint64_t* p_full = s_empty + 2;           // (EW_THREADS arrivals)
+  uint64_t* g_done = p_full + 1;
+  constexpr int NBAR = 2 * NST + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
   float* lse_s = reinterpret_cast<float*>(smem + SM::LD_OFF);   // [2][64]
   float* dsum_s = lse_s + 128;                                   // [2][64]
 
@@ -119,7 +122,10 @@ __global__ void __launch_bounds__(NT, 1)
   const int64_t rb = ((int64_t)sq * a.heads + h) * s;   // row base of lse / dsum
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < 11; ++i) mbar_init(&bars[i], (i == 7 || i == 8 || i == 9) ? EW_THREADS : 1);
+    for (int i = 0; i < NBAR; ++i) {
+      const bool ew = &bars[i] == s_empty || &bars[i] == s_empty + 1 || &bars[i] == p_full;
+      mbar_init(&bars[i], ew ? EW_THREADS : 1);
+    }
     mbar_fence_init();
     prefetch_tmap(&tm_kv);
     prefetch_tmap(&tm_q);
@@ -142,9 +148,9 @@ __global__ void __launch_bounds__(NT, 1)
         tma_load_3d(smem + SM::V_OFF + i * SM::SUB128, &tm_kv, kv_full, 2 * d + h * DH + 64 * i, k0, sq);
       }
       for (int i = 0; i < nq; ++i) {
-        const int st = i & 1;
+        const int st = i % NST;
         const int q0 = (qstart + i) * QB;
-        mbar_wait(&q_empty[st], ((i >> 1) & 1) ^ 1);
+        mbar_wait(&q_empty[st], ((i / NST) & 1) ^ 1);
         mbar_expect_tx(&q_full[st], 2 * SM::QT);
 #pragma unroll
         for (int c = 0; c < DH / 64; ++c) {
@@ -162,8 +168,8 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_wait(kv_full, 0);
       for (int i = 0; i <= nq; ++i) {
         if (i < nq) {
-          const int st = i & 1, b = i & 1;
-          mbar_wait(&q_full[st], (i >> 1) & 1);
+          const int st = i % NST, b = i & 1;
+          mbar_wait(&q_full[st], (i / NST) & 1);
           mbar_wait(&s_empty[b], ((i >> 1) & 1) ^ 1);
           fence_after();
           const uint32_t sQ = smem_u32(smem + SM::Q_OFF + st * SM::QT);
@@ -177,7 +183,7 @@ __global__ void __launch_bounds__(NT, 1)
           umma_commit(&s_full[b]);
         }
         if (i >= 1) {
-          const int ii = i - 1, st = ii & 1;
+          const int ii = i - 1, st = ii % NST;
           mbar_wait(p_full, ii & 1);
           fence_after();
           const uint32_t sQ = smem_u32(smem + SM::Q_OFF + st * SM::QT);
@@ -205,7 +211,16 @@ __global__ void __launch_bounds__(NT, 1)
     const float sl2 = a.scale * LOG2E;
     uint8_t* sPt = smem + SM::PT_OFF;
     uint8_t* sDSt = smem + SM::DST_OFF;
+    // lse (log2 units) / dsum of query tile i: loaded one iteration ahead into a register by threads
+    // tid < 128, parked in shared buffer i&1 at the end of iteration i-1 (barrier at the top of i)
+    auto ld_stat = [&](int i) -> float {
+      const int q = (qstart + i) * QB + (tid & 63);
+      if (tid >= 128 || i >= nq || q >= s) return 0.f;
+      return tid < 64 ? a.lse[rb + q] * LOG2E : a.dsum[rb + q];
+    };
+    if (tid < 128) (tid < 64 ? lse_s : dsum_s)[tid & 63] = ld_stat(0);
     for (int i = 0; i < nq; ++i) {
+      const float pre = ld_stat(i + 1);
       const int b = i & 1, st = i & 1;
       const int q0 = (qstart + i) * QB;
       mbar_wait(&s_full[b], (i >> 1) & 1);
@@ -216,25 +231,29 @@ __global__ void __launch_bounds__(NT, 1)
       tmem_wait_ld();
       fence_before();
       mbar_arrive(&s_empty[b]);
-      // lse (log2 units) and dsum of this query tile -> shared memory
-      if (tid < 128) {
-        const int t = tid & 63, q = q0 + t;
-        float v = 0.f;
-        if (q < s) v = tid < 64 ? a.lse[rb + q] * LOG2E : a.dsum[rb + q];
-        (tid < 64 ? lse_s : dsum_s)[st * 64 + t] = v;
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(EW_THREADS) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(EW_THREADS) : "memory");   // tile i's lse / dsum visible
       const float* ls = lse_s + st * 64 + hf * 32;
       const float* ds_ = dsum_s + st * 64 + hf * 32;
       uint32_t pp[16], pd[16];
+      // valid iff q < s, kj < s and (causal) kj <= q; only tiles touching the diagonal / the end mask
+      const int qa = q0 + hf * 32;
+      const bool need_mask = kj >= s || qa + 32 > s || (a.causal && kj > qa);
+      float sc[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -ls[c]);
+      if (need_mask) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int q = qa + c;
+          if (!(q < s && kj < s && (!a.causal || kj <= q))) sc[c] = -INFINITY;
+        }
+      }
 #pragma unroll
       for (int c = 0; c < 32; c += 2) {
         float p[2], g[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int q = q0 + hf * 32 + c + e;
-          const bool valid = q < s && kj < s && (!a.causal || kj <= q);
-          p[e] = valid ? exp2f(__uint_as_float(rsv[c + e]) * sl2 - ls[c + e]) : 0.f;
+          p[e] = ex2(sc[c + e]);
           g[e] = p[e] * (__uint_as_float(rdp[c + e]) - ds_[c + e]) * a.scale;
         }
         pp[c / 2] = pack_bf16x2(p[0], p[1]);
@@ -249,6 +268,7 @@ __global__ void __launch_bounds__(NT, 1)
       fence_proxy_async();
       fence_before();
       mbar_arrive(p_full);
+      if (tid < 128) (tid < 64 ? lse_s : dsum_s)[(st ^ 1) * 64 + (tid & 63)] = pre;   // tile i+1
     }
     mbar_wait(g_done, (nq - 1) & 1);
     fence_after();
@@ -276,9 +296,10 @@ struct DqSmem {
   static constexpr int KT = DH / 64 * SUB64;    // K (or V) [64][DH]
   static constexpr int Q_OFF = 0;
   static constexpr int G_OFF = Q_OFF + QT;
-  static constexpr int K_OFF = G_OFF + QT;      // [2]
-  static constexpr int V_OFF = K_OFF + 2 * KT;  // [2]
-  static constexpr int DS_OFF = V_OFF + 2 * KT; // dS [128][64]
+  static constexpr int NST = 3;                 // K / V ring depth
+  static constexpr int K_OFF = G_OFF + QT;      // [NST]
+  static constexpr int V_OFF = K_OFF + NST * KT;  // [NST]
+  static constexpr int DS_OFF = V_OFF + NST * KT; // dS [128][64]
   static constexpr int BAR_OFF = DS_OFF + SUB128;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
@@ -291,14 +312,16 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+  constexpr int NST = SM::NST;
   uint64_t* qg_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* s_empty = bars + 7;   // [2] (128)
-  uint64_t* p_full = bars + 9;    // (128)
-  uint64_t* g_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* kv_full = bars + 1;             // [NST]
+  uint64_t* kv_empty = kv_full + NST;       // [NST]
+  uint64_t* s_full = kv_empty + NST;        // [2]
+  uint64_t* s_empty = s_full + 2;           // [2] (EW_THREADS)
+  uint64_t* p_full = s_empty + 2;           // (EW_THREADS)
+  uint64_t* g_done = p_full + 1;
+  constexpr int NBAR = 2 * NST + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqt = gridDim.x;
@@ -310,7 +333,10 @@ __global__ void __launch_bounds__(NT, 1)
   const int nk = (kend + KB2 - 1) / KB2;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < 11; ++i) mbar_init(&bars[i], (i == 7 || i == 8 || i == 9) ? EW_THREADS : 1);
+    for (int i = 0; i < NBAR; ++i) {
+      const bool ew = &bars[i] == s_empty || &bars[i] == s_empty + 1 || &bars[i] == p_full;
+      mbar_init(&bars[i], ew ? EW_THREADS : 1);
+    }
     mbar_fence_init();
     prefetch_tmap(&tm_q);
     prefetch_tmap(&tm_g);
@@ -333,8 +359,8 @@ __global__ void __launch_bounds__(NT, 1)
         tma_load_3d(smem + SM::G_OFF + c * SM::SUB128, &tm_g, qg_full, h * DH + 64 * c, q0, sq);
       }
       for (int j = 0; j < nk; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        const int st = j % NST;
+        mbar_wait(&kv_empty[st], ((j / NST) & 1) ^ 1);
         mbar_expect_tx(&kv_full[st], 2 * SM::KT);
 #pragma unroll
         for (int c = 0; c < DH / 64; ++c) {
@@ -353,8 +379,8 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_wait(qg_full, 0);
       for (int j = 0; j <= nk; ++j) {
         if (j < nk) {
-          const int st = j & 1, b = j & 1;
-          mbar_wait(&kv_full[st], (j >> 1) & 1);
+          const int st = j % NST, b = j & 1;
+          mbar_wait(&kv_full[st], (j / NST) & 1);
           mbar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);
           fence_after();
           const uint32_t sK = smem_u32(smem + SM::K_OFF + st * SM::KT);
@@ -368,7 +394,7 @@ __global__ void __launch_bounds__(NT, 1)
           umma_commit(&s_full[b]);
         }
         if (j >= 1) {
-          const int jj = j - 1, st = jj & 1;
+          const int jj = j - 1, st = jj % NST;
           mbar_wait(p_full, jj & 1);
           fence_after();
           const uint32_t sK = smem_u32(smem + SM::K_OFF + st * SM::KT);
@@ -403,16 +429,23 @@ __global__ void __launch_bounds__(NT, 1)
       fence_before();
       mbar_arrive(&s_empty[b]);
       uint32_t pd[16];
+      const int ka = j * KB2 + hf * 32;
+      const bool need_mask = q >= s || ka + 32 > s || (a.causal && ka + 31 > q0 + qd * 32);
+      float sc[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -lse2);
+      if (need_mask) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int kj = ka + c;
+          if (!(q < s && kj < s && (!a.causal || kj <= q))) sc[c] = -INFINITY;
+        }
+      }
 #pragma unroll
       for (int c = 0; c < 32; c += 2) {
         float g[2];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int kj = j * KB2 + hf * 32 + c + e;
-          const bool valid = q < s && kj < s && (!a.causal || kj <= q);
-          const float p = valid ? exp2f(__uint_as_float(rsv[c + e]) * sl2 - lse2) : 0.f;
-          g[e] = p * (__uint_as_float(rdp[c + e]) - Dq) * a.scale;
-        }
+        for (int e = 0; e < 2; ++e) g[e] = ex2(sc[c + e]) * (__uint_as_float(rdp[c + e]) - Dq) * a.scale;
         pd[c / 2] = pack_bf16x2(g[0], g[1]);
       }
       if (j >= 1) {
