@@ -119,6 +119,8 @@ generic : {
 }
 
 // =============================================================== backward: dx (rows)
+// Two passes over the row (the second hits L2): pass 1 accumulates sum(dxhat) and sum(dxhat xhat),
+// pass 2 recomputes dxhat, xhat and writes dx.  No row kept in registers -> full occupancy.
 template <int NV>
 __global__ void __launch_bounds__(256) ln_bwd_warp(const float* __restrict__ dout, const float* __restrict__ x,
                                                    const float2* __restrict__ stats, const void* gamma, DT pdt,
@@ -128,25 +130,28 @@ __global__ void __launch_bounds__(256) ln_bwd_warp(const float* __restrict__ dou
   if (row >= rows) return;
   const int64_t base = (int64_t)row * d;
   const float2 sr = stats[row];
-  float4 xh[NV], gh[NV];
   float s1 = 0.f, s2 = 0.f;
-#pragma unroll
+#pragma unroll 4
   for (int k = 0; k < NV; ++k) {
     const int c = lane * 4 + 128 * k;
     const float4 xv = *reinterpret_cast<const float4*>(x + base + c);
     const float4 go = *reinterpret_cast<const float4*>(dout + base + c);
     const float4 g = ld4(gamma, pdt, c);
-    xh[k] = make_float4((xv.x - sr.x) * sr.y, (xv.y - sr.x) * sr.y, (xv.z - sr.x) * sr.y, (xv.w - sr.x) * sr.y);
-    gh[k] = make_float4(go.x * g.x, go.y * g.y, go.z * g.z, go.w * g.w);
-    s1 += (gh[k].x + gh[k].y) + (gh[k].z + gh[k].w);
-    s2 += (gh[k].x * xh[k].x + gh[k].y * xh[k].y) + (gh[k].z * xh[k].z + gh[k].w * xh[k].w);
+    const float g0 = go.x * g.x, g1 = go.y * g.y, g2 = go.z * g.z, g3 = go.w * g.w;
+    s1 += (g0 + g1) + (g2 + g3);
+    s2 += (g0 * (xv.x - sr.x) + g1 * (xv.y - sr.x)) + (g2 * (xv.z - sr.x) + g3 * (xv.w - sr.x));
   }
-  const float m1 = warp_sum(s1) / d, m2 = warp_sum(s2) / d;
-#pragma unroll
+  const float m1 = warp_sum(s1) / d, m2 = warp_sum(s2) * sr.y / d;
+#pragma unroll 4
   for (int k = 0; k < NV; ++k) {
     const int c = lane * 4 + 128 * k;
-    float4 v = make_float4(sr.y * (gh[k].x - m1 - xh[k].x * m2), sr.y * (gh[k].y - m1 - xh[k].y * m2),
-                           sr.y * (gh[k].z - m1 - xh[k].z * m2), sr.y * (gh[k].w - m1 - xh[k].w * m2));
+    const float4 xv = *reinterpret_cast<const float4*>(x + base + c);
+    const float4 go = *reinterpret_cast<const float4*>(dout + base + c);
+    const float4 g = ld4(gamma, pdt, c);
+    float4 v = make_float4(sr.y * (go.x * g.x - m1 - (xv.x - sr.x) * sr.y * m2),
+                           sr.y * (go.y * g.y - m1 - (xv.y - sr.x) * sr.y * m2),
+                           sr.y * (go.z * g.z - m1 - (xv.z - sr.x) * sr.y * m2),
+                           sr.y * (go.w * g.w - m1 - (xv.w - sr.x) * sr.y * m2));
     if (resid) {
       const float4 r = *reinterpret_cast<const float4*>(resid + base + c);
       v.x += r.x; v.y += r.y; v.z += r.z; v.w += r.w;
