@@ -168,6 +168,115 @@ __device__ __forceinline__ void stage_write_row(uint8_t* buf, DT t, int r, const
   }
 }
 
+// Epilogue warps (EPI_WARP0 ..): for every tile of this CTA, wait for the accumulator stage, drain it
+// from TMEM through the fused epilogue, release the stage (`release(as)`).  Rows of a tile start at
+// mb * tile_m + m_off (m_off = the CTA's half of a CTA-pair tile).
+template <int BN, bool TMA_EPI, typename Coords, typename Release>
+__device__ __forceinline__ void epilogue_loop(const GemmArgs& g, const EpiMaps& em, uint8_t* smem_epi, uint64_t* ebar,
+                                              uint64_t* tfull, uint32_t tmem_base, int num_tiles, int t0, int tstride,
+                                              int m_off, int tile_m, Coords tile_coords, Release release) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ew = warp - EPI_WARP0;
+  const int q = warp & 3;          // TMEM lane quadrant this warp may access
+  const int half = ew >> 2;
+  const Epi& e = g.epi;
+  uint8_t* sbuf = smem_epi + ew * STAGE_EPI;
+  // staged-path roles of the single input box and the output box(es)
+  const bool has_in = TMA_EPI && (e.res || e.acc_in || e.kind == EPI_GELU_BWD);
+  const DT in_dt = e.kind == EPI_GELU_BWD ? e.aux_dt : DT::F32;
+  const uint32_t in_bytes = EPI_TILE * EPI_TILE * (uint32_t)dt_size(in_dt);
+  uint32_t ephase = 0;
+  int it = 0;
+  for (int t = t0; t < num_tiles; t += tstride, ++it) {
+    int mb, nb;
+    tile_coords(t, mb, nb);
+    const int as = it & 1;
+    const uint32_t aphase = (it >> 1) & 1;
+    mbar_wait(&tfull[as], aphase);
+    fence_after();
+    const int m0w = mb * tile_m + m_off + q * 32;   // first row of this warp's 32-row strip
+    const int64_t m = m0w + lane;
+    const uint32_t taddr = tmem_base + as * BN + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+    for (int ch = half * (BN / 64); ch < (half + 1) * (BN / 64); ++ch) {
+      const int n0 = nb * BN + ch * 32;
+      if (!TMA_EPI) {
+        float v[32];
+        tmem_ld32(taddr + ch * 32, v);
+        if (m < g.M && n0 < g.N) epi_chunk_direct(e, m, n0, (int)min(32, g.N - n0), v);
+        continue;
+      }
+      if (n0 >= g.N || m0w >= g.M) continue;   // whole box outside the matrix (warp-uniform)
+      // previous TMA store must have finished reading the staging box before it is reused
+      if (lane == 0) {
+        bulk_wait_read0();
+        if (has_in) {
+          mbar_expect_tx(&ebar[ew], in_bytes);
+          tma_load_2d(sbuf, &em.in, &ebar[ew], n0, m0w);
+        }
+      }
+      __syncwarp();
+      uint32_t raw[32];
+      tmem_ld32_nowait(taddr + ch * 32, raw);
+      tmem_wait_ld();
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]);
+      if (has_in) {
+        mbar_wait(&ebar[ew], ephase);
+        ephase ^= 1;
+      }
+      if (e.kind == EPI_STORE) {
+        if (e.bias) {
+          float b[32];
+          if (n0 + 32 <= g.N) load32(e.bias, e.bias_dt, n0, b);
+          else for (int i = 0; i < 32; ++i) b[i] = n0 + i < g.N ? ld_elem(e.bias, n0 + i, e.bias_dt) : 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += b[i];
+        }
+        if (has_in) {
+          float x[32];
+          stage_read_row(sbuf, DT::F32, lane, x);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += x[i];
+        }
+        stage_write_row(sbuf, e.out_dt, lane, v);
+      } else if (e.kind == EPI_GELU_FWD) {
+        float b[32];
+        if (n0 + 32 <= g.N) load32(e.bias, e.bias_dt, n0, b);
+        else for (int i = 0; i < 32; ++i) b[i] = n0 + i < g.N ? ld_elem(e.bias, n0 + i, e.bias_dt) : 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] += b[i];
+        stage_write_row(sbuf, e.aux_dt, lane, v);              // u  -> first 2 KB
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = gelu_fast(v[i]);
+        stage_write_row(sbuf + 2048, e.out_dt, lane, v);       // g  -> second 2 KB
+      } else {  // EPI_GELU_BWD: u was TMA-loaded into the box; out overwrites it in place
+        float u[32];
+        stage_read_row(sbuf, in_dt, lane, u);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_fast(u[i]);
+        stage_write_row(sbuf, e.out_dt, lane, v);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        if (e.kind == EPI_GELU_FWD) {
+          tma_store_2d(&em.aux, sbuf, n0, m0w);
+          tma_store_2d(&em.out, sbuf + 2048, n0, m0w);
+        } else {
+          tma_store_2d(&em.out, sbuf, n0, m0w);
+        }
+        bulk_commit();
+      }
+    }
+    fence_before();
+    __syncwarp();
+    if (lane == 0) release(as);
+  }
+  if (TMA_EPI && lane == 0) bulk_wait0();
+}
+
 template <int BN, bool A_MN, bool B_MN, bool TMA_EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -276,111 +385,157 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp >= EPI_WARP0) {  // ===== epilogue: TMEM -> registers -> fused epilogue -> global
-    const int ew = warp - EPI_WARP0;
-    const int q = warp & 3;          // TMEM lane quadrant this warp may access
-    const int half = ew >> 2;
-    const Epi& e = g.epi;
-    uint8_t* sbuf = smem + SM::EPI_OFF + ew * STAGE_EPI;
-    // staged-path roles of the single input box and the output box(es)
-    const bool has_in = TMA_EPI && (e.res || e.acc_in || e.kind == EPI_GELU_BWD);
-    const DT in_dt = e.kind == EPI_GELU_BWD ? e.aux_dt : DT::F32;
-    const uint32_t in_bytes = EPI_TILE * EPI_TILE * (uint32_t)dt_size(in_dt);
-    uint32_t ephase = 0;
-    int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-      int mb, nb;
-      tile_coords(t, mb, nb);
-      const int as = it & 1;
-      const uint32_t aphase = (it >> 1) & 1;
-      mbar_wait(&tfull[as], aphase);
-      fence_after();
-      const int m0w = mb * BM + q * 32;           // first row of this warp's 32-row strip
-      const int64_t m = m0w + lane;
-      const uint32_t taddr = tmem_base + as * BN + ((uint32_t)(q * 32) << 16);
-#pragma unroll 1
-      for (int ch = half * (BN / 64); ch < (half + 1) * (BN / 64); ++ch) {
-        const int n0 = nb * BN + ch * 32;
-        if (!TMA_EPI) {
-          float v[32];
-          tmem_ld32(taddr + ch * 32, v);
-          if (m < g.M && n0 < g.N) epi_chunk_direct(e, m, n0, (int)min(32, g.N - n0), v);
-          continue;
-        }
-        if (n0 >= g.N || m0w >= g.M) continue;   // whole box outside the matrix (warp-uniform)
-        // previous TMA store must have finished reading the staging box before it is reused
-        if (lane == 0) {
-          bulk_wait_read0();
-          if (has_in) {
-            mbar_expect_tx(&ebar[ew], in_bytes);
-            tma_load_2d(sbuf, &em.in, &ebar[ew], n0, m0w);
-          }
-        }
-        __syncwarp();
-        uint32_t raw[32];
-        tmem_ld32_nowait(taddr + ch * 32, raw);
-        tmem_wait_ld();
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]);
-        if (has_in) {
-          mbar_wait(&ebar[ew], ephase);
-          ephase ^= 1;
-        }
-        if (e.kind == EPI_STORE) {
-          if (e.bias) {
-            float b[32];
-            if (n0 + 32 <= g.N) load32(e.bias, e.bias_dt, n0, b);
-            else for (int i = 0; i < 32; ++i) b[i] = n0 + i < g.N ? ld_elem(e.bias, n0 + i, e.bias_dt) : 0.f;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += b[i];
-          }
-          if (has_in) {
-            float x[32];
-            stage_read_row(sbuf, DT::F32, lane, x);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += x[i];
-          }
-          stage_write_row(sbuf, e.out_dt, lane, v);
-        } else if (e.kind == EPI_GELU_FWD) {
-          float b[32];
-          if (n0 + 32 <= g.N) load32(e.bias, e.bias_dt, n0, b);
-          else for (int i = 0; i < 32; ++i) b[i] = n0 + i < g.N ? ld_elem(e.bias, n0 + i, e.bias_dt) : 0.f;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += b[i];
-          stage_write_row(sbuf, e.aux_dt, lane, v);              // u  -> first 2 KB
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
-          stage_write_row(sbuf + 2048, e.out_dt, lane, v);       // g  -> second 2 KB
-        } else {  // EPI_GELU_BWD: u was TMA-loaded into the box; out overwrites it in place
-          float u[32];
-          stage_read_row(sbuf, in_dt, lane, u);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(u[i]);
-          stage_write_row(sbuf, e.out_dt, lane, v);
-        }
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) {
-          if (e.kind == EPI_GELU_FWD) {
-            tma_store_2d(&em.aux, sbuf, n0, m0w);
-            tma_store_2d(&em.out, sbuf + 2048, n0, m0w);
-          } else {
-            tma_store_2d(&em.out, sbuf, n0, m0w);
-          }
-          bulk_commit();
-        }
-      }
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[as]);
-    }
-    if (TMA_EPI && lane == 0) bulk_wait0();
+    epilogue_loop<BN, TMA_EPI>(g, em, smem + SM::EPI_OFF, ebar, tfull, tmem_base, num_tiles, blockIdx.x, gridDim.x,
+                               0, BM,
+                               [&](int t, int& mb, int& nb) { tile_coords(t, mb, nb); },
+                               [&](int as) { mbar_arrive(&tempty[as]); });
   }
   fence_before();
   __syncthreads();
   if (warp == 2) {
     fence_after();
     tmem_dealloc(tmem_base, SM::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ CTA-pair kernel (cta_group::2)
+// A cluster of 2 CTAs computes a 256 x 256 tile: CTA r loads rows [128r, 128r+128) of A and columns
+// [128r, 128r+128) of B into its own shared memory; the leader (rank 0) issues
+// tcgen05.mma.cta_group::2 (M=256, N=256) which reads both CTAs' operands and writes rows 0..127 of D
+// into the leader's TMEM and rows 128..255 into the peer's.  Per-SM operand traffic is a third lower
+// than the single-CTA 128 x 256 tile at the same MMA rate.  Each CTA drains its own TMEM (epilogue_loop).
+constexpr int PAIR_N = 256;
+struct Smem2 {
+  static constexpr int STAGES = 5;
+  static constexpr int A_BYTES = BM * BK * 2;            // this CTA's 128 rows of A
+  static constexpr int B_BYTES = (PAIR_N / 2) * BK * 2;  // this CTA's 128 columns of B
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * PAIR_N;
+  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
+  static constexpr int BAR_OFF = EPI_OFF + EPI_WARPS * STAGE_EPI;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+template <bool A_MN, bool B_MN, bool TMA_EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ EpiMaps em, const GemmArgs g) {
+  using SM = Smem2;
+  constexpr int STAGES = SM::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);   // used in the leader only
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;                                        // leader: arrivals from both CTAs
+  uint64_t* ebar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + EPI_WARPS);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int num_m = (g.M + 2 * BM - 1) / (2 * BM), num_n = (g.N + PAIR_N - 1) / PAIR_N;
+  const int num_tiles = num_m * num_n;
+  const int nk = (g.K + BK - 1) / BK;
+  constexpr int GM = 8;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * EPI_WARPS); }
+    for (int s = 0; s < EPI_WARPS; ++s) mbar_init(&ebar[s], 1);
+    mbar_fence_init();
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+  }
+  if (warp == 2) tmem_alloc_cg2(tmem_slot, SM::TMEM_COLS);
+  fence_before();
+  cluster_sync();   // barriers of both CTAs initialised, TMEM allocated in both
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto tile_coords = [&](int t, int& mb, int& nb) {
+    const int per_group = GM * num_n;
+    const int grp = t / per_group;
+    const int first_m = grp * GM;
+    const int gsz = min(num_m - first_m, GM);
+    const int r = t % per_group;
+    mb = first_m + r % gsz;
+    nb = r / gsz;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ===== TMA producer (both CTAs), completion counted on the leader's full barrier
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < num_tiles; t += npairs) {
+        int mb, nb;
+        tile_coords(t, mb, nb);
+        const int m0 = mb * 2 * BM + rank * BM, n0 = nb * PAIR_N + rank * (PAIR_N / 2);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * SM::STAGE_BYTES;
+          uint8_t* sb = sa + SM::A_BYTES;
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * SM::STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d_cg2(sa, &tmA, &full[stage], k0, m0);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i) tma_load_2d_cg2(sa + i * 64 * BK * 2, &tmA, &full[stage], m0 + 64 * i, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d_cg2(sb, &tmB, &full[stage], k0, n0);
+          } else {
+#pragma unroll
+            for (int i = 0; i < (PAIR_N / 2) / 64; ++i)
+              tma_load_2d_cg2(sb + i * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * i, k0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ===== MMA issuer (leader CTA only)
+      constexpr uint32_t idesc = make_idesc(2 * BM, PAIR_N, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = pair; t < num_tiles; t += npairs, ++it) {
+        const int as = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(&tempty[as], aphase ^ 1);     // both CTAs drained this accumulator stage
+        fence_after();
+        const uint32_t dtm = tmem_base + as * PAIR_N;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          fence_after();
+          const uint32_t sa = smem_u32(smem + stage * SM::STAGE_BYTES);
+          const uint32_t sb = sa + SM::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            const uint64_t ad = A_MN ? make_desc(sa + k * UMMA_K * 128, 64 * BK * 2, 1024)
+                                     : make_desc(sa + k * UMMA_K * 2, 16, 1024);
+            const uint64_t bd = B_MN ? make_desc(sb + k * UMMA_K * 128, 64 * BK * 2, 1024)
+                                     : make_desc(sb + k * UMMA_K * 2, 16, 1024);
+            umma_f16_cg2(dtm, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit_cg2_mc(&empty[stage], 0x3);   // frees this smem slot in both CTAs
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_cg2_mc(&tfull[as], 0x3);        // accumulator ready in both CTAs
+      }
+    }
+  } else if (warp >= EPI_WARP0) {  // ===== epilogue (both CTAs, each its own 128 rows)
+    const uint32_t leader_tempty = mapa(smem_u32(tempty), 0);
+    epilogue_loop<PAIR_N, TMA_EPI>(g, em, smem + SM::EPI_OFF, ebar, tfull, tmem_base, num_tiles, pair, npairs,
+                                   (int)rank * BM, 2 * BM, [&](int t, int& mb, int& nb) { tile_coords(t, mb, nb); },
+                                   [&](int as) { mbar_arrive_cluster(leader_tempty + as * 8); });
+  }
+  fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    fence_after();
+    tmem_dealloc_cg2(tmem_base, SM::TMEM_COLS);
   }
 }
 
@@ -460,7 +615,48 @@ static cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
   return launch_k<BN, A_MN, B_MN, false>(ta, tb, em, g, st);
 }
 
+template <bool A_MN, bool B_MN, bool TMA_EPI>
+static cudaError_t launch2_k(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const GemmArgs& g,
+                             cudaStream_t st) {
+  auto kern = gemm_tc2_kernel<A_MN, B_MN, TMA_EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem2::TOTAL);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + PAIR_N - 1) / PAIR_N);
+  const int pairs = std::min(tiles, num_sms() / 2);
+  note_launch(), kern<<<2 * pairs, NUM_THREADS, Smem2::TOTAL, st>>>(ta, tb, em, g);
+  return cudaGetLastError();
+}
+
+template <bool A_MN, bool B_MN>
+static cudaError_t launch2(const GemmArgs& g, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  cudaError_t e;
+  if (!A_MN) e = make_map(&ta, g.A, DT::BF16, g.K, g.M, g.lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+  else e = make_map(&ta, g.A, DT::BF16, g.M, g.K, g.lda, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (e != cudaSuccess) return e;
+  if (!B_MN) e = make_map(&tb, g.B, DT::BF16, g.K, g.N, g.ldb, BK, PAIR_N / 2, CU_TENSOR_MAP_SWIZZLE_128B);
+  else e = make_map(&tb, g.B, DT::BF16, g.N, g.K, g.ldb, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (e != cudaSuccess) return e;
+  EpiMaps em;
+  if (epi_maps(g, &em)) return launch2_k<A_MN, B_MN, true>(ta, tb, em, g, st);
+  memset(&em, 0, sizeof(em));
+  return launch2_k<A_MN, B_MN, false>(ta, tb, em, g, st);
+}
+
 }  // namespace tc
+
+static int gemm_mode() {   // LGA_GEMM_PAIR=0 forces the single-CTA kernel (A/B comparisons)
+  static int m = -1;
+  if (m < 0) {
+    const char* v = getenv("LGA_GEMM_PAIR");
+    m = (v && v[0] == '0') ? 0 : 1;
+  }
+  return m;
+}
 
 cudaError_t gemm_bf16_tc(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return cudaSuccess;
@@ -469,6 +665,10 @@ cudaError_t gemm_bf16_tc(const GemmArgs& g, cudaStream_t st) {
   // BN = 256 when there are enough tiles to fill the machine, else 128
   const int tiles256 = ((g.M + 127) / 128) * ((g.N + 255) / 256);
   const bool wide = g.N > 128 && tiles256 >= num_sms();
+  const int pair_tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256);
+  if (gemm_mode() == 1 && g.N > 128 && pair_tiles >= num_sms() / 2)
+    return amn ? (bmn ? tc::launch2<true, true>(g, st) : tc::launch2<true, false>(g, st))
+               : (bmn ? tc::launch2<false, true>(g, st) : tc::launch2<false, false>(g, st));
 #define L(BN) (amn ? (bmn ? tc::launch<BN, true, true>(g, st) : tc::launch<BN, true, false>(g, st)) \
                    : (bmn ? tc::launch<BN, false, true>(g, st) : tc::launch<BN, false, false>(g, st)))
   return wide ? L(256) : L(128);

@@ -32,7 +32,7 @@ def _launch(tmp_path, sh, precision=0, schedule=0, chunk=0, steps=1):
            "--master-addr=127.0.0.1", f"--master-port={_port[0]}", os.path.join(HERE, "dist_worker.py"),
            "--out", str(tmp_path), "--shape", shape, "--precision", str(precision), "--schedule", str(schedule),
            "--chunk", str(chunk), "--steps", str(steps)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return [dict(np.load(os.path.join(tmp_path, f"rank{k}.npz"))) for k in range(world)]
 
@@ -87,4 +87,15 @@ def test_pp2_dp2_fp32(tmp_path):
 
 def test_dp2_bf16(tmp_path):
     sh = synth.Shape(layers=2, d=256, heads=2, seq=128, micro_batch=1, n_micro=4, dp=2)
+    _check(_launch(tmp_path, sh, precision=1), sh, 2e-2, elem=2)
+
+
+def test_pp4_fp32_modular_pipeline(tmp_path):
+    """P = 4: the ring has four distinct edges (stage 3 -> 0 wraps)."""
+    sh = synth.Shape(layers=8, d=64, heads=4, seq=32, micro_batch=2, n_micro=4, dp=1, pp=4)
+    _check(_launch(tmp_path, sh), sh, 1e-5)
+
+
+def test_pp4_bf16_modular_pipeline(tmp_path):
+    sh = synth.Shape(layers=4, d=256, heads=2, seq=128, micro_batch=1, n_micro=4, dp=1, pp=4)
     _check(_launch(tmp_path, sh, precision=1), sh, 2e-2, elem=2)

@@ -54,7 +54,8 @@ def relerr(a, b):
     return ((a.double() - b.double()).norm() / b.double().norm()).item()
 
 
-SHAPES = [(128, 128, 64), (256, 512, 256), (200, 328, 136), (1000, 768, 768), (64, 2304, 4096), (4096, 256, 1000)]
+SHAPES = [(128, 128, 64), (256, 512, 256), (200, 328, 136), (1000, 768, 768), (64, 2304, 4096), (4096, 256, 1000),
+          (2200, 8400, 200)]   # the last one has >= 74 256x256 tiles -> CTA-pair (cta_group::2) kernel, ragged M/N/K
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
@@ -70,9 +71,9 @@ def test_tc_gemm_store_f32(M, N, K, amaj, bmaj):
     assert relerr(out, ref) < 1e-5
 
 
+@pytest.mark.parametrize("M,N,K", [(520, 384, 192), (2400, 8200, 128)])
 @pytest.mark.parametrize("kind", ["bias_bf16", "bias_res_acc", "gelu_fwd", "gelu_bwd"])
-def test_tc_gemm_epilogues(kind):
-    M, N, K = 520, 384, 192
+def test_tc_gemm_epilogues(kind, M, N, K):
     g = torch.Generator(device="cuda").manual_seed(1)
     A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
     B = torch.randn(K, N, device="cuda", generator=g).bfloat16()      # MN-major B (forward form)
