@@ -225,9 +225,11 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
           mbar_wait(&o_done[hf], (gt - 1) & 1);   // PV of the previous tile done: O_h stable, P_h buffer free
           fence_after();
         }
-        float scale = 1.f;
-        if (m_new != m_used && m_used != -INFINITY) {   // lazy rescale of this half's accumulator row
-          scale = ex2(m_used - m_new);
+        // lazy rescale of this half's accumulator row.  tcgen05.ld / st are warp-collective, so the whole
+        // warp enters when any lane needs it; lanes that do not rescale multiply by 1.
+        const bool resc = m_new != m_used && m_used != -INFINITY;
+        const float scale = resc ? ex2(m_used - m_new) : 1.f;
+        if (__any_sync(0xffffffffu, resc)) {
 #pragma unroll 1
           for (int c = 0; c < DH / 32; ++c) {
             float tt[32];

@@ -327,6 +327,22 @@ static GradDst grad_dst(lga_handle* h, int chunk_idx, int nchunks, int gb, int64
   return r;
 }
 
+// LGA_TRACE=1: synchronise the compute stream and log after every layer pass (debugging hangs)
+static bool trace_on() {
+  static int t = -1;
+  if (t < 0) {
+    const char* v = getenv("LGA_TRACE");
+    t = (v && v[0] == '1') ? 1 : 0;
+  }
+  return t == 1;
+}
+static void trace(lga_handle* h, const char* what, int64_t layer) {
+  if (!trace_on()) return;
+  fprintf(stderr, "[lga rank %d stage %d] %s layer %lld issued\n", h->rank, h->stage, what, (long long)layer);
+  CK(cudaStreamSynchronize(h->s_comp));
+  fprintf(stderr, "[lga rank %d stage %d] %s layer %lld done\n", h->rank, h->stage, what, (long long)layer);
+}
+
 // ------------------------------------------------------------------ layer executor
 // Forward of local layer j over micro-batches [m0, m0+c) (module docstring of kernels.cuh).
 // x_in: [c][M][d] fp32; y_out: fp32 destination or nullptr (recompute: FFN2 not needed).
@@ -345,6 +361,7 @@ static void layer_fwd(lga_handle* h, const void* W, const float* x_in, float* y_
     g.epi.kind = EPI_STORE; g.epi.bias = eoff((void*)W, E, c.o_bqkv); g.epi.bias_dt = E;
     g.epi.out = h->qkv; g.epi.ldo = 3 * d; g.epi.out_dt = E;
     gemm(h, g, st);
+    trace(h, "  qkv gemm", -1);
   }
   {  // o = attention(q, k, v)
     AttnArgs a;
@@ -355,6 +372,7 @@ static void layer_fwd(lga_handle* h, const void* W, const float* x_in, float* y_
     if (c.bf16) CK(attn_fwd_bf16(a, st)); else attn_fwd_f32(a, st);
     KCHECK();
     prof_end(h, p, st, FAM_ATTN, attn_flops_fwd(c, a.nseq));
+    trace(h, "  attn fwd", -1);
   }
   {  // h1 = x + o Wo + bo
     GemmArgs g;
@@ -365,6 +383,7 @@ static void layer_fwd(lga_handle* h, const void* W, const float* x_in, float* y_
     g.epi.res = x_in; g.epi.ldr = d;
     g.epi.out = h->h1; g.epi.ldo = d; g.epi.out_dt = DT::F32;
     gemm(h, g, st);
+    trace(h, "  oproj gemm", -1);
   }
   ln_fwd(h->h1, eoff((void*)W, E, c.o_ln2w), eoff((void*)W, E, c.o_ln2b), E, h->cn, E, h->st2, T, d, c.ln_eps, st);
   KCHECK();
@@ -377,6 +396,7 @@ static void layer_fwd(lga_handle* h, const void* W, const float* x_in, float* y_
     g.epi.aux = h->u; g.epi.ldaux = c.f; g.epi.aux_dt = E;
     g.epi.out = h->g; g.epi.ldo = c.f; g.epi.out_dt = E;
     gemm(h, g, st);
+    trace(h, "  ffn1 gemm", -1);
   }
   if (y_out) {  // y = h1 + g W2 + b2
     GemmArgs g;
@@ -387,6 +407,7 @@ static void layer_fwd(lga_handle* h, const void* W, const float* x_in, float* y_
     g.epi.res = h->h1; g.epi.ldr = d;
     g.epi.out = y_out; g.epi.ldo = d; g.epi.out_dt = DT::F32;
     gemm(h, g, st);
+    trace(h, "  ffn2 gemm", -1);
   }
 }
 
@@ -653,6 +674,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
       }
     }
     CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
+    trace(h, "fwd", i);
   }
   CK(cudaEventRecord(h->ev_fwd_end, h->s_comp));
   // ---------------- backward: layer-major, recompute + backward over all micro-batches
@@ -710,6 +732,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
       }
     }
     CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
+    trace(h, "bwd", i);
     CK(cudaEventRecord(h->ev_grad[gb], h->s_comp));
     CK(cudaStreamWaitEvent(h->s_comm, h->ev_grad[gb], 0));
     void* shard_g = reduce_scatter(h, gb);

@@ -127,14 +127,18 @@ def _attn_ref(qkv, nseq, s, H, dh, causal):
     return q, k, v
 
 
-@pytest.mark.parametrize("path,dh,s,causal", [(0, 16, 37, 1), (0, 64, 128, 0), (1, 64, 256, 1), (1, 128, 200, 1), (2, 128, 200, 1), (2, 64, 300, 0), (1, 64, 300, 0),
-                                              (1, 128, 512, 0), (1, 64, 1024, 1)])
-def test_attention_fwd_bwd(path, dh, s, causal):
+@pytest.mark.parametrize("path,dh,s,causal,mag", [(0, 16, 37, 1, 1), (0, 64, 128, 0, 1), (1, 64, 256, 1, 1),
+                                                  (1, 128, 200, 1, 1), (2, 128, 200, 1, 1), (2, 64, 300, 0, 1),
+                                                  (1, 64, 300, 0, 1), (1, 128, 512, 0, 1), (1, 64, 1024, 1, 1),
+                                                  (1, 128, 1024, 1, 6), (1, 64, 700, 0, 6), (0, 32, 300, 1, 6)])
+def test_attention_fwd_bwd(path, dh, s, causal, mag):
     nseq, H = 2, 3
     d = H * dh
     dt = torch.float32 if path == 0 else torch.bfloat16
     g = torch.Generator(device="cuda").manual_seed(3)
-    qkv = torch.randn(nseq * s, 3 * d, device="cuda", generator=g).to(dt)
+    # mag > 1 makes score rows drift by far more than 2^8 across key tiles: forces the lazy O rescale on
+    # some rows of a warp but not others (the divergent-collective case)
+    qkv = (torch.randn(nseq * s, 3 * d, device="cuda", generator=g) * torch.linspace(0.3, mag, nseq * s, device="cuda")[:, None]).to(dt)
     o = torch.empty(nseq * s, d, device="cuda", dtype=dt)
     lse = torch.empty(nseq, H, s, device="cuda")
     assert L.lgatest_attn_fwd(path, nseq, s, H, dh, causal, P(qkv), P(o), P(lse), stream()) == 0
