@@ -41,6 +41,7 @@ def nccl_dirs():
 def _flags():
     inc, _ = nccl_dirs()
     extra = ["-DLGA_HANG_DEBUG"] if os.environ.get("LGA_HANG_DEBUG") == "1" else []
+    extra += ["-D" + f for f in os.environ.get("LGA_EXTRA_DEFINES", "").split(",") if f]
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
                    "-I" + inc, "-I" + os.path.join(ROOT, "include"), "-I" + CSRC] + extra
 

@@ -45,7 +45,7 @@ template <int DH>
 __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUtensorMap tm, const AttnArgs a) {
   using SM = FwdSmem<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps shared provenance
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;     // [2]

@@ -18,7 +18,7 @@ namespace fatb {
 
 using namespace tcu;
 
-constexpr int EW_WARPS = 8;                 // element-wise warps: 2 per TMEM lane quadrant
+constexpr int EW_WARPS = 16;                // element-wise warps: 4 per TMEM lane quadrant, 16 columns each
 constexpr int EW_THREADS = EW_WARPS * 32;
 constexpr int NT = (4 + EW_WARPS) * 32;
 constexpr float LOG2E = 1.4426950408889634f;
@@ -42,11 +42,11 @@ __global__ void dsum_kernel(AttnArgs a) {
   if (l == 0) a.dsum[((tok / a.seq) * a.heads + h) * a.seq + tok % a.seq] = acc;
 }
 
-// 32 bf16 (4 chunks of 16 B, chunk indices 4*half .. 4*half+3) of row r of a [128][64] K-major SW128 tile
-__device__ __forceinline__ void st_half_row_bf16(uint8_t* tile, int r, int half, const uint32_t (&pk)[16]) {
+// 16 bf16 (2 chunks of 16 B, chunk indices 2*quarter, 2*quarter+1) of row r of a [128][64] K-major SW128 tile
+__device__ __forceinline__ void st_quarter_row_bf16(uint8_t* tile, int r, int quarter, const uint32_t (&pk)[8]) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t addr = smem_u32(tile) + sw128(r, half * 4 + i);
+  for (int i = 0; i < 2; ++i) {
+    const uint32_t addr = smem_u32(tile) + sw128(r, quarter * 2 + i);
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[i * 4]), "r"(pk[i * 4 + 1]),
                  "r"(pk[i * 4 + 2]), "r"(pk[i * 4 + 3])
                  : "memory");
@@ -57,15 +57,19 @@ __device__ __forceinline__ void st_half_row_bf16(uint8_t* tile, int r, int half,
 // lanes with `valid` store.
 __device__ __forceinline__ void store_row_bf16_global(__nv_bfloat16* dst, uint32_t taddr, int ncols, float scale,
                                                       bool valid) {
-  for (int c = 0; c < ncols; c += 32) {
-    float t[32];
-    tmem_ld32(taddr + c, t);
+  for (int c = 0; c < ncols; c += 16) {   // ncols is a multiple of 16
+    uint32_t r[16];
+    tmem_ld16_nowait(taddr + c, r);
+    tmem_wait_ld();
     if (!valid) continue;
+    float t[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i] = __uint_as_float(r[i]) * scale;
     uint4* p = reinterpret_cast<uint4*>(dst + c);
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      p[i] = make_uint4(pack_bf16x2(t[8 * i] * scale, t[8 * i + 1] * scale), pack_bf16x2(t[8 * i + 2] * scale, t[8 * i + 3] * scale),
-                        pack_bf16x2(t[8 * i + 4] * scale, t[8 * i + 5] * scale), pack_bf16x2(t[8 * i + 6] * scale, t[8 * i + 7] * scale));
+    for (int i = 0; i < 2; ++i)
+      p[i] = make_uint4(pack_bf16x2(t[8 * i], t[8 * i + 1]), pack_bf16x2(t[8 * i + 2], t[8 * i + 3]),
+                        pack_bf16x2(t[8 * i + 4], t[8 * i + 5]), pack_bf16x2(t[8 * i + 6], t[8 * i + 7]));
   }
 }
 
@@ -84,9 +88,9 @@ struct DkvSmem {
   static constexpr int NST = 3;                        // Q / dO ring depth
   static constexpr int Q_OFF = V_OFF + KT;             // [NST]
   static constexpr int G_OFF = Q_OFF + NST * QT;       // dO [NST]
-  static constexpr int PT_OFF = G_OFF + NST * QT;      // P^T [128][64]
-  static constexpr int DST_OFF = PT_OFF + SUB128;      // dS^T [128][64]
-  static constexpr int LD_OFF = DST_OFF + SUB128;      // lse[2][64], dsum[2][64] (floats)
+  static constexpr int PT_OFF = G_OFF + NST * QT;      // P^T [2][128][64]
+  static constexpr int DST_OFF = PT_OFF + 2 * SUB128;  // dS^T [2][128][64]
+  static constexpr int LD_OFF = DST_OFF + 2 * SUB128;  // lse[2][64], dsum[2][64] (floats)
   static constexpr int BAR_OFF = LD_OFF + 4 * 64 * 4;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
@@ -97,7 +101,7 @@ __global__ void __launch_bounds__(NT, 1)
                 const __grid_constant__ CUtensorMap tm_g, const AttnArgs a) {
   using SM = DkvSmem<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps shared provenance
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
   constexpr int NST = SM::NST;
   uint64_t* kv_full = bars + 0;
@@ -106,8 +110,8 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* s_full = q_empty + NST;         // [2]
   uint64_t* s_empty = s_full + 2;           // [2] (EW_THREADS arrivals)
   uint64_t* p_full = s_empty + 2;           // (EW_THREADS arrivals)
-  uint64_t* g_done = p_full + 1;
-  constexpr int NBAR = 2 * NST + 7;
+  uint64_t* g_done = p_full + 1;            // [2] per P^T / dS^T buffer
+  constexpr int NBAR = 2 * NST + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
   float* lse_s = reinterpret_cast<float*>(smem + SM::LD_OFF);   // [2][64]
   float* dsum_s = lse_s + 128;                                   // [2][64]
@@ -183,27 +187,28 @@ __global__ void __launch_bounds__(NT, 1)
           umma_commit(&s_full[b]);
         }
         if (i >= 1) {
-          const int ii = i - 1, st = ii % NST;
+          const int ii = i - 1, st = ii % NST, pb = ii & 1;
           mbar_wait(p_full, ii & 1);
           fence_after();
           const uint32_t sQ = smem_u32(smem + SM::Q_OFF + st * SM::QT);
           const uint32_t sG = smem_u32(smem + SM::G_OFF + st * SM::QT);
+          const uint32_t sPtb = sPt + pb * SM::SUB128, sDStb = sDSt + pb * SM::SUB128;
 #pragma unroll
           for (int kk = 0; kk < QB / 16; ++kk) {
             const uint32_t oa = kk * 32;                // K-major A: 16 queries = 32 B into the swizzle span
             const uint32_t ob = kk * 16 * 128;          // MN-major B: 16 query rows
             const uint32_t acc = (ii > 0 || kk > 0) ? 1u : 0u;
-            umma_f16(t_dv, make_desc(sPt + oa, 16, 1024), make_desc(sG + ob, SM::SUB64, 1024), idesc_g, acc);
-            umma_f16(t_dk, make_desc(sDSt + oa, 16, 1024), make_desc(sQ + ob, SM::SUB64, 1024), idesc_g, acc);
+            umma_f16(t_dv, make_desc(sPtb + oa, 16, 1024), make_desc(sG + ob, SM::SUB64, 1024), idesc_g, acc);
+            umma_f16(t_dk, make_desc(sDStb + oa, 16, 1024), make_desc(sQ + ob, SM::SUB64, 1024), idesc_g, acc);
           }
-          umma_commit(g_done);
+          umma_commit(&g_done[pb]);
           umma_commit(&q_empty[st]);
         }
       }
     }
-  } else if (warp >= 4) {  // ===== element-wise: one key row per thread pair (two query-column halves)
+  } else if (warp >= 4) {  // ===== element-wise: one key row per 4 threads (query-column quarters)
     const int qd = warp & 3;
-    const int hf = (warp - 4) >> 2;
+    const int hf = (warp - 4) >> 2;            // quarter 0..3 of the 64 query columns
     const int r = qd * 32 + lane;
     const int tid = threadIdx.x - 128;
     const int kj = k0 + r;
@@ -211,7 +216,7 @@ __global__ void __launch_bounds__(NT, 1)
     const float sl2 = a.scale * LOG2E;
     uint8_t* sPt = smem + SM::PT_OFF;
     uint8_t* sDSt = smem + SM::DST_OFF;
-    // lse (log2 units) / dsum of query tile i: loaded one iteration ahead into a register by threads
+    // lse (log2 units) / dsum of query tile i: loaded two iterations ahead into a register by threads
     // tid < 128, parked in shared buffer i&1 at the end of iteration i-1 (barrier at the top of i)
     auto ld_stat = [&](int i) -> float {
       const int q = (qstart + i) * QB + (tid & 63);
@@ -219,37 +224,38 @@ __global__ void __launch_bounds__(NT, 1)
       return tid < 64 ? a.lse[rb + q] * LOG2E : a.dsum[rb + q];
     };
     if (tid < 128) (tid < 64 ? lse_s : dsum_s)[tid & 63] = ld_stat(0);
+    float pre1 = ld_stat(1);
     for (int i = 0; i < nq; ++i) {
-      const float pre = ld_stat(i + 1);
+      const float pre2 = ld_stat(i + 2);
       const int b = i & 1, st = i & 1;
       const int q0 = (qstart + i) * QB;
       mbar_wait(&s_full[b], (i >> 1) & 1);
       fence_after();
-      uint32_t rsv[32], rdp[32];
-      tmem_ld32_nowait(t_st[b] + lrow + hf * 32, rsv);
-      tmem_ld32_nowait(t_dpt[b] + lrow + hf * 32, rdp);
+      uint32_t rsv[16], rdp[16];
+      tmem_ld16_nowait(t_st[b] + lrow + hf * 16, rsv);
+      tmem_ld16_nowait(t_dpt[b] + lrow + hf * 16, rdp);
       tmem_wait_ld();
       fence_before();
       mbar_arrive(&s_empty[b]);
       asm volatile("bar.sync 1, %0;" ::"n"(EW_THREADS) : "memory");   // tile i's lse / dsum visible
-      const float* ls = lse_s + st * 64 + hf * 32;
-      const float* ds_ = dsum_s + st * 64 + hf * 32;
-      uint32_t pp[16], pd[16];
+      const float* ls = lse_s + st * 64 + hf * 16;
+      const float* ds_ = dsum_s + st * 64 + hf * 16;
       // valid iff q < s, kj < s and (causal) kj <= q; only tiles touching the diagonal / the end mask
-      const int qa = q0 + hf * 32;
-      const bool need_mask = kj >= s || qa + 32 > s || (a.causal && kj > qa);
-      float sc[32];
+      const int qa = q0 + hf * 16;
+      const bool need_mask = kj >= s || qa + 16 > s || (a.causal && kj > qa);
+      float sc[16];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -ls[c]);
+      for (int c = 0; c < 16; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -ls[c]);
       if (need_mask) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
+        for (int c = 0; c < 16; ++c) {
           const int q = qa + c;
           if (!(q < s && kj < s && (!a.causal || kj <= q))) sc[c] = -INFINITY;
         }
       }
+      uint32_t pp[8], pd[8];
 #pragma unroll
-      for (int c = 0; c < 32; c += 2) {
+      for (int c = 0; c < 16; c += 2) {
         float p[2], g[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -259,22 +265,25 @@ __global__ void __launch_bounds__(NT, 1)
         pp[c / 2] = pack_bf16x2(p[0], p[1]);
         pd[c / 2] = pack_bf16x2(g[0], g[1]);
       }
-      if (i >= 1) {
-        mbar_wait(g_done, (i - 1) & 1);   // previous dV/dK MMAs done: P^T / dS^T buffers free
+      const int pb = i & 1;
+      if (i >= 2) {
+        mbar_wait(&g_done[pb], ((i >> 1) & 1) ^ 1);   // dV/dK MMAs of iteration i-2 done: buffer pb free
         fence_after();
       }
-      st_half_row_bf16(sPt, r, hf, pp);
-      st_half_row_bf16(sDSt, r, hf, pd);
+      st_quarter_row_bf16(sPt + pb * SM::SUB128, r, hf, pp);
+      st_quarter_row_bf16(sDSt + pb * SM::SUB128, r, hf, pd);
       fence_proxy_async();
       fence_before();
       mbar_arrive(p_full);
-      if (tid < 128) (tid < 64 ? lse_s : dsum_s)[(st ^ 1) * 64 + (tid & 63)] = pre;   // tile i+1
+      if (tid < 128) (tid < 64 ? lse_s : dsum_s)[(st ^ 1) * 64 + (tid & 63)] = pre1;   // tile i+1
+      pre1 = pre2;
     }
-    mbar_wait(g_done, (nq - 1) & 1);
+    mbar_wait(&g_done[(nq - 1) & 1], ((nq - 1) >> 1) & 1);   // last iteration's MMAs (and all earlier) done
     fence_after();
-    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + kj) * 3 * d + h * DH + hf * (DH / 2);
-    store_row_bf16_global(out + d, t_dk + lrow + hf * (DH / 2), DH / 2, 1.f, kj < s);
-    store_row_bf16_global(out + 2 * d, t_dv + lrow + hf * (DH / 2), DH / 2, 1.f, kj < s);
+    constexpr int OC = DH / 4;   // output columns per quarter
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + kj) * 3 * d + h * DH + hf * OC;
+    store_row_bf16_global(out + d, t_dk + lrow + hf * OC, OC, 1.f, kj < s);
+    store_row_bf16_global(out + 2 * d, t_dv + lrow + hf * OC, OC, 1.f, kj < s);
   }
   fence_before();
   __syncthreads();
@@ -296,11 +305,11 @@ struct DqSmem {
   static constexpr int KT = DH / 64 * SUB64;    // K (or V) [64][DH]
   static constexpr int Q_OFF = 0;
   static constexpr int G_OFF = Q_OFF + QT;
-  static constexpr int NST = 3;                 // K / V ring depth
+  static constexpr int NST = 4;                 // K / V ring depth
   static constexpr int K_OFF = G_OFF + QT;      // [NST]
   static constexpr int V_OFF = K_OFF + NST * KT;  // [NST]
-  static constexpr int DS_OFF = V_OFF + NST * KT; // dS [128][64]
-  static constexpr int BAR_OFF = DS_OFF + SUB128;
+  static constexpr int DS_OFF = V_OFF + NST * KT; // dS [2][128][64]
+  static constexpr int BAR_OFF = DS_OFF + 2 * SUB128;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
@@ -310,7 +319,7 @@ __global__ void __launch_bounds__(NT, 1)
               const __grid_constant__ CUtensorMap tm_kv, const AttnArgs a) {
   using SM = DqSmem<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps shared provenance
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
   constexpr int NST = SM::NST;
   uint64_t* qg_full = bars + 0;
@@ -319,8 +328,8 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* s_full = kv_empty + NST;        // [2]
   uint64_t* s_empty = s_full + 2;           // [2] (EW_THREADS)
   uint64_t* p_full = s_empty + 2;           // (EW_THREADS)
-  uint64_t* g_done = p_full + 1;
-  constexpr int NBAR = 2 * NST + 7;
+  uint64_t* g_done = p_full + 1;            // [2] per dS buffer
+  constexpr int NBAR = 2 * NST + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -394,22 +403,22 @@ __global__ void __launch_bounds__(NT, 1)
           umma_commit(&s_full[b]);
         }
         if (j >= 1) {
-          const int jj = j - 1, st = jj % NST;
+          const int jj = j - 1, st = jj % NST, pb = jj & 1;
           mbar_wait(p_full, jj & 1);
           fence_after();
           const uint32_t sK = smem_u32(smem + SM::K_OFF + st * SM::KT);
 #pragma unroll
           for (int kk = 0; kk < KB2 / 16; ++kk)
-            umma_f16(t_dq, make_desc(sDS + kk * 32, 16, 1024), make_desc(sK + kk * 16 * 128, SM::SUB64, 1024), idesc_q,
-                     (jj > 0 || kk > 0) ? 1u : 0u);
-          umma_commit(g_done);
+            umma_f16(t_dq, make_desc(sDS + pb * SM::SUB128 + kk * 32, 16, 1024),
+                     make_desc(sK + kk * 16 * 128, SM::SUB64, 1024), idesc_q, (jj > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(&g_done[pb]);
           umma_commit(&kv_empty[st]);
         }
       }
     }
-  } else if (warp >= 4) {  // ===== element-wise: one query row per thread pair (two key-column halves)
+  } else if (warp >= 4) {  // ===== element-wise: one query row per 4 threads (key-column quarters)
     const int qd = warp & 3;
-    const int hf = (warp - 4) >> 2;
+    const int hf = (warp - 4) >> 2;            // quarter 0..3 of the 64 key columns
     const int r = qd * 32 + lane;
     const int q = q0 + r;
     const uint32_t lrow = (uint32_t)(qd * 32) << 16;
@@ -422,45 +431,47 @@ __global__ void __launch_bounds__(NT, 1)
       const int b = j & 1;
       mbar_wait(&s_full[b], (j >> 1) & 1);
       fence_after();
-      uint32_t rsv[32], rdp[32];
-      tmem_ld32_nowait(t_s[b] + lrow + hf * 32, rsv);
-      tmem_ld32_nowait(t_dp[b] + lrow + hf * 32, rdp);
+      uint32_t rsv[16], rdp[16];
+      tmem_ld16_nowait(t_s[b] + lrow + hf * 16, rsv);
+      tmem_ld16_nowait(t_dp[b] + lrow + hf * 16, rdp);
       tmem_wait_ld();
       fence_before();
       mbar_arrive(&s_empty[b]);
-      uint32_t pd[16];
-      const int ka = j * KB2 + hf * 32;
-      const bool need_mask = q >= s || ka + 32 > s || (a.causal && ka + 31 > q0 + qd * 32);
-      float sc[32];
+      const int ka = j * KB2 + hf * 16;
+      const bool need_mask = q >= s || ka + 16 > s || (a.causal && ka + 15 > q0 + qd * 32);
+      float sc[16];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -lse2);
+      for (int c = 0; c < 16; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -lse2);
       if (need_mask) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
+        for (int c = 0; c < 16; ++c) {
           const int kj = ka + c;
           if (!(q < s && kj < s && (!a.causal || kj <= q))) sc[c] = -INFINITY;
         }
       }
+      uint32_t pd[8];
 #pragma unroll
-      for (int c = 0; c < 32; c += 2) {
+      for (int c = 0; c < 16; c += 2) {
         float g[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) g[e] = ex2(sc[c + e]) * (__uint_as_float(rdp[c + e]) - Dq) * a.scale;
         pd[c / 2] = pack_bf16x2(g[0], g[1]);
       }
-      if (j >= 1) {
-        mbar_wait(g_done, (j - 1) & 1);
+      const int pb = j & 1;
+      if (j >= 2) {
+        mbar_wait(&g_done[pb], ((j >> 1) & 1) ^ 1);   // dQ MMAs of iteration j-2 done: buffer pb free
         fence_after();
       }
-      st_half_row_bf16(sDS, r, hf, pd);
+      st_quarter_row_bf16(sDS + pb * SM::SUB128, r, hf, pd);
       fence_proxy_async();
       fence_before();
       mbar_arrive(p_full);
     }
-    mbar_wait(g_done, (nk - 1) & 1);
+    mbar_wait(&g_done[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
     fence_after();
-    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + q) * 3 * d + h * DH + hf * (DH / 2);
-    store_row_bf16_global(out, t_dq + lrow + hf * (DH / 2), DH / 2, 1.f, q < s);
+    constexpr int OC = DH / 4;
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + q) * 3 * d + h * DH + hf * OC;
+    store_row_bf16_global(out, t_dq + lrow + hf * OC, OC, 1.f, q < s);
   }
   fence_before();
   __syncthreads();

@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   using SM = Smem<BN>;
   constexpr int STAGES = SM::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps shared provenance
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -423,7 +423,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   using SM = Smem2;
   constexpr int STAGES = SM::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps shared provenance
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);   // used in the leader only
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
