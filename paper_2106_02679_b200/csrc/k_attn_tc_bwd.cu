@@ -4,12 +4,14 @@
 //   dsum_i = rowsum(dO_i * o_i)
 //   dK/dV kernel, one CTA per 128-key tile, looping over 64-query tiles:
 //     S^T = K Q^T, dP^T = V dO^T            (tcgen05, M=128 keys, N=64 queries, K=d_h; TMEM, 2 buffers)
-//     P^T = exp(S^T*scale - lse), dS^T = P^T (dP^T - dsum) * scale   (4 warps, one key row per thread)
-//     dV += P^T dO, dK += dS^T Q              (tcgen05, A = P^T / dS^T from smem, B = dO / Q read MN-major
+//     P^T = exp(S^T*scale - lse), dS^T = P^T (dP^T - dsum) * scale   (element-wise warps, bf16 into TMEM)
+//     dV += P^T dO, dK += dS^T Q              (tcgen05, A = P^T / dS^T from TMEM, B = dO / Q read MN-major
 //                                              from the very tiles TMA loaded K-major for the first two MMAs)
 //   dQ kernel, one CTA per 128-query tile, looping over 64-key tiles:
-//     S = Q K^T, dP = dO V^T ; dS = P (dP - dsum) * scale ; dQ += dS K   (K read MN-major)
-// Warp roles: 0 TMA, 1 MMA issuer, 2 TMEM allocator, 4..7 element-wise + epilogue.
+//     S = Q K^T, dP = dO V^T ; dS = P (dP - dsum) * scale ; dQ += dS K   (dS from TMEM, K read MN-major)
+// P / dS never touch shared memory, which goes to deeper Q/dO (K/V) rings: the load latency, not the
+// tensor pipe, bounded the smem-staged version (MMA issuer stalled on the ring's full barrier).
+// Warp roles: 0 TMA, 1 MMA issuer, 2 TMEM allocator, 4..19 element-wise (two ping-pong groups) + epilogue.
 #include "kernels.cuh"
 #include "tc_common.cuh"
 
@@ -18,9 +20,21 @@ namespace fatb {
 
 using namespace tcu;
 
-constexpr int EW_WARPS = 16;                // element-wise warps: 4 per TMEM lane quadrant, 16 columns each
-constexpr int EW_THREADS = EW_WARPS * 32;
+constexpr int EW_WARPS = 16;                // element-wise warps: two ping-pong groups of 8
+constexpr int GRP_THREADS = EW_WARPS * 16;  // threads per group
 constexpr int NT = (4 + EW_WARPS) * 32;
+#ifndef LGA_BWD_NST_DKV64      // ring depths (overridable for experiments)
+#define LGA_BWD_NST_DKV64 6
+#endif
+#ifndef LGA_BWD_NST_DKV128
+#define LGA_BWD_NST_DKV128 4
+#endif
+#ifndef LGA_BWD_NST_DQ64
+#define LGA_BWD_NST_DQ64 8
+#endif
+#ifndef LGA_BWD_NST_DQ128
+#define LGA_BWD_NST_DQ128 5
+#endif
 constexpr float LOG2E = 1.4426950408889634f;
 
 // rowsum(dO * o) per (sequence, head, position); one warp per row
@@ -40,17 +54,6 @@ __global__ void dsum_kernel(AttnArgs a) {
   }
   acc = warp_sum(acc);
   if (l == 0) a.dsum[((tok / a.seq) * a.heads + h) * a.seq + tok % a.seq] = acc;
-}
-
-// 16 bf16 (2 chunks of 16 B, chunk indices 2*quarter, 2*quarter+1) of row r of a [128][64] K-major SW128 tile
-__device__ __forceinline__ void st_quarter_row_bf16(uint8_t* tile, int r, int quarter, const uint32_t (&pk)[8]) {
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const uint32_t addr = smem_u32(tile) + sw128(r, quarter * 2 + i);
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[i * 4]), "r"(pk[i * 4 + 1]),
-                 "r"(pk[i * 4 + 2]), "r"(pk[i * 4 + 3])
-                 : "memory");
-  }
 }
 
 // TMEM row -> bf16 global row.  tcgen05.ld is warp-collective: every lane executes it, only
@@ -73,7 +76,35 @@ __device__ __forceinline__ void store_row_bf16_global(__nv_bfloat16* dst, uint32
   }
 }
 
+// 4-byte cp.async global -> shared (zero-filled when !valid) and its completion arriving on an mbarrier
+// (.noinc: the barrier's expected count includes one arrival per issuing thread)
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// The element-wise warps form two ping-pong groups of 8 (2 per TMEM lane quadrant, 32 columns each):
+// group g handles iterations i = g, g+2, ... with its own TMEM S/dP buffer, smem P/dS buffer and
+// s_empty / p_full barriers, so one group's load -> exp -> store -> arrive latency chain overlaps the
+// other's; the MMA warp issues S(i) two iterations ahead of the gradient MMAs of iteration i-2.
+// After the loop every group needs all gradient MMAs done: wait this group's last commit first (its own
+// barrier, so the parity wait cannot alias an older phase), then the very last one.
+__device__ __forceinline__ void wait_all_done(uint64_t* g_done, int grp, int n) {
+  const int own = n - 1 >= grp ? n - 1 - ((n - 1 - grp) & 1) : -1;
+  if (own >= 0) mbar_wait(&g_done[grp], (own >> 1) & 1);
+  if (own != n - 1) mbar_wait(&g_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
+  fence_after();
+}
+
 // =============================================================================== dK / dV
+// TMEM (512 columns): S^T[2] at 0 / 64, dP^T[2] at 128 / 192, dV at 256, dK at 256 + DH.
+// The element-wise thread owning key row r and query columns [32h, 32h+32) of buffer b writes the bf16
+// P^T (dS^T) of those 32 queries, packed two per column, over the first 16 of the S^T (dP^T) columns it
+// has just read; the gradient MMAs read them as their TMEM A operand.  The MMA issuer therefore issues
+// S^T(i+2) into buffer b only after the gradient MMAs of iteration i have completed.
 constexpr int KB = 128;  // keys per CTA
 constexpr int QB = 64;   // queries per iteration
 
@@ -85,13 +116,11 @@ struct DkvSmem {
   static constexpr int QT = DH / 64 * SUB64;           // Q (or dO) tile [64][DH]
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = K_OFF + KT;
-  static constexpr int NST = 3;                        // Q / dO ring depth
+  static constexpr int NST = DH == 64 ? LGA_BWD_NST_DKV64 : LGA_BWD_NST_DKV128;   // Q / dO / lse / dsum ring
   static constexpr int Q_OFF = V_OFF + KT;             // [NST]
   static constexpr int G_OFF = Q_OFF + NST * QT;       // dO [NST]
-  static constexpr int PT_OFF = G_OFF + NST * QT;      // P^T [2][128][64]
-  static constexpr int DST_OFF = PT_OFF + 2 * SUB128;  // dS^T [2][128][64]
-  static constexpr int LD_OFF = DST_OFF + 2 * SUB128;  // lse[2][64], dsum[2][64] (floats)
-  static constexpr int BAR_OFF = LD_OFF + 4 * 64 * 4;
+  static constexpr int LD_OFF = G_OFF + NST * QT;      // [NST] x {lse[64], dsum[64]} fp32
+  static constexpr int BAR_OFF = LD_OFF + NST * 512;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
@@ -105,16 +134,15 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
   constexpr int NST = SM::NST;
   uint64_t* kv_full = bars + 0;
-  uint64_t* q_full = bars + 1;              // [NST]
+  uint64_t* q_full = bars + 1;              // [NST] (expect_tx + 32 cp.async arrivals)
   uint64_t* q_empty = q_full + NST;         // [NST]
-  uint64_t* s_full = q_empty + NST;         // [2]
-  uint64_t* s_empty = s_full + 2;           // [2] (EW_THREADS arrivals)
-  uint64_t* p_full = s_empty + 2;           // (EW_THREADS arrivals)
-  uint64_t* g_done = p_full + 1;            // [2] per P^T / dS^T buffer
-  constexpr int NBAR = 2 * NST + 8;
+  uint64_t* s_full = q_empty + NST;         // [2] per group / TMEM buffer
+  uint64_t* p_full = s_full + 2;            // [2] (GRP_THREADS arrivals)
+  uint64_t* g_done = p_full + 2;            // [2]
+  constexpr int NBAR = 2 * NST + 7;
+  static_assert(NBAR * 8 + 4 <= 256, "barrier area");
+  static_assert(SM::TOTAL <= 232448, "shared memory");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
-  float* lse_s = reinterpret_cast<float*>(smem + SM::LD_OFF);   // [2][64]
-  float* dsum_s = lse_s + 128;                                   // [2][64]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, h = blockIdx.y, sq = blockIdx.z;
@@ -123,12 +151,13 @@ __global__ void __launch_bounds__(NT, 1)
   const int nq_all = (s + QB - 1) / QB;
   const int qstart = a.causal ? k0 / QB : 0;
   const int nq = nq_all - qstart;
-  const int64_t rb = ((int64_t)sq * a.heads + h) * s;   // row base of lse / dsum
+  const int rb = (sq * a.heads + h) * s;   // row base of lse / dsum
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < NBAR; ++i) {
-      const bool ew = &bars[i] == s_empty || &bars[i] == s_empty + 1 || &bars[i] == p_full;
-      mbar_init(&bars[i], ew ? EW_THREADS : 1);
+      const bool qf = (&bars[i] >= q_full && &bars[i] < q_empty);
+      const bool ew = (&bars[i] >= p_full && &bars[i] < g_done);
+      mbar_init(&bars[i], qf ? 33 : ew ? GRP_THREADS : 1);
     }
     mbar_fence_init();
     prefetch_tmap(&tm_kv);
@@ -140,21 +169,24 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   fence_after();
   const uint32_t tb = *tmem_slot;
-  const uint32_t t_st[2] = {tb, tb + 64}, t_dpt[2] = {tb + 128, tb + 192};
+  auto t_st = [&](int b) { return tb + 64 * b; };
+  auto t_dpt = [&](int b) { return tb + 128 + 64 * b; };
   const uint32_t t_dv = tb + 256, t_dk = tb + 256 + DH;
 
-  if (warp == 0) {
-    if (lane == 0) {  // ===== TMA producer
+  if (warp == 0) {  // ===== producer: TMA (lane 0) + lse / dsum cp.async (all lanes)
+    if (lane == 0) {
       mbar_expect_tx(kv_full, 2 * SM::KT);
 #pragma unroll
       for (int i = 0; i < DH / 64; ++i) {
         tma_load_3d(smem + SM::K_OFF + i * SM::SUB128, &tm_kv, kv_full, d + h * DH + 64 * i, k0, sq);
         tma_load_3d(smem + SM::V_OFF + i * SM::SUB128, &tm_kv, kv_full, 2 * d + h * DH + 64 * i, k0, sq);
       }
-      for (int i = 0; i < nq; ++i) {
-        const int st = i % NST;
-        const int q0 = (qstart + i) * QB;
-        mbar_wait(&q_empty[st], ((i / NST) & 1) ^ 1);
+    }
+    for (int i = 0; i < nq; ++i) {
+      const int st = i % NST;
+      const int q0 = (qstart + i) * QB;
+      mbar_wait(&q_empty[st], ((i / NST) & 1) ^ 1);
+      if (lane == 0) {
         mbar_expect_tx(&q_full[st], 2 * SM::QT);
 #pragma unroll
         for (int c = 0; c < DH / 64; ++c) {
@@ -162,128 +194,120 @@ __global__ void __launch_bounds__(NT, 1)
           tma_load_3d(smem + SM::G_OFF + st * SM::QT + c * SM::SUB64, &tm_g, &q_full[st], h * DH + 64 * c, q0, sq);
         }
       }
+      // lse / dsum of the 64 queries (zero past the sequence end; those queries are masked)
+      float* ld = reinterpret_cast<float*>(smem + SM::LD_OFF + st * 512);
+#pragma unroll
+      for (int e = lane; e < 128; e += 32) {
+        const int q = q0 + (e & 63);
+        cp_async4(ld + e, (e < 64 ? a.lse : a.dsum) + rb + min(q, s - 1), q < s);
+      }
+      cp_async_mbar_arrive(&q_full[st]);
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ===== MMA issuer
       constexpr uint32_t idesc_s = make_idesc(128, QB, false, false);
       constexpr uint32_t idesc_g = make_idesc(128, DH, false, true);
       const uint32_t sK = smem_u32(smem + SM::K_OFF), sV = smem_u32(smem + SM::V_OFF);
-      const uint32_t sPt = smem_u32(smem + SM::PT_OFF), sDSt = smem_u32(smem + SM::DST_OFF);
-      mbar_wait(kv_full, 0);
-      for (int i = 0; i <= nq; ++i) {
-        if (i < nq) {
-          const int st = i % NST, b = i & 1;
-          mbar_wait(&q_full[st], (i / NST) & 1);
-          mbar_wait(&s_empty[b], ((i >> 1) & 1) ^ 1);
-          fence_after();
-          const uint32_t sQ = smem_u32(smem + SM::Q_OFF + st * SM::QT);
-          const uint32_t sG = smem_u32(smem + SM::G_OFF + st * SM::QT);
+      auto issue_s = [&](int i) {   // S^T(i) = K Q^T, dP^T(i) = V dO^T into buffer i & 1
+        const int st = i % NST, b = i & 1;
+        mbar_wait(&q_full[st], (i / NST) & 1);
+        fence_after();
+        const uint32_t sQ = smem_u32(smem + SM::Q_OFF + st * SM::QT);
+        const uint32_t sG = smem_u32(smem + SM::G_OFF + st * SM::QT);
 #pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk) {
-            const uint32_t oa = (kk >> 2) * SM::SUB128 + (kk & 3) * 32, ob = (kk >> 2) * SM::SUB64 + (kk & 3) * 32;
-            umma_f16(t_st[b], make_desc(sK + oa, 16, 1024), make_desc(sQ + ob, 16, 1024), idesc_s, kk > 0);
-            umma_f16(t_dpt[b], make_desc(sV + oa, 16, 1024), make_desc(sG + ob, 16, 1024), idesc_s, kk > 0);
-          }
-          umma_commit(&s_full[b]);
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * SM::SUB128 + (kk & 3) * 32, ob = (kk >> 2) * SM::SUB64 + (kk & 3) * 32;
+          umma_f16(t_st(b), make_desc(sK + oa, 16, 1024), make_desc(sQ + ob, 16, 1024), idesc_s, kk > 0);
+          umma_f16(t_dpt(b), make_desc(sV + oa, 16, 1024), make_desc(sG + ob, 16, 1024), idesc_s, kk > 0);
         }
-        if (i >= 1) {
-          const int ii = i - 1, st = ii % NST, pb = ii & 1;
-          mbar_wait(p_full, ii & 1);
-          fence_after();
-          const uint32_t sQ = smem_u32(smem + SM::Q_OFF + st * SM::QT);
-          const uint32_t sG = smem_u32(smem + SM::G_OFF + st * SM::QT);
-          const uint32_t sPtb = sPt + pb * SM::SUB128, sDStb = sDSt + pb * SM::SUB128;
+        umma_commit(&s_full[b]);
+      };
+      mbar_wait(kv_full, 0);
+      issue_s(0);
+      if (nq > 1) issue_s(1);
+      for (int i = 0; i < nq; ++i) {  // dV += P^T dO, dK += dS^T Q (A from TMEM), then S^T(i+2)
+        const int st = i % NST, b = i & 1;
+        mbar_wait(&p_full[b], (i >> 1) & 1);
+        fence_after();
+        const uint32_t sQ = smem_u32(smem + SM::Q_OFF + st * SM::QT);
+        const uint32_t sG = smem_u32(smem + SM::G_OFF + st * SM::QT);
 #pragma unroll
-          for (int kk = 0; kk < QB / 16; ++kk) {
-            const uint32_t oa = kk * 32;                // K-major A: 16 queries = 32 B into the swizzle span
-            const uint32_t ob = kk * 16 * 128;          // MN-major B: 16 query rows
-            const uint32_t acc = (ii > 0 || kk > 0) ? 1u : 0u;
-            umma_f16(t_dv, make_desc(sPtb + oa, 16, 1024), make_desc(sG + ob, SM::SUB64, 1024), idesc_g, acc);
-            umma_f16(t_dk, make_desc(sDStb + oa, 16, 1024), make_desc(sQ + ob, SM::SUB64, 1024), idesc_g, acc);
-          }
-          umma_commit(&g_done[pb]);
-          umma_commit(&q_empty[st]);
+        for (int kk = 0; kk < QB / 16; ++kk) {
+          const uint32_t ta = 32 * (kk >> 1) + 8 * (kk & 1);   // 16 queries: owner half, 8 packed columns
+          const uint32_t ob = kk * 16 * 128;                   // MN-major B: 16 query rows
+          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+          umma_f16_ts(t_dv, t_st(b) + ta, make_desc(sG + ob, SM::SUB64, 1024), idesc_g, acc);
+          umma_f16_ts(t_dk, t_dpt(b) + ta, make_desc(sQ + ob, SM::SUB64, 1024), idesc_g, acc);
+        }
+        umma_commit(&g_done[b]);
+        umma_commit(&q_empty[st]);
+        if (i + 2 < nq) {
+          mbar_wait(&g_done[b], (i >> 1) & 1);   // P^T / dS^T of iteration i consumed: buffer b free
+          fence_after();
+          issue_s(i + 2);
         }
       }
     }
-  } else if (warp >= 4) {  // ===== element-wise: one key row per 4 threads (query-column quarters)
+  } else if (warp >= 4) {  // ===== element-wise: ping-pong groups, one key row per 2 threads of a group
+    const int grp = (warp - 4) >> 3;
+    const int hf = ((warp - 4) >> 2) & 1;       // half (32 columns) of the 64 query columns
     const int qd = warp & 3;
-    const int hf = (warp - 4) >> 2;            // quarter 0..3 of the 64 query columns
     const int r = qd * 32 + lane;
-    const int tid = threadIdx.x - 128;
     const int kj = k0 + r;
     const uint32_t lrow = (uint32_t)(qd * 32) << 16;
     const float sl2 = a.scale * LOG2E;
-    uint8_t* sPt = smem + SM::PT_OFF;
-    uint8_t* sDSt = smem + SM::DST_OFF;
-    // lse (log2 units) / dsum of query tile i: loaded two iterations ahead into a register by threads
-    // tid < 128, parked in shared buffer i&1 at the end of iteration i-1 (barrier at the top of i)
-    auto ld_stat = [&](int i) -> float {
-      const int q = (qstart + i) * QB + (tid & 63);
-      if (tid >= 128 || i >= nq || q >= s) return 0.f;
-      return tid < 64 ? a.lse[rb + q] * LOG2E : a.dsum[rb + q];
-    };
-    if (tid < 128) (tid < 64 ? lse_s : dsum_s)[tid & 63] = ld_stat(0);
-    float pre1 = ld_stat(1);
-    for (int i = 0; i < nq; ++i) {
-      const float pre2 = ld_stat(i + 2);
-      const int b = i & 1, st = i & 1;
-      const int q0 = (qstart + i) * QB;
-      mbar_wait(&s_full[b], (i >> 1) & 1);
-      fence_after();
-      uint32_t rsv[16], rdp[16];
-      tmem_ld16_nowait(t_st[b] + lrow + hf * 16, rsv);
-      tmem_ld16_nowait(t_dpt[b] + lrow + hf * 16, rdp);
-      tmem_wait_ld();
-      fence_before();
-      mbar_arrive(&s_empty[b]);
-      asm volatile("bar.sync 1, %0;" ::"n"(EW_THREADS) : "memory");   // tile i's lse / dsum visible
-      const float* ls = lse_s + st * 64 + hf * 16;
-      const float* ds_ = dsum_s + st * 64 + hf * 16;
+    for (int i = grp; i < nq; i += 2) {
+      const int st = i % NST;
+      const int qa = (qstart + i) * QB + hf * 32;
+      const float* ls = reinterpret_cast<const float*>(smem + SM::LD_OFF + st * 512) + hf * 32;
+      const float* dsm = ls + 64;
       // valid iff q < s, kj < s and (causal) kj <= q; only tiles touching the diagonal / the end mask
-      const int qa = q0 + hf * 16;
-      const bool need_mask = kj >= s || qa + 16 > s || (a.causal && kj > qa);
-      float sc[16];
+      const bool need_mask = kj >= s || qa + 32 > s || (a.causal && kj > qa);
+      mbar_wait(&s_full[grp], (i >> 1) & 1);
+      fence_after();
+      mbar_wait(&q_full[st], (i / NST) & 1);   // lse / dsum of tile i landed with Q / dO
 #pragma unroll
-      for (int c = 0; c < 16; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -ls[c]);
-      if (need_mask) {
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t rsv[16], rdp[16];
+        tmem_ld16_nowait(t_st(grp) + lrow + hf * 32 + ch * 16, rsv);
+        tmem_ld16_nowait(t_dpt(grp) + lrow + hf * 32 + ch * 16, rdp);
+        tmem_wait_ld();
+        float sc[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const int q = qa + c;
-          if (!(q < s && kj < s && (!a.causal || kj <= q))) sc[c] = -INFINITY;
+        for (int c = 0; c < 16; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -ls[ch * 16 + c] * LOG2E);
+        if (need_mask) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const int q = qa + ch * 16 + c;
+            if (!(q < s && kj < s && (!a.causal || kj <= q))) sc[c] = -INFINITY;
+          }
         }
-      }
-      uint32_t pp[8], pd[8];
+        uint32_t pp[8], pd[8];
 #pragma unroll
-      for (int c = 0; c < 16; c += 2) {
-        float p[2], g[2];
+        for (int c = 0; c < 16; c += 2) {
+          float p[2], g[2];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          p[e] = ex2(sc[c + e]);
-          g[e] = p[e] * (__uint_as_float(rdp[c + e]) - ds_[c + e]) * a.scale;
+          for (int e = 0; e < 2; ++e) {
+            p[e] = ex2(sc[c + e]);
+            g[e] = p[e] * (__uint_as_float(rdp[c + e]) - dsm[ch * 16 + c + e]) * a.scale;
+          }
+          pp[c / 2] = pack_bf16x2(p[0], p[1]);
+          pd[c / 2] = pack_bf16x2(g[0], g[1]);
         }
-        pp[c / 2] = pack_bf16x2(p[0], p[1]);
-        pd[c / 2] = pack_bf16x2(g[0], g[1]);
+        // packed columns 32h + 8ch .. +7 lie inside chunk 0's range, already read by this thread
+        tmem_st8_nowait(t_st(grp) + lrow + hf * 32 + ch * 8, pp);
+        tmem_st8_nowait(t_dpt(grp) + lrow + hf * 32 + ch * 8, pd);
       }
-      const int pb = i & 1;
-      if (i >= 2) {
-        mbar_wait(&g_done[pb], ((i >> 1) & 1) ^ 1);   // dV/dK MMAs of iteration i-2 done: buffer pb free
-        fence_after();
-      }
-      st_quarter_row_bf16(sPt + pb * SM::SUB128, r, hf, pp);
-      st_quarter_row_bf16(sDSt + pb * SM::SUB128, r, hf, pd);
-      fence_proxy_async();
+      tmem_wait_st();
       fence_before();
-      mbar_arrive(p_full);
-      if (tid < 128) (tid < 64 ? lse_s : dsum_s)[(st ^ 1) * 64 + (tid & 63)] = pre1;   // tile i+1
-      pre1 = pre2;
+      mbar_arrive(&p_full[grp]);
     }
-    mbar_wait(&g_done[(nq - 1) & 1], ((nq - 1) >> 1) & 1);   // last iteration's MMAs (and all earlier) done
-    fence_after();
-    constexpr int OC = DH / 4;   // output columns per quarter
-    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + kj) * 3 * d + h * DH + hf * OC;
-    store_row_bf16_global(out + d, t_dk + lrow + hf * OC, OC, 1.f, kj < s);
-    store_row_bf16_global(out + 2 * d, t_dv + lrow + hf * OC, OC, 1.f, kj < s);
+    wait_all_done(g_done, grp, nq);
+    constexpr int OC = DH / 4;   // output columns per (group, half)
+    const int oq = grp * 2 + hf;
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + kj) * 3 * d + h * DH + oq * OC;
+    store_row_bf16_global(out + d, t_dk + lrow + oq * OC, OC, 1.f, kj < s);
+    store_row_bf16_global(out + 2 * d, t_dv + lrow + oq * OC, OC, 1.f, kj < s);
   }
   fence_before();
   __syncthreads();
@@ -294,6 +318,7 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 // =============================================================================== dQ
+// TMEM: S[2] at 0 / 64, dP[2] at 128 / 192, dQ at 256, dS[2] (bf16 packed, 32 columns) at 384 / 416.
 constexpr int QB2 = 128;  // queries per CTA
 constexpr int KB2 = 64;   // keys per iteration
 
@@ -305,11 +330,10 @@ struct DqSmem {
   static constexpr int KT = DH / 64 * SUB64;    // K (or V) [64][DH]
   static constexpr int Q_OFF = 0;
   static constexpr int G_OFF = Q_OFF + QT;
-  static constexpr int NST = 4;                 // K / V ring depth
+  static constexpr int NST = DH == 64 ? LGA_BWD_NST_DQ64 : LGA_BWD_NST_DQ128;   // K / V ring depth
   static constexpr int K_OFF = G_OFF + QT;      // [NST]
   static constexpr int V_OFF = K_OFF + NST * KT;  // [NST]
-  static constexpr int DS_OFF = V_OFF + NST * KT; // dS [2][128][64]
-  static constexpr int BAR_OFF = DS_OFF + 2 * SUB128;
+  static constexpr int BAR_OFF = V_OFF + NST * KT;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
@@ -325,11 +349,13 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* qg_full = bars + 0;
   uint64_t* kv_full = bars + 1;             // [NST]
   uint64_t* kv_empty = kv_full + NST;       // [NST]
-  uint64_t* s_full = kv_empty + NST;        // [2]
-  uint64_t* s_empty = s_full + 2;           // [2] (EW_THREADS)
-  uint64_t* p_full = s_empty + 2;           // (EW_THREADS)
-  uint64_t* g_done = p_full + 1;            // [2] per dS buffer
-  constexpr int NBAR = 2 * NST + 8;
+  uint64_t* s_full = kv_empty + NST;        // [2] per group
+  uint64_t* s_empty = s_full + 2;           // [2] (GRP_THREADS)
+  uint64_t* p_full = s_empty + 2;           // [2] (GRP_THREADS)
+  uint64_t* g_done = p_full + 2;            // [2] per dS buffer
+  constexpr int NBAR = 2 * NST + 9;
+  static_assert(NBAR * 8 + 4 <= 256, "barrier area");
+  static_assert(SM::TOTAL <= 232448, "shared memory");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -343,8 +369,8 @@ __global__ void __launch_bounds__(NT, 1)
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < NBAR; ++i) {
-      const bool ew = &bars[i] == s_empty || &bars[i] == s_empty + 1 || &bars[i] == p_full;
-      mbar_init(&bars[i], ew ? EW_THREADS : 1);
+      const bool ew = (&bars[i] >= s_empty && &bars[i] < g_done);
+      mbar_init(&bars[i], ew ? GRP_THREADS : 1);
     }
     mbar_fence_init();
     prefetch_tmap(&tm_q);
@@ -356,7 +382,9 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   fence_after();
   const uint32_t tb = *tmem_slot;
-  const uint32_t t_s[2] = {tb, tb + 64}, t_dp[2] = {tb + 128, tb + 192};
+  auto t_s = [&](int b) { return tb + 64 * b; };
+  auto t_dp = [&](int b) { return tb + 128 + 64 * b; };
+  auto t_ds = [&](int b) { return tb + 384 + 32 * b; };
   const uint32_t t_dq = tb + 256;
 
   if (warp == 0) {
@@ -384,10 +412,9 @@ __global__ void __launch_bounds__(NT, 1)
       constexpr uint32_t idesc_s = make_idesc(128, KB2, false, false);
       constexpr uint32_t idesc_q = make_idesc(128, DH, false, true);
       const uint32_t sQ = smem_u32(smem + SM::Q_OFF), sG = smem_u32(smem + SM::G_OFF);
-      const uint32_t sDS = smem_u32(smem + SM::DS_OFF);
       mbar_wait(qg_full, 0);
-      for (int j = 0; j <= nk; ++j) {
-        if (j < nk) {
+      for (int j = 0; j < nk + 2; ++j) {
+        if (j < nk) {  // S(j), dP(j)
           const int st = j % NST, b = j & 1;
           mbar_wait(&kv_full[st], (j / NST) & 1);
           mbar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);
@@ -397,28 +424,29 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int kk = 0; kk < DH / 16; ++kk) {
             const uint32_t oa = (kk >> 2) * SM::SUB128 + (kk & 3) * 32, ob = (kk >> 2) * SM::SUB64 + (kk & 3) * 32;
-            umma_f16(t_s[b], make_desc(sQ + oa, 16, 1024), make_desc(sK + ob, 16, 1024), idesc_s, kk > 0);
-            umma_f16(t_dp[b], make_desc(sG + oa, 16, 1024), make_desc(sV + ob, 16, 1024), idesc_s, kk > 0);
+            umma_f16(t_s(b), make_desc(sQ + oa, 16, 1024), make_desc(sK + ob, 16, 1024), idesc_s, kk > 0);
+            umma_f16(t_dp(b), make_desc(sG + oa, 16, 1024), make_desc(sV + ob, 16, 1024), idesc_s, kk > 0);
           }
           umma_commit(&s_full[b]);
         }
-        if (j >= 1) {
-          const int jj = j - 1, st = jj % NST, pb = jj & 1;
-          mbar_wait(p_full, jj & 1);
+        if (j >= 2) {  // dQ += dS K of iteration j-2 (A = dS from TMEM)
+          const int jj = j - 2, st = jj % NST, pb = jj & 1;
+          mbar_wait(&p_full[pb], (jj >> 1) & 1);
           fence_after();
           const uint32_t sK = smem_u32(smem + SM::K_OFF + st * SM::KT);
 #pragma unroll
           for (int kk = 0; kk < KB2 / 16; ++kk)
-            umma_f16(t_dq, make_desc(sDS + pb * SM::SUB128 + kk * 32, 16, 1024),
-                     make_desc(sK + kk * 16 * 128, SM::SUB64, 1024), idesc_q, (jj > 0 || kk > 0) ? 1u : 0u);
+            umma_f16_ts(t_dq, t_ds(pb) + 16 * (kk >> 1) + 8 * (kk & 1), make_desc(sK + kk * 16 * 128, SM::SUB64, 1024),
+                        idesc_q, (jj > 0 || kk > 0) ? 1u : 0u);
           umma_commit(&g_done[pb]);
           umma_commit(&kv_empty[st]);
         }
       }
     }
-  } else if (warp >= 4) {  // ===== element-wise: one query row per 4 threads (key-column quarters)
+  } else if (warp >= 4) {  // ===== element-wise: ping-pong groups, one query row per 2 threads of a group
+    const int grp = (warp - 4) >> 3;
+    const int hf = ((warp - 4) >> 2) & 1;       // half (32 columns) of the 64 key columns
     const int qd = warp & 3;
-    const int hf = (warp - 4) >> 2;            // quarter 0..3 of the 64 key columns
     const int r = qd * 32 + lane;
     const int q = q0 + r;
     const uint32_t lrow = (uint32_t)(qd * 32) << 16;
@@ -426,52 +454,54 @@ __global__ void __launch_bounds__(NT, 1)
     const int64_t rb = ((int64_t)sq * a.heads + h) * s;
     const float lse2 = q < s ? a.lse[rb + q] * LOG2E : 0.f;
     const float Dq = q < s ? a.dsum[rb + q] : 0.f;
-    uint8_t* sDS = smem + SM::DS_OFF;
-    for (int j = 0; j < nk; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
+    for (int j = grp; j < nk; j += 2) {
+      const int ka = j * KB2 + hf * 32;
+      const bool need_mask = q >= s || ka + 32 > s || (a.causal && ka + 31 > q0 + qd * 32);
+      mbar_wait(&s_full[grp], (j >> 1) & 1);
       fence_after();
-      uint32_t rsv[16], rdp[16];
-      tmem_ld16_nowait(t_s[b] + lrow + hf * 16, rsv);
-      tmem_ld16_nowait(t_dp[b] + lrow + hf * 16, rdp);
-      tmem_wait_ld();
-      fence_before();
-      mbar_arrive(&s_empty[b]);
-      const int ka = j * KB2 + hf * 16;
-      const bool need_mask = q >= s || ka + 16 > s || (a.causal && ka + 15 > q0 + qd * 32);
-      float sc[16];
+      uint32_t pd[16];
 #pragma unroll
-      for (int c = 0; c < 16; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -lse2);
-      if (need_mask) {
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t rsv[16], rdp[16];
+        tmem_ld16_nowait(t_s(grp) + lrow + hf * 32 + ch * 16, rsv);
+        tmem_ld16_nowait(t_dp(grp) + lrow + hf * 32 + ch * 16, rdp);
+        tmem_wait_ld();
+        if (ch == 1) {
+          fence_before();
+          mbar_arrive(&s_empty[grp]);
+        }
+        float sc[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const int kj = ka + c;
-          if (!(q < s && kj < s && (!a.causal || kj <= q))) sc[c] = -INFINITY;
+        for (int c = 0; c < 16; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -lse2);
+        if (need_mask) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const int kj = ka + ch * 16 + c;
+            if (!(q < s && kj < s && (!a.causal || kj <= q))) sc[c] = -INFINITY;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 16; c += 2) {
+          float g[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) g[e] = ex2(sc[c + e]) * (__uint_as_float(rdp[c + e]) - Dq) * a.scale;
+          pd[ch * 8 + c / 2] = pack_bf16x2(g[0], g[1]);
         }
       }
-      uint32_t pd[8];
-#pragma unroll
-      for (int c = 0; c < 16; c += 2) {
-        float g[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) g[e] = ex2(sc[c + e]) * (__uint_as_float(rdp[c + e]) - Dq) * a.scale;
-        pd[c / 2] = pack_bf16x2(g[0], g[1]);
-      }
-      const int pb = j & 1;
       if (j >= 2) {
-        mbar_wait(&g_done[pb], ((j >> 1) & 1) ^ 1);   // dQ MMAs of iteration j-2 done: buffer pb free
+        mbar_wait(&g_done[grp], ((j >> 1) & 1) ^ 1);   // dQ MMAs of iteration j-2 done: dS buffer free
         fence_after();
       }
-      st_quarter_row_bf16(sDS + pb * SM::SUB128, r, hf, pd);
-      fence_proxy_async();
+      tmem_st16_nowait(t_ds(grp) + lrow + hf * 16, pd);
+      tmem_wait_st();
       fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[grp]);
     }
-    mbar_wait(&g_done[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
-    fence_after();
+    wait_all_done(g_done, grp, nk);
     constexpr int OC = DH / 4;
-    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + q) * 3 * d + h * DH + hf * OC;
-    store_row_bf16_global(out, t_dq + lrow + hf * OC, OC, 1.f, q < s);
+    const int oq = grp * 2 + hf;
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + q) * 3 * d + h * DH + oq * OC;
+    store_row_bf16_global(out, t_dq + lrow + oq * OC, OC, 1.f, q < s);
   }
   fence_before();
   __syncthreads();

@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+timeout 400 python -m pytest tests/test_gpu_kernels.py -q -x -k attention 2>&1 | tail -3
+timeout 120 python tools/kbench.py attn 2>&1 | grep bwd; timeout 120 python tools/kbench.py attn --dh 64 --heads 32 2>&1 | grep bwd
+timeout 300 python -m pytest tests/test_gpu_step.py -q -x 2>&1 | tail -2
