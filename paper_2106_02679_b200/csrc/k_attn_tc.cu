@@ -119,56 +119,62 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ===== MMA issuer
-      constexpr uint32_t idesc_s = make_idesc(128, BKV, false, false);
-      constexpr uint32_t idesc_o = make_idesc(128, DH, false, true);
-      const uint32_t sQ = smem_u32(smem + SM::Q_OFF);
-      const uint32_t sP = smem_u32(smem + SM::P_OFF);
-      int js = 0;   // global S / KV tile counter
-      int it = 0;
-      for (int t = blockIdx.x; t < n_items; t += gridDim.x, ++it) {
-        int qt, h, sq, nkv;
-        item(t, qt, h, sq, nkv);
-        mbar_wait(q_full, it & 1);
-        const int j0 = js;   // global index of this item's first tile
-        for (int j = 0; j <= nkv; ++j) {
-          if (j < nkv) {
-            const int g = j0 + j, st = g & 1, b = g & 1;
-            mbar_wait(&k_full[st], (g >> 1) & 1);
-            mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
-            fence_after();
-            const uint32_t sK = smem_u32(smem + SM::K_OFF + st * SM::TILE);
+  } else if (warp == 1) {  // ===== MMA issuer (whole warp; one elected lane issues)
+    constexpr uint32_t idesc_s = make_idesc(128, BKV, false, false);
+    constexpr uint32_t idesc_o = make_idesc(128, DH, false, true);
+    const bool leader = elect_one();
+    const uint64_t dQ = make_desc(smem_u32(smem + SM::Q_OFF), 16, 1024);
+    const uint64_t dK = make_desc(smem_u32(smem + SM::K_OFF), 16, 1024);
+    const uint64_t dP = make_desc(smem_u32(smem + SM::P_OFF), 16, 1024);
+    const uint64_t dVm = make_desc(smem_u32(smem + SM::V_OFF), SM::SUB, 1024);   // MN-major: d_h blocks at 16 KB
+    int js = 0;   // global S / KV tile counter
+    int it = 0;
+    for (int t = blockIdx.x; t < n_items; t += gridDim.x, ++it) {
+      int qt, h, sq, nkv;
+      item(t, qt, h, sq, nkv);
+      mbar_wait(q_full, it & 1);
+      const int j0 = js;   // global index of this item's first tile
+      for (int j = 0; j <= nkv; ++j) {
+        if (j < nkv) {
+          const int g = j0 + j, st = g & 1, b = g & 1;
+          mbar_wait(&k_full[st], (g >> 1) & 1);
+          mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
+          fence_after();
+          const uint64_t dk = desc_add(dK, st * SM::TILE);
+          if (leader) {
 #pragma unroll
             for (int kk = 0; kk < DH / 16; ++kk) {
               const uint32_t off = (kk >> 2) * SM::SUB + (kk & 3) * 32;
-              umma_f16(t_s[b], make_desc(sQ + off, 16, 1024), make_desc(sK + off, 16, 1024), idesc_s, kk > 0);
+              umma_f16(tbase + 128 * b, desc_add(dQ, off), desc_add(dk, off), idesc_s, kk > 0);
             }
             umma_commit(&s_full[b]);
             if (j == nkv - 1) umma_commit(q_empty);   // Q no longer needed by this item
           }
-          if (j >= 1) {
-            const int jj = j - 1, g = j0 + jj, st = g & 1;
-            if (jj == 0) mbar_wait(o_free, (it & 1) ^ 1);   // previous item's epilogue has read O
-            mbar_wait(&v_full[st], (g >> 1) & 1);
-            const uint32_t sV = smem_u32(smem + SM::V_OFF + st * SM::TILE);
+          __syncwarp();
+        }
+        if (j >= 1) {
+          const int jj = j - 1, g = j0 + jj, st = g & 1;
+          if (jj == 0) mbar_wait(o_free, (it & 1) ^ 1);   // previous item's epilogue has read O
+          mbar_wait(&v_full[st], (g >> 1) & 1);
+          const uint64_t dv = desc_add(dVm, st * SM::TILE);
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {   // O_h += P_h V_h over keys 64h .. 64h+63
-              mbar_wait(&p_full[hh], g & 1);
-              fence_after();
+          for (int hh = 0; hh < 2; ++hh) {   // O_h += P_h V_h over keys 64h .. 64h+63
+            mbar_wait(&p_full[hh], g & 1);
+            fence_after();
+            if (leader) {
 #pragma unroll
-              for (int kk = 4 * hh; kk < 4 * hh + 4; ++kk) {
-                const uint64_t ad = make_desc(sP + hh * SM::SUB + (kk & 3) * 32, 16, 1024);
-                const uint64_t bd = make_desc(sV + kk * 16 * 128, SM::SUB, 1024);   // MN-major: d_h blocks at 16 KB
-                umma_f16(t_o[hh], ad, bd, idesc_o, (jj > 0 || kk > 4 * hh) ? 1u : 0u);
-              }
+              for (int kk = 4 * hh; kk < 4 * hh + 4; ++kk)
+                umma_f16(t_o[hh], desc_add(dP, hh * SM::SUB + (kk & 3) * 32), desc_add(dv, kk * 16 * 128), idesc_o,
+                         (jj > 0 || kk > 4 * hh) ? 1u : 0u);
               umma_commit(&o_done[hh]);
             }
-            umma_commit(&kv_empty[st]);
+            __syncwarp();
           }
+          if (leader) umma_commit(&kv_empty[st]);
+          __syncwarp();
         }
-        js += nkv;
       }
+      js += nkv;
     }
   } else if (warp >= 4) {  // ===== softmax + epilogue: one query row and one key half per thread
     const int qd = warp & 3;

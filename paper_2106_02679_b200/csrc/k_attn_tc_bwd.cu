@@ -76,6 +76,16 @@ __device__ __forceinline__ void store_row_bf16_global(__nv_bfloat16* dst, uint32
   }
 }
 
+#ifdef LGA_BWD_TRACE
+// Timing-only instrumentation (development builds): SM clock64() at pipeline events of the 16 dK/dV CTAs
+// of (sequence 0, head 0): [kt][i][event], row 39 = CTA start / K,V landed / end.
+__device__ long long g_bwd_trace[16][40][8];
+#define BTR(i, k) \
+  if (blockIdx.y == 0 && blockIdx.z == 0 && blockIdx.x < 16) g_bwd_trace[blockIdx.x][i][k] = clock64()
+#else
+#define BTR(i, k)
+#endif
+
 // 4-byte cp.async global -> shared (zero-filled when !valid) and its completion arriving on an mbarrier
 // (.noinc: the barrier's expected count includes one arrival per issuing thread)
 __device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
@@ -154,6 +164,7 @@ __global__ void __launch_bounds__(NT, 1)
   const int rb = (sq * a.heads + h) * s;   // row base of lse / dsum
 
   if (warp == 0 && lane == 0) {
+    BTR(39, 0);
     for (int i = 0; i < NBAR; ++i) {
       const bool qf = (&bars[i] >= q_full && &bars[i] < q_empty);
       const bool ew = (&bars[i] >= p_full && &bars[i] < g_done);
@@ -203,49 +214,63 @@ __global__ void __launch_bounds__(NT, 1)
       }
       cp_async_mbar_arrive(&q_full[st]);
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ===== MMA issuer
-      constexpr uint32_t idesc_s = make_idesc(128, QB, false, false);
-      constexpr uint32_t idesc_g = make_idesc(128, DH, false, true);
-      const uint32_t sK = smem_u32(smem + SM::K_OFF), sV = smem_u32(smem + SM::V_OFF);
-      auto issue_s = [&](int i) {   // S^T(i) = K Q^T, dP^T(i) = V dO^T into buffer i & 1
-        const int st = i % NST, b = i & 1;
-        mbar_wait(&q_full[st], (i / NST) & 1);
-        fence_after();
-        const uint32_t sQ = smem_u32(smem + SM::Q_OFF + st * SM::QT);
-        const uint32_t sG = smem_u32(smem + SM::G_OFF + st * SM::QT);
+  } else if (warp == 1) {  // ===== MMA issuer (whole warp; one elected lane issues)
+    constexpr uint32_t idesc_s = make_idesc(128, QB, false, false);
+    constexpr uint32_t idesc_g = make_idesc(128, DH, false, true);
+    const bool leader = elect_one();
+    const uint64_t dK = make_desc(smem_u32(smem + SM::K_OFF), 16, 1024);
+    const uint64_t dV = make_desc(smem_u32(smem + SM::V_OFF), 16, 1024);
+    const uint64_t dQk = make_desc(smem_u32(smem + SM::Q_OFF), 16, 1024);          // Q, K-major
+    const uint64_t dGk = make_desc(smem_u32(smem + SM::G_OFF), 16, 1024);          // dO, K-major
+    const uint64_t dQm = make_desc(smem_u32(smem + SM::Q_OFF), SM::SUB64, 1024);   // Q, MN-major
+    const uint64_t dGm = make_desc(smem_u32(smem + SM::G_OFF), SM::SUB64, 1024);   // dO, MN-major
+    auto issue_s = [&](int i) {   // S^T(i) = K Q^T, dP^T(i) = V dO^T into buffer i & 1
+      const int st = i % NST, b = i & 1;
+      mbar_wait(&q_full[st], (i / NST) & 1);
+      BTR(i, 3);
+      fence_after();
+      const uint64_t dq = desc_add(dQk, st * SM::QT), dg = desc_add(dGk, st * SM::QT);
+      if (leader) {
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t oa = (kk >> 2) * SM::SUB128 + (kk & 3) * 32, ob = (kk >> 2) * SM::SUB64 + (kk & 3) * 32;
-          umma_f16(t_st(b), make_desc(sK + oa, 16, 1024), make_desc(sQ + ob, 16, 1024), idesc_s, kk > 0);
-          umma_f16(t_dpt(b), make_desc(sV + oa, 16, 1024), make_desc(sG + ob, 16, 1024), idesc_s, kk > 0);
+          umma_f16(t_st(b), desc_add(dK, oa), desc_add(dq, ob), idesc_s, kk > 0);
+          umma_f16(t_dpt(b), desc_add(dV, oa), desc_add(dg, ob), idesc_s, kk > 0);
         }
         umma_commit(&s_full[b]);
-      };
-      mbar_wait(kv_full, 0);
-      issue_s(0);
-      if (nq > 1) issue_s(1);
-      for (int i = 0; i < nq; ++i) {  // dV += P^T dO, dK += dS^T Q (A from TMEM), then S^T(i+2)
-        const int st = i % NST, b = i & 1;
-        mbar_wait(&p_full[b], (i >> 1) & 1);
-        fence_after();
-        const uint32_t sQ = smem_u32(smem + SM::Q_OFF + st * SM::QT);
-        const uint32_t sG = smem_u32(smem + SM::G_OFF + st * SM::QT);
+      }
+      __syncwarp();
+    };
+    mbar_wait(kv_full, 0);
+    BTR(39, 1);
+    issue_s(0);
+    if (nq > 1) issue_s(1);
+    for (int i = 0; i < nq; ++i) {  // dV += P^T dO, dK += dS^T Q (A from TMEM), then S^T(i+2)
+      const int st = i % NST, b = i & 1;
+      mbar_wait(&p_full[b], (i >> 1) & 1);
+      BTR(i, 0);
+      fence_after();
+      const uint64_t dq = desc_add(dQm, st * SM::QT), dg = desc_add(dGm, st * SM::QT);
+      if (leader) {
 #pragma unroll
         for (int kk = 0; kk < QB / 16; ++kk) {
           const uint32_t ta = 32 * (kk >> 1) + 8 * (kk & 1);   // 16 queries: owner half, 8 packed columns
           const uint32_t ob = kk * 16 * 128;                   // MN-major B: 16 query rows
           const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-          umma_f16_ts(t_dv, t_st(b) + ta, make_desc(sG + ob, SM::SUB64, 1024), idesc_g, acc);
-          umma_f16_ts(t_dk, t_dpt(b) + ta, make_desc(sQ + ob, SM::SUB64, 1024), idesc_g, acc);
+          umma_f16_ts(t_dv, t_st(b) + ta, desc_add(dg, ob), idesc_g, acc);
+          umma_f16_ts(t_dk, t_dpt(b) + ta, desc_add(dq, ob), idesc_g, acc);
         }
         umma_commit(&g_done[b]);
         umma_commit(&q_empty[st]);
-        if (i + 2 < nq) {
-          mbar_wait(&g_done[b], (i >> 1) & 1);   // P^T / dS^T of iteration i consumed: buffer b free
-          fence_after();
-          issue_s(i + 2);
-        }
+      }
+      __syncwarp();
+      if (i + 2 < nq) {
+#ifndef LGA_EXP_NO_GDONE_WAIT
+        mbar_wait(&g_done[b], (i >> 1) & 1);   // P^T / dS^T of iteration i consumed: buffer b free
+#endif
+        BTR(i, 2);
+        fence_after();
+        issue_s(i + 2);
       }
     }
   } else if (warp >= 4) {  // ===== element-wise: ping-pong groups, one key row per 2 threads of a group
@@ -264,17 +289,33 @@ __global__ void __launch_bounds__(NT, 1)
       // valid iff q < s, kj < s and (causal) kj <= q; only tiles touching the diagonal / the end mask
       const bool need_mask = kj >= s || qa + 32 > s || (a.causal && kj > qa);
       mbar_wait(&s_full[grp], (i >> 1) & 1);
+      if ((warp & 7) == 4 && lane == 0) BTR(i, 4);
       fence_after();
       mbar_wait(&q_full[st], (i / NST) & 1);   // lse / dsum of tile i landed with Q / dO
 #pragma unroll
       for (int ch = 0; ch < 2; ++ch) {
         uint32_t rsv[16], rdp[16];
+#ifdef LGA_EXP_NO_TMEM_LD
+#pragma unroll
+        for (int c = 0; c < 16; ++c) rsv[c] = __float_as_uint(0.01f * c), rdp[c] = 0;
+#else
         tmem_ld16_nowait(t_st(grp) + lrow + hf * 32 + ch * 16, rsv);
         tmem_ld16_nowait(t_dpt(grp) + lrow + hf * 32 + ch * 16, rdp);
         tmem_wait_ld();
+#endif
         float sc[16];
 #pragma unroll
         for (int c = 0; c < 16; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -ls[ch * 16 + c] * LOG2E);
+#ifdef LGA_EXP_EW_FAST
+        if (true) {
+          uint32_t pp[8], pd[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) pp[c] = __float_as_uint(sc[2 * c]) ^ rdp[2 * c], pd[c] = rdp[2 * c + 1];
+          tmem_st8_nowait(t_st(grp) + lrow + hf * 32 + ch * 8, pp);
+          tmem_st8_nowait(t_dpt(grp) + lrow + hf * 32 + ch * 8, pd);
+          continue;
+        }
+#endif
         if (need_mask) {
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
@@ -299,6 +340,7 @@ __global__ void __launch_bounds__(NT, 1)
         tmem_st8_nowait(t_dpt(grp) + lrow + hf * 32 + ch * 8, pd);
       }
       tmem_wait_st();
+      if ((warp & 7) == 4 && lane == 0) BTR(i, 5);
       fence_before();
       mbar_arrive(&p_full[grp]);
     }
@@ -315,6 +357,7 @@ __global__ void __launch_bounds__(NT, 1)
     fence_after();
     tmem_dealloc(tb, 512);
   }
+  if (threadIdx.x == 0) BTR(39, 2);
 }
 
 // =============================================================================== dQ
@@ -407,40 +450,48 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ===== MMA issuer
-      constexpr uint32_t idesc_s = make_idesc(128, KB2, false, false);
-      constexpr uint32_t idesc_q = make_idesc(128, DH, false, true);
-      const uint32_t sQ = smem_u32(smem + SM::Q_OFF), sG = smem_u32(smem + SM::G_OFF);
-      mbar_wait(qg_full, 0);
-      for (int j = 0; j < nk + 2; ++j) {
-        if (j < nk) {  // S(j), dP(j)
-          const int st = j % NST, b = j & 1;
-          mbar_wait(&kv_full[st], (j / NST) & 1);
-          mbar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);
-          fence_after();
-          const uint32_t sK = smem_u32(smem + SM::K_OFF + st * SM::KT);
-          const uint32_t sV = smem_u32(smem + SM::V_OFF + st * SM::KT);
+  } else if (warp == 1) {  // ===== MMA issuer (whole warp; one elected lane issues)
+    constexpr uint32_t idesc_s = make_idesc(128, KB2, false, false);
+    constexpr uint32_t idesc_q = make_idesc(128, DH, false, true);
+    const bool leader = elect_one();
+    const uint64_t dQ = make_desc(smem_u32(smem + SM::Q_OFF), 16, 1024);
+    const uint64_t dG = make_desc(smem_u32(smem + SM::G_OFF), 16, 1024);
+    const uint64_t dK = make_desc(smem_u32(smem + SM::K_OFF), 16, 1024);
+    const uint64_t dV = make_desc(smem_u32(smem + SM::V_OFF), 16, 1024);
+    const uint64_t dKm = make_desc(smem_u32(smem + SM::K_OFF), SM::SUB64, 1024);   // K, MN-major
+    mbar_wait(qg_full, 0);
+    for (int j = 0; j < nk + 2; ++j) {
+      if (j < nk) {  // S(j), dP(j)
+        const int st = j % NST, b = j & 1;
+        mbar_wait(&kv_full[st], (j / NST) & 1);
+        mbar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);
+        fence_after();
+        const uint64_t dk = desc_add(dK, st * SM::KT), dv = desc_add(dV, st * SM::KT);
+        if (leader) {
 #pragma unroll
           for (int kk = 0; kk < DH / 16; ++kk) {
             const uint32_t oa = (kk >> 2) * SM::SUB128 + (kk & 3) * 32, ob = (kk >> 2) * SM::SUB64 + (kk & 3) * 32;
-            umma_f16(t_s(b), make_desc(sQ + oa, 16, 1024), make_desc(sK + ob, 16, 1024), idesc_s, kk > 0);
-            umma_f16(t_dp(b), make_desc(sG + oa, 16, 1024), make_desc(sV + ob, 16, 1024), idesc_s, kk > 0);
+            umma_f16(t_s(b), desc_add(dQ, oa), desc_add(dk, ob), idesc_s, kk > 0);
+            umma_f16(t_dp(b), desc_add(dG, oa), desc_add(dv, ob), idesc_s, kk > 0);
           }
           umma_commit(&s_full[b]);
         }
-        if (j >= 2) {  // dQ += dS K of iteration j-2 (A = dS from TMEM)
-          const int jj = j - 2, st = jj % NST, pb = jj & 1;
-          mbar_wait(&p_full[pb], (jj >> 1) & 1);
-          fence_after();
-          const uint32_t sK = smem_u32(smem + SM::K_OFF + st * SM::KT);
+        __syncwarp();
+      }
+      if (j >= 2) {  // dQ += dS K of iteration j-2 (A = dS from TMEM)
+        const int jj = j - 2, st = jj % NST, pb = jj & 1;
+        mbar_wait(&p_full[pb], (jj >> 1) & 1);
+        fence_after();
+        const uint64_t dk = desc_add(dKm, st * SM::KT);
+        if (leader) {
 #pragma unroll
           for (int kk = 0; kk < KB2 / 16; ++kk)
-            umma_f16_ts(t_dq, t_ds(pb) + 16 * (kk >> 1) + 8 * (kk & 1), make_desc(sK + kk * 16 * 128, SM::SUB64, 1024),
-                        idesc_q, (jj > 0 || kk > 0) ? 1u : 0u);
+            umma_f16_ts(t_dq, t_ds(pb) + 16 * (kk >> 1) + 8 * (kk & 1), desc_add(dk, kk * 16 * 128), idesc_q,
+                        (jj > 0 || kk > 0) ? 1u : 0u);
           umma_commit(&g_done[pb]);
           umma_commit(&kv_empty[st]);
         }
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {  // ===== element-wise: ping-pong groups, one query row per 2 threads of a group
@@ -540,6 +591,12 @@ static cudaError_t run(const AttnArgs& a, cudaStream_t st) {
 }
 
 }  // namespace fatb
+
+#ifdef LGA_BWD_TRACE
+extern "C" int lgatest_bwd_trace(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, fatb::g_bwd_trace, sizeof(fatb::g_bwd_trace));
+}
+#endif
 
 cudaError_t attn_bwd_bf16(const AttnArgs& a, cudaStream_t st) {
   if (a.nseq <= 0) return cudaSuccess;

@@ -99,6 +99,17 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes
   d |= (uint64_t)2 << 61;
   return d;
 }
+// A descriptor advanced by `bytes` within the same shared buffer (start-address field = addr >> 4 never
+// carries: shared addresses stay below 2^18).  With a base from make_desc() hoisted out of the loop, each
+// MMA's operand costs one uniform add -- short MMAs (N <= 128) are otherwise issue-bound on descriptor math.
+__device__ __forceinline__ uint64_t desc_add(uint64_t desc, uint32_t bytes) { return desc + (bytes >> 4); }
+// One lane of a converged warp (elect.sync); the MMA warp runs its loops on all 32 lanes so the
+// descriptor arithmetic stays in uniform registers, and only the elected lane issues tcgen05.mma / commit.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(p));
+  return p != 0;
+}
 // Instruction descriptor, kind::f16: D fp32 (bits 4-5 = 1), A and B bf16 (bits 7-9, 10-12 = 1),
 // A / B major (bits 15 / 16: 0 = K, 1 = MN), N >> 3 (bits 17-22), M >> 4 (bits 24-28).
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn) {
