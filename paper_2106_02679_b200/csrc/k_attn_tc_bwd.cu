@@ -37,23 +37,32 @@ constexpr int NT = (4 + EW_WARPS) * 32;
 #endif
 constexpr float LOG2E = 1.4426950408889634f;
 
-// rowsum(dO * o) per (sequence, head, position); one warp per row
-__global__ void dsum_kernel(AttnArgs a) {
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);   // token*heads + h
-  const int l = threadIdx.x & 31;
-  if (row >= (int64_t)a.nseq * a.seq * a.heads) return;
-  const int h = (int)(row % a.heads);
-  const int64_t tok = row / a.heads;
-  const __nv_bfloat16* o = static_cast<const __nv_bfloat16*>(a.o) + tok * a.d + (int64_t)h * a.dh;
-  const __nv_bfloat16* g = static_cast<const __nv_bfloat16*>(a.dO) + tok * a.d + (int64_t)h * a.dh;
+// rowsum(dO * o) per (sequence, head, position): d_h / 8 lanes per row (8 or 16, 16-byte loads), shuffle
+// reduction within the lane group
+__global__ void __launch_bounds__(256) dsum_kernel(AttnArgs a) {
+  const int lph = a.dh >> 3;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gid / lph;   // token * heads + h
+  const int part = (int)(gid % lph);
+  const bool valid = row < (int64_t)a.nseq * a.seq * a.heads;
   float acc = 0.f;
-  for (int c = l * 2; c < a.dh; c += 64) {
-    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + c));
-    const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(g + c));
-    acc += x.x * y.x + x.y * y.y;
+  int h = 0;
+  int64_t tok = 0;
+  if (valid) {
+    h = (int)(row % a.heads);
+    tok = row / a.heads;
+    const int64_t off = tok * a.d + (int64_t)h * a.dh + part * 8;
+    const uint4 x = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.o) + off);
+    const uint4 y = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.dO) + off);
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      acc = fmaf(__uint_as_float(xs[i] << 16), __uint_as_float(ys[i] << 16), acc);
+      acc = fmaf(__uint_as_float(xs[i] & 0xFFFF0000u), __uint_as_float(ys[i] & 0xFFFF0000u), acc);
+    }
   }
-  acc = warp_sum(acc);
-  if (l == 0) a.dsum[((tok / a.seq) * a.heads + h) * a.seq + tok % a.seq] = acc;
+  for (int o = lph >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (valid && part == 0) a.dsum[((tok / a.seq) * a.heads + h) * a.seq + tok % a.seq] = acc;
 }
 
 // TMEM row -> bf16 global row.  tcgen05.ld is warp-collective: every lane executes it, only
@@ -565,7 +574,7 @@ __global__ void __launch_bounds__(NT, 1)
 template <int DH>
 static cudaError_t run(const AttnArgs& a, cudaStream_t st) {
   const int64_t rows = (int64_t)a.nseq * a.seq * a.heads;
-  note_launch(), dsum_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(a);
+  note_launch(), dsum_kernel<<<(unsigned)((rows * (a.dh / 8) + 255) / 256), 256, 0, st>>>(a);
   CUtensorMap kv128, q64, g64, q128, g128, kv64;
   cudaError_t e;
   const uint64_t ld = 3ull * a.d;

@@ -434,16 +434,21 @@ static void bias_grad(lga_handle* h, const void* X, DT xdt, int64_t ldx, int n, 
 // Backward of local layer j over one chunk; the layer's intermediates are in the workspace
 // (recomputed just before).  dY: fp32 [c][M][d] gradient of the layer output, read;
 // dx_out: where dX goes (in place over dY, the previous stage's buffer, or a scratch sink).
+// bf16: the GEMMs read dY as bf16 from h->dYe -- cast here unless dYe_ready (the previous layer's LN1
+// backward already wrote it next to its fp32 dX); dx_e_out: also write dX as bf16 there (or nullptr).
 static void layer_bwd(lga_handle* h, const void* W, const float* x_in, const float* dY, float* dx_out,
-                      int chunk_idx, int nchunks, int gb, cudaStream_t st) {
+                      int chunk_idx, int nchunks, int gb, cudaStream_t st, bool dYe_ready = false,
+                      void* dx_e_out = nullptr) {
   const Cfg& c = h->c;
   const int T = c.c * c.M;
   const int d = c.d, f = c.f;
   const DT E = c.E;
   const void* dYe = dY;
   if (c.bf16) {
-    cast_f32(dY, h->dYe, E, (int64_t)T * d, st);
-    KCHECK();
+    if (!dYe_ready) {
+      cast_f32(dY, h->dYe, E, (int64_t)T * d, st);
+      KCHECK();
+    }
     dYe = h->dYe;
   }
   auto dst = [&](int64_t off) { return grad_dst(h, chunk_idx, nchunks, gb, off); };
@@ -516,8 +521,8 @@ static void layer_bwd(lga_handle* h, const void* W, const float* x_in, const flo
   }
   // ---- LN1 backward + residual: dX = dh1 + LN1'(dA)
   {
-    const int nblk = ln_bwd(h->dC, x_in, h->st1, eoff((void*)W, E, c.o_ln1w), E, h->dh1, dx_out, nullptr, E, h->partial, T,
-                            d, st);
+    const int nblk = ln_bwd(h->dC, x_in, h->st1, eoff((void*)W, E, c.o_ln1w), E, h->dh1, dx_out, dx_e_out, E, h->partial,
+                            T, d, st);
     KCHECK();
     GradDst gw = dst(c.o_ln1w), gbias = dst(c.o_ln1b);
     colsum_finish(h->partial, nblk, 2LL * d, d, gw.acc_in, gw.out, gw.out_dt, st);
@@ -719,7 +724,10 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
       if (i == 0) dx = h->dscratch;
       else if (c.P == 1) dx = dYc;
       else dx = c.no_comm ? h->dscratch : h->prev_dY + m0 * mb;
-      layer_bwd(h, W, xin, dYc, dx, k, nchunks, gb, h->s_comp);
+      // one chunk on one stage: the LN1 backward also writes the bf16 dY of the next layer processed
+      const bool fuse_e = c.bf16 && c.P == 1 && nchunks == 1;
+      layer_bwd(h, W, xin, dYc, dx, k, nchunks, gb, h->s_comp, fuse_e && i < c.L - 1,
+                fuse_e && i > 0 ? h->dYe : nullptr);
       h->last.bwd_units += c.c;
       if (c.P > 1 && i > 0) {
         h->sent_bwd += c.c;

@@ -1,9 +1,6 @@
-# Round-1 evidence: launch list of one 1.3B step and a full ncu capture of the top kernel (CTA-pair GEMM).
+# Launch list of one 1.3B step (ncu, serialised, cold L2: compare shares), plus a plain bench run first.
 cd $GRAFT_REPO_ROOT
-python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/plain.log 2>&1 && \
+python bench.py --steps 5 --warmup 3 > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -s 1900 -c 1100 --csv --log-file gpurun_out/launches_r1_final.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1
-python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:gemm_tc2_kernel -s 200 -c 8 -o gpurun_out/prof_gemm2_r1 \
-    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
-tail -2 gpurun_out/ncu_full.log
+tail -1 gpurun_out/ncu_launch.log
