@@ -8,7 +8,7 @@
 // Online softmax with lazy rescaling: the running max m used for P only moves when a row max exceeds
 // it by more than 2^8, then O (in TMEM) and l are rescaled by the softmax thread that owns the row.
 // The result is the same definition (O3): o = sum_j P_j V_j / l, lse = m + log2(l) (natural log saved).
-// Warp roles: 0 TMA, 1 MMA issuer, 2 TMEM allocator, 4..7 softmax + epilogue.
+// Warp roles: 0 TMA (Q, K), 1 MMA issuer, 2 TMEM allocator, 3 TMA (V), 4..11 softmax + epilogue.
 #include "kernels.cuh"
 #include "tc_common.cuh"
 
@@ -28,17 +28,27 @@ constexpr int SM_THREADS = SM_WARPS * 32;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_THRESHOLD = 8.0f;   // log2 units
 
+#ifdef LGA_FWD_TRACE
+// Timing-only instrumentation (development builds): clock64() at pipeline events of CTA 0's first item.
+__device__ long long g_fwd_trace[40][8];
+#define FTR(j, k) \
+  if (blockIdx.x == 0 && t == 0 && (j) < 40) g_fwd_trace[j][k] = clock64()
+#else
+#define FTR(j, k)
+#endif
+
 template <int DH>
 struct FwdSmem {
   static constexpr int TILE = BQ * DH * 2;          // [128][DH] bf16 as DH/64 swizzled [128][64] sub-tiles
   static constexpr int SUB = 128 * 64 * 2;          // 16 KB
+  static constexpr int NK = 3, NV = 2;              // K ring (freed when S completes), V ring (freed after PV)
   static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = Q_OFF + TILE;        // 2 stages
-  static constexpr int V_OFF = K_OFF + 2 * TILE;    // 2 stages
-  static constexpr int P_OFF = V_OFF + 2 * TILE;    // [128][128] bf16 = 2 sub-tiles
-  static constexpr int RED_OFF = P_OFF + 2 * SUB;   // [2 halves][128 rows] maxima, then [2][128] sums
-  static constexpr int BAR_OFF = RED_OFF + 4 * 128 * 4;
+  static constexpr int K_OFF = Q_OFF + TILE;        // [NK]
+  static constexpr int V_OFF = K_OFF + NK * TILE;   // [NV]
+  static constexpr int P_OFF = V_OFF + NV * TILE;   // [128][128] bf16 = 2 sub-tiles; epilogue scratch after the last PV
+  static constexpr int BAR_OFF = P_OFF + 2 * SUB;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+  static_assert(TOTAL <= 232448, "shared memory");
 };
 
 template <int DH>
@@ -47,17 +57,21 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps shared provenance
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+  constexpr int NK = SM::NK, NV = SM::NV;
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;     // [2]
-  uint64_t* v_full = bars + 3;     // [2]
-  uint64_t* kv_empty = bars + 5;   // [2]
-  uint64_t* s_full = bars + 7;     // [2]
-  uint64_t* s_empty = bars + 9;    // [2]   (SM_THREADS arrivals)
-  uint64_t* p_full = bars + 11;    // [2 halves] (SM_THREADS/2 arrivals each)
-  uint64_t* o_done = bars + 13;    // [2 halves]
-  uint64_t* q_empty = bars + 15;   // Q buffer free (all S MMAs of an item done)
-  uint64_t* o_free = bars + 16;    // O accumulators read by the epilogue (SM_THREADS arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* k_full = q_full + 1;       // [NK]
+  uint64_t* k_empty = k_full + NK;     // [NK]
+  uint64_t* v_full = k_empty + NK;     // [NV]
+  uint64_t* v_empty = v_full + NV;     // [NV]
+  uint64_t* s_full = v_empty + NV;     // [2]
+  uint64_t* s_empty = s_full + 2;      // [2]   (SM_THREADS arrivals)
+  uint64_t* p_full = s_empty + 2;      // [2 halves] (SM_THREADS/2 arrivals each)
+  uint64_t* o_done = p_full + 2;       // [2 halves]
+  uint64_t* q_empty = o_done + 2;      // Q buffer free (all S MMAs of an item done)
+  uint64_t* o_free = q_empty + 1;      // O accumulators read by the epilogue (SM_THREADS arrivals)
+  constexpr int NBAR = 1 + 2 * NK + 2 * NV + 10;
+  static_assert(NBAR * 8 + 4 <= 256, "barrier area");
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s = a.seq, d = a.d;
@@ -65,20 +79,25 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
   const int per_q = a.heads * a.nseq;
   const int n_items = nqt * per_q;
   const int nkv_all = (s + BKV - 1) / BKV;
-  // work item t -> (query tile, head, sequence); causal: heaviest query tiles first
+  // work item t -> (query tile, head, sequence).  Items come in chunks of G (sequence, head) pairs, all
+  // query tiles of a chunk together (heaviest first under causal masking), so the CTAs running at any time
+  // share each pair's K / V tiles in L2 instead of streaming every tile from HBM once per query tile.
+  constexpr int G = 16;
   auto item = [&](int t, int& qt, int& h, int& sq, int& nkv) {
-    const int qi = t / per_q, rem = t % per_q;
+    const int chunk = t / (G * nqt), w = t % (G * nqt);
+    const int np = min(G, per_q - chunk * G);   // pairs in this chunk (the last may be partial)
+    const int qi = w / np, pair = chunk * G + w % np;
     qt = a.causal ? nqt - 1 - qi : qi;
-    h = rem % a.heads;
-    sq = rem / a.heads;
+    h = pair % a.heads;
+    sq = pair / a.heads;
     nkv = a.causal ? min(nkv_all, (qt * BQ + BQ - 1) / BKV + 1) : nkv_all;
   };
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < 17; ++i) {
+    for (int i = 0; i < NBAR; ++i) {
       uint32_t cnt = 1;
-      if (i == 9 || i == 10 || i == 16) cnt = SM_THREADS;
-      if (i == 11 || i == 12) cnt = SM_THREADS / 2;
+      if (&bars[i] == s_empty || &bars[i] == s_empty + 1 || &bars[i] == o_free) cnt = SM_THREADS;
+      if (&bars[i] == p_full || &bars[i] == p_full + 1) cnt = SM_THREADS / 2;
       mbar_init(&bars[i], cnt);   // softmax threads arrive individually
     }
     mbar_fence_init();
@@ -89,11 +108,10 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
   __syncthreads();
   fence_after();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t t_s[2] = {tbase, tbase + 128};
   const uint32_t t_o[2] = {tbase + 256, tbase + 256 + DH};   // one O accumulator per key half (DH <= 128)
 
   if (warp == 0) {
-    if (lane == 0) {  // ===== TMA producer
+    if (lane == 0) {  // ===== TMA producer: Q and K
       int jt = 0;     // global KV tile counter (ring stage / phase)
       int it = 0;
       for (int t = blockIdx.x; t < n_items; t += gridDim.x, ++it) {
@@ -105,12 +123,24 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
         for (int i = 0; i < DH / 64; ++i)
           tma_load_3d(smem + SM::Q_OFF + i * SM::SUB, &tm, q_full, h * DH + 64 * i, qt * BQ, sq);
         for (int j = 0; j < nkv; ++j, ++jt) {
-          const int st = jt & 1;
-          mbar_wait(&kv_empty[st], ((jt >> 1) & 1) ^ 1);
+          const int st = jt % NK;
+          mbar_wait(&k_empty[st], ((jt / NK) & 1) ^ 1);
           mbar_expect_tx(&k_full[st], SM::TILE);
 #pragma unroll
           for (int i = 0; i < DH / 64; ++i)
             tma_load_3d(smem + SM::K_OFF + st * SM::TILE + i * SM::SUB, &tm, &k_full[st], d + h * DH + 64 * i, j * BKV, sq);
+        }
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {  // ===== TMA producer: V
+      int jt = 0;
+      for (int t = blockIdx.x; t < n_items; t += gridDim.x) {
+        int qt, h, sq, nkv;
+        item(t, qt, h, sq, nkv);
+        for (int j = 0; j < nkv; ++j, ++jt) {
+          const int st = jt % NV;
+          mbar_wait(&v_empty[st], ((jt / NV) & 1) ^ 1);
           mbar_expect_tx(&v_full[st], SM::TILE);
 #pragma unroll
           for (int i = 0; i < DH / 64; ++i)
@@ -136,9 +166,10 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
       const int j0 = js;   // global index of this item's first tile
       for (int j = 0; j <= nkv; ++j) {
         if (j < nkv) {
-          const int g = j0 + j, st = g & 1, b = g & 1;
-          mbar_wait(&k_full[st], (g >> 1) & 1);
+          const int g = j0 + j, st = g % NK, b = g & 1;
+          mbar_wait(&k_full[st], (g / NK) & 1);
           mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
+          FTR(j, 0);
           fence_after();
           const uint64_t dk = desc_add(dK, st * SM::TILE);
           if (leader) {
@@ -148,18 +179,20 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
               umma_f16(tbase + 128 * b, desc_add(dQ, off), desc_add(dk, off), idesc_s, kk > 0);
             }
             umma_commit(&s_full[b]);
+            umma_commit(&k_empty[st]);                // K tile consumed
             if (j == nkv - 1) umma_commit(q_empty);   // Q no longer needed by this item
           }
           __syncwarp();
         }
         if (j >= 1) {
-          const int jj = j - 1, g = j0 + jj, st = g & 1;
+          const int jj = j - 1, g = j0 + jj, st = g % NV;
           if (jj == 0) mbar_wait(o_free, (it & 1) ^ 1);   // previous item's epilogue has read O
-          mbar_wait(&v_full[st], (g >> 1) & 1);
+          mbar_wait(&v_full[st], (g / NV) & 1);
           const uint64_t dv = desc_add(dVm, st * SM::TILE);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {   // O_h += P_h V_h over keys 64h .. 64h+63
             mbar_wait(&p_full[hh], g & 1);
+            FTR(jj, 1 + hh);
             fence_after();
             if (leader) {
 #pragma unroll
@@ -170,7 +203,7 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
             }
             __syncwarp();
           }
-          if (leader) umma_commit(&kv_empty[st]);
+          if (leader) umma_commit(&v_empty[st]);
           __syncwarp();
         }
       }
@@ -183,7 +216,7 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const float sl2 = a.scale * LOG2E;
     uint8_t* sP = smem + SM::P_OFF + hf * SM::SUB;   // this half's [128][64] P sub-tile
-    float* red = reinterpret_cast<float*>(smem + SM::RED_OFF);
+    float* red = reinterpret_cast<float*>(smem + SM::P_OFF);   // [2][128] maxima, [2][128] sums (after the last PV)
     int gt = 0;   // global tile counter
     for (int t = blockIdx.x; t < n_items; t += gridDim.x) {
       int qt, h, sq, nkv;
@@ -193,10 +226,11 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
       for (int j = 0; j < nkv; ++j, ++gt) {
         const int b = gt & 1;
         mbar_wait(&s_full[b], (gt >> 1) & 1);
+        if (warp == 4 && lane == 0) FTR(j, 3);
         fence_after();
         uint32_t raw[2][32];
-        tmem_ld32_nowait(t_s[b] + lane_off + hf * 64, raw[0]);
-        tmem_ld32_nowait(t_s[b] + lane_off + hf * 64 + 32, raw[1]);
+        tmem_ld32_nowait(tbase + 128 * b + lane_off + hf * 64, raw[0]);
+        tmem_ld32_nowait(tbase + 128 * b + lane_off + hf * 64 + 32, raw[1]);
         tmem_wait_ld();
         fence_before();
         mbar_arrive(&s_empty[b]);
@@ -227,10 +261,12 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
           rs += p0 + p1;
           pk[c / 2] = pack_bf16x2(p0, p1);
         }
+        if (warp == 4 && lane == 0) FTR(j, 4);
         if (j >= 1) {
           mbar_wait(&o_done[hf], (gt - 1) & 1);   // PV of the previous tile done: O_h stable, P_h buffer free
           fence_after();
         }
+        if (warp == 4 && lane == 0) FTR(j, 5);
         // lazy rescale of this half's accumulator row.  tcgen05.ld / st are warp-collective, so the whole
         // warp enters when any lane needs it; lanes that do not rescale multiply by 1.
         const bool resc = m_new != m_used && m_used != -INFINITY;
@@ -239,10 +275,10 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
 #pragma unroll 1
           for (int c = 0; c < DH / 32; ++c) {
             float tt[32];
-            tmem_ld32(t_o[hf] + lane_off + c * 32, tt);
+            tmem_ld32(tbase + 256 + DH * hf + lane_off + c * 32, tt);
 #pragma unroll
             for (int i = 0; i < 32; ++i) tt[i] *= scale;
-            tmem_st32(t_o[hf] + lane_off + c * 32, tt);
+            tmem_st32(tbase + 256 + DH * hf + lane_off + c * 32, tt);
           }
         }
         l = l * scale + rs;
@@ -256,9 +292,14 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
         }
         fence_proxy_async();
         fence_before();
+        if (warp == 4 && lane == 0) FTR(j, 6);
+        if (warp == 8 && lane == 0) FTR(j, 7);
         mbar_arrive(&p_full[hf]);
       }
       // epilogue: combine the halves, o = (2^(m0-m) O_0 + 2^(m1-m) O_1) / (2^(m0-m) l_0 + 2^(m1-m) l_1)
+      mbar_wait(&o_done[0], (gt - 1) & 1);   // every PV of the item done: O final, P buffer free for `red`
+      mbar_wait(&o_done[1], (gt - 1) & 1);
+      fence_after();
       red[hf * 128 + r] = m_used;
       red[256 + hf * 128 + r] = l;
       asm volatile("bar.sync 1, %0;" ::"n"(SM_THREADS) : "memory");
@@ -270,9 +311,6 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
       const float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - mm), f1 = m1 == -INFINITY ? 0.f : ex2(m1 - mm);
       const float lt = f0 * l0 + f1 * l1;
       const float inv = lt > 0.f ? 1.f / lt : 0.f;
-      mbar_wait(&o_done[0], (gt - 1) & 1);
-      mbar_wait(&o_done[1], (gt - 1) & 1);
-      fence_after();
       __nv_bfloat16* og = static_cast<__nv_bfloat16*>(a.o) + ((int64_t)sq * s + q) * d + h * DH;
 #pragma unroll 1
       for (int c = hf * (DH / 64); c < (hf + 1) * (DH / 64); ++c) {   // this thread's half of the O columns
@@ -320,6 +358,12 @@ static cudaError_t run_fwd(const AttnArgs& a, cudaStream_t st) {
 }
 
 }  // namespace fat
+
+#ifdef LGA_FWD_TRACE
+extern "C" int lgatest_fwd_trace(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, fat::g_fwd_trace, sizeof(fat::g_fwd_trace));
+}
+#endif
 
 cudaError_t attn_fwd_bf16(const AttnArgs& a, cudaStream_t st) {
   if (a.nseq <= 0) return cudaSuccess;
