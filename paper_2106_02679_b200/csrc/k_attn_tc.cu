@@ -2,12 +2,15 @@
 //
 // One CTA = 128 query rows of one (sequence, head).  Per 128-key tile j:
 //   S_j = Q K_j^T        tcgen05.mma (M=128, N=128, K=d_h), fp32 in TMEM (two S buffers)
-//   P_j = exp2(S_j*scale*log2e - m)   by 4 softmax warps, one query row (TMEM lane) per thread,
-//                        written as bf16 into shared memory in the UMMA K-major SW128 layout
-//   O  += P_j V_j        tcgen05.mma (M=128, N=d_h, K=128), V read MN-major from the same tile TMA loaded
+//   P_j = exp2(S_j*scale*log2e - m)   by 8 softmax warps, one query row (TMEM lane) and one key half per
+//                        thread, written as bf16 into TMEM over S_j
+//   O  += P_j V_j        tcgen05.mma (M=128, N=d_h, K=128; A = P from TMEM), V read MN-major from the tile
+//                        TMA loaded
 // Online softmax with lazy rescaling: the running max m used for P only moves when a row max exceeds
 // it by more than 2^8, then O (in TMEM) and l are rescaled by the softmax thread that owns the row.
 // The result is the same definition (O3): o = sum_j P_j V_j / l, lse = m + log2(l) (natural log saved).
+// P never touches shared memory: the softmax thread writes it (bf16) into TMEM over the S columns it has
+// just read, and the PV MMA takes its A operand from TMEM.
 // Warp roles: 0 TMA (Q, K), 1 MMA issuer, 2 TMEM allocator, 3 TMA (V), 4..11 softmax + epilogue.
 #include "kernels.cuh"
 #include "tc_common.cuh"
@@ -45,8 +48,8 @@ struct FwdSmem {
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = Q_OFF + TILE;        // [NK]
   static constexpr int V_OFF = K_OFF + NK * TILE;   // [NV]
-  static constexpr int P_OFF = V_OFF + NV * TILE;   // [128][128] bf16 = 2 sub-tiles; epilogue scratch after the last PV
-  static constexpr int BAR_OFF = P_OFF + 2 * SUB;
+  static constexpr int RED_OFF = V_OFF + NV * TILE; // [2 halves][128 rows] maxima, then [2][128] sums
+  static constexpr int BAR_OFF = RED_OFF + 4 * 128 * 4;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
   static_assert(TOTAL <= 232448, "shared memory");
 };
@@ -64,12 +67,15 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
   uint64_t* v_full = k_empty + NK;     // [NV]
   uint64_t* v_empty = v_full + NV;     // [NV]
   uint64_t* s_full = v_empty + NV;     // [2]
-  uint64_t* s_empty = s_full + 2;      // [2]   (SM_THREADS arrivals)
-  uint64_t* p_full = s_empty + 2;      // [2 halves] (SM_THREADS/2 arrivals each)
-  uint64_t* o_done = p_full + 2;       // [2 halves]
+  uint64_t* p_full = s_full + 2;       // [2 buffers][2 halves] (SM_THREADS/2 arrivals each).  Per buffer: P(g+2)
+                                       // needs S(g+2), issued after PV(g), so a half can never be two phases
+                                       // ahead of the MMA warp's wait (one barrier per half could: S(g+1) is
+                                       // issued before P(g) is awaited)
+  uint64_t* o_done = p_full + 4;       // [2 halves]
   uint64_t* q_empty = o_done + 2;      // Q buffer free (all S MMAs of an item done)
   uint64_t* o_free = q_empty + 1;      // O accumulators read by the epilogue (SM_THREADS arrivals)
-  constexpr int NBAR = 1 + 2 * NK + 2 * NV + 10;
+  uint64_t* p_free = o_free + 1;       // [2] per S / P TMEM buffer: PV of the tile in it done
+  constexpr int NBAR = 1 + 2 * NK + 2 * NV + 12;
   static_assert(NBAR * 8 + 4 <= 256, "barrier area");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
@@ -96,8 +102,8 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < NBAR; ++i) {
       uint32_t cnt = 1;
-      if (&bars[i] == s_empty || &bars[i] == s_empty + 1 || &bars[i] == o_free) cnt = SM_THREADS;
-      if (&bars[i] == p_full || &bars[i] == p_full + 1) cnt = SM_THREADS / 2;
+      if (&bars[i] == o_free) cnt = SM_THREADS;
+      if (&bars[i] >= p_full && &bars[i] < p_full + 4) cnt = SM_THREADS / 2;
       mbar_init(&bars[i], cnt);   // softmax threads arrive individually
     }
     mbar_fence_init();
@@ -155,7 +161,6 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
     const bool leader = elect_one();
     const uint64_t dQ = make_desc(smem_u32(smem + SM::Q_OFF), 16, 1024);
     const uint64_t dK = make_desc(smem_u32(smem + SM::K_OFF), 16, 1024);
-    const uint64_t dP = make_desc(smem_u32(smem + SM::P_OFF), 16, 1024);
     const uint64_t dVm = make_desc(smem_u32(smem + SM::V_OFF), SM::SUB, 1024);   // MN-major: d_h blocks at 16 KB
     int js = 0;   // global S / KV tile counter
     int it = 0;
@@ -168,7 +173,7 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
         if (j < nkv) {
           const int g = j0 + j, st = g % NK, b = g & 1;
           mbar_wait(&k_full[st], (g / NK) & 1);
-          mbar_wait(&s_empty[b], ((g >> 1) & 1) ^ 1);
+          if (g >= 2) mbar_wait(&p_free[b], ((g - 2) >> 1) & 1);   // buffer b holds P(g-2) until PV(g-2) read it
           FTR(j, 0);
           fence_after();
           const uint64_t dk = desc_add(dK, st * SM::TILE);
@@ -185,25 +190,28 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
           __syncwarp();
         }
         if (j >= 1) {
-          const int jj = j - 1, g = j0 + jj, st = g % NV;
+          const int jj = j - 1, g = j0 + jj, st = g % NV, pb = g & 1;
           if (jj == 0) mbar_wait(o_free, (it & 1) ^ 1);   // previous item's epilogue has read O
           mbar_wait(&v_full[st], (g / NV) & 1);
           const uint64_t dv = desc_add(dVm, st * SM::TILE);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {   // O_h += P_h V_h over keys 64h .. 64h+63
-            mbar_wait(&p_full[hh], g & 1);
+            mbar_wait(&p_full[pb * 2 + hh], (g >> 1) & 1);
             FTR(jj, 1 + hh);
             fence_after();
             if (leader) {
 #pragma unroll
-              for (int kk = 4 * hh; kk < 4 * hh + 4; ++kk)
-                umma_f16(t_o[hh], desc_add(dP, hh * SM::SUB + (kk & 3) * 32), desc_add(dv, kk * 16 * 128), idesc_o,
-                         (jj > 0 || kk > 4 * hh) ? 1u : 0u);
+              for (int kk = 4 * hh; kk < 4 * hh + 4; ++kk)   // A = P_h from TMEM: 16 keys = 8 packed columns
+                umma_f16_ts(t_o[hh], tbase + 128 * pb + 64 * hh + 8 * (kk & 3), desc_add(dv, kk * 16 * 128), idesc_o,
+                            (jj > 0 || kk > 4 * hh) ? 1u : 0u);
               umma_commit(&o_done[hh]);
             }
             __syncwarp();
           }
-          if (leader) umma_commit(&v_empty[st]);
+          if (leader) {
+            umma_commit(&v_empty[st]);
+            umma_commit(&p_free[pb]);
+          }
           __syncwarp();
         }
       }
@@ -215,8 +223,7 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
     const int r = qd * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const float sl2 = a.scale * LOG2E;
-    uint8_t* sP = smem + SM::P_OFF + hf * SM::SUB;   // this half's [128][64] P sub-tile
-    float* red = reinterpret_cast<float*>(smem + SM::P_OFF);   // [2][128] maxima, [2][128] sums (after the last PV)
+    float* red = reinterpret_cast<float*>(smem + SM::RED_OFF);
     int gt = 0;   // global tile counter
     for (int t = blockIdx.x; t < n_items; t += gridDim.x) {
       int qt, h, sq, nkv;
@@ -232,8 +239,6 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
         tmem_ld32_nowait(tbase + 128 * b + lane_off + hf * 64, raw[0]);
         tmem_ld32_nowait(tbase + 128 * b + lane_off + hf * 64 + 32, raw[1]);
         tmem_wait_ld();
-        fence_before();
-        mbar_arrive(&s_empty[b]);
         const int k0 = j * BKV + hf * 64;
         // masking only where a key can be past the sequence end or after the query (uniform per warp)
         const bool need_mask = (k0 + 64 > s) || (a.causal && k0 + 63 > q0 + qd * 32);
@@ -246,55 +251,51 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
           for (int c = 0; c < 64; ++c)
             if (c > lim) sv[c] = -INFINITY;
         }
-        float mx = -INFINITY;
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // 4 independent chains
 #pragma unroll
-        for (int c = 0; c < 64; ++c) mx = fmaxf(mx, sv[c]);
+        for (int c = 0; c < 64; ++c) m4[c & 3] = fmaxf(m4[c & 3], sv[c]);
+        float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
         mx *= sl2;
         const float m_new = (mx > m_used + RESCALE_THRESHOLD) ? mx : m_used;
         const float moff = m_new == -INFINITY ? 0.f : -m_new;   // fully masked so far: every p is 2^-inf = 0
-        float rs = 0.f;
+        float r4[4] = {0.f, 0.f, 0.f, 0.f};
         uint32_t pk[32];
 #pragma unroll
         for (int c = 0; c < 64; c += 2) {
           const float p0 = ex2(fmaf(sv[c], sl2, moff));
           const float p1 = ex2(fmaf(sv[c + 1], sl2, moff));
-          rs += p0 + p1;
+          r4[(c >> 1) & 3] += p0 + p1;
           pk[c / 2] = pack_bf16x2(p0, p1);
         }
+        const float rs = (r4[0] + r4[1]) + (r4[2] + r4[3]);
         if (warp == 4 && lane == 0) FTR(j, 4);
-        if (j >= 1) {
-          mbar_wait(&o_done[hf], (gt - 1) & 1);   // PV of the previous tile done: O_h stable, P_h buffer free
-          fence_after();
-        }
-        if (warp == 4 && lane == 0) FTR(j, 5);
-        // lazy rescale of this half's accumulator row.  tcgen05.ld / st are warp-collective, so the whole
-        // warp enters when any lane needs it; lanes that do not rescale multiply by 1.
+        // lazy rescale of this half's accumulator row, once PV(j-1) has finished accumulating into it (the
+        // parity wait is safe at any time: s_full(j) implies PV(j-2) complete).  tcgen05.ld / st are
+        // warp-collective, so the whole warp enters when any lane needs it; other lanes multiply by 1.
         const bool resc = m_new != m_used && m_used != -INFINITY;
         const float scale = resc ? ex2(m_used - m_new) : 1.f;
         if (__any_sync(0xffffffffu, resc)) {
+          mbar_wait(&o_done[hf], (gt - 1) & 1);
+          fence_after();
 #pragma unroll 1
           for (int c = 0; c < DH / 32; ++c) {
             float tt[32];
-            tmem_ld32(tbase + 256 + DH * hf + lane_off + c * 32, tt);
+            tmem_ld32(t_o[hf] + lane_off + c * 32, tt);
 #pragma unroll
             for (int i = 0; i < 32; ++i) tt[i] *= scale;
-            tmem_st32(tbase + 256 + DH * hf + lane_off + c * 32, tt);
+            tmem_st32(t_o[hf] + lane_off + c * 32, tt);
           }
         }
+        if (warp == 4 && lane == 0) FTR(j, 5);
         l = l * scale + rs;
         m_used = m_new;
-#pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          const uint32_t addr = smem_u32(sP) + sw128(r, ch);
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[ch * 4]), "r"(pk[ch * 4 + 1]),
-                       "r"(pk[ch * 4 + 2]), "r"(pk[ch * 4 + 3])
-                       : "memory");
-        }
-        fence_proxy_async();
+        // P (bf16, two keys per column) over the first 32 of this thread's own 64 S columns
+        tmem_st32_u(tbase + 128 * b + lane_off + hf * 64, pk);
+        tmem_wait_st();
         fence_before();
         if (warp == 4 && lane == 0) FTR(j, 6);
         if (warp == 8 && lane == 0) FTR(j, 7);
-        mbar_arrive(&p_full[hf]);
+        mbar_arrive(&p_full[b * 2 + hf]);
       }
       // epilogue: combine the halves, o = (2^(m0-m) O_0 + 2^(m1-m) O_1) / (2^(m0-m) l_0 + 2^(m1-m) l_1)
       mbar_wait(&o_done[0], (gt - 1) & 1);   // every PV of the item done: O final, P buffer free for `red`

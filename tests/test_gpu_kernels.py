@@ -131,8 +131,7 @@ def _attn_ref(qkv, nseq, s, H, dh, causal):
                                                   (1, 128, 200, 1, 1), (2, 128, 200, 1, 1), (2, 64, 300, 0, 1),
                                                   (1, 64, 300, 0, 1), (1, 128, 512, 0, 1), (1, 64, 1024, 1, 1),
                                                   (1, 128, 1024, 1, 6), (1, 64, 700, 0, 6), (0, 32, 300, 1, 6)])
-def test_attention_fwd_bwd(path, dh, s, causal, mag):
-    nseq, H = 2, 3
+def test_attention_fwd_bwd(path, dh, s, causal, mag, nseq=2, H=3):
     d = H * dh
     dt = torch.float32 if path == 0 else torch.bfloat16
     g = torch.Generator(device="cuda").manual_seed(3)
@@ -163,3 +162,10 @@ def test_attention_fwd_bwd(path, dh, s, causal, mag):
     got = dqkv.float().view(nseq * s, 3, d)
     for i, r in enumerate((gq, gk, gv)):
         assert relerr(got[:, i], pack(r)) < (1e-5 if path == 0 else 2e-2), i
+
+
+@pytest.mark.parametrize("dh,s,causal,mag", [(128, 512, 1, 1), (64, 512, 1, 6), (128, 384, 0, 1)])
+def test_attention_many_items_per_cta(dh, s, causal, mag):
+    """Persistent forward with ~7 work items per CTA and short key loops: item transitions back to back
+    (a barrier that can run two phases ahead of its waiter deadlocks only here)."""
+    test_attention_fwd_bwd(1, dh, s, causal, mag, nseq=16, H=16)
