@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <mutex>
+#include <type_traits>
 
 namespace lga {
 namespace fat {
@@ -30,6 +31,10 @@ constexpr int NT = (4 + SM_WARPS) * 32;
 constexpr int SM_THREADS = SM_WARPS * 32;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_THRESHOLD = 8.0f;   // log2 units
+#ifndef LGA_POLY_PAIRS
+#define LGA_POLY_PAIRS 3
+#endif
+constexpr int POLY_PAIRS = LGA_POLY_PAIRS;  // of every 8 exponent pairs, computed by polynomial (FMA pipe)
 
 #ifdef LGA_FWD_TRACE
 // Timing-only instrumentation (development builds): clock64() at pipeline events of CTA 0's first item.
@@ -258,16 +263,33 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
         mx *= sl2;
         const float m_new = (mx > m_used + RESCALE_THRESHOLD) ? mx : m_used;
         const float moff = m_new == -INFINITY ? 0.f : -m_new;   // fully masked so far: every p is 2^-inf = 0
-        float r4[4] = {0.f, 0.f, 0.f, 0.f};
         uint32_t pk[32];
+        uint64_t r2[2] = {0, 0};   // packed partial row sums
+        const uint64_t SL2 = f2pack(sl2, sl2), MO = f2pack(moff, moff);
+        // p = 2^(s*scale*log2e - m): on the SFU, except (unmasked tiles) POLY_PAIRS of every 8 pairs on the
+        // FMA pipe -- the SFU alone takes 8 cycles per warp instruction and bounds the tile otherwise
+        auto exps = [&](auto poly_on) {
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) {
-          const float p0 = ex2(fmaf(sv[c], sl2, moff));
-          const float p1 = ex2(fmaf(sv[c + 1], sl2, moff));
-          r4[(c >> 1) & 3] += p0 + p1;
-          pk[c / 2] = pack_bf16x2(p0, p1);
-        }
-        const float rs = (r4[0] + r4[1]) + (r4[2] + r4[3]);
+          for (int pi = 0; pi < 32; ++pi) {
+            const uint64_t x = f2fma(f2pack(sv[2 * pi], sv[2 * pi + 1]), SL2, MO);
+            float p0, p1;
+            if (decltype(poly_on)::value && (pi & 7) < POLY_PAIRS) {
+              ex2_poly2(x, p0, p1);
+            } else {
+              float x0, x1;
+              f2unpack(x, x0, x1);
+              p0 = ex2(x0), p1 = ex2(x1);
+            }
+            r2[pi & 1] = f2add(r2[pi & 1], f2pack(p0, p1));
+            pk[pi] = pack_bf16x2(p0, p1);
+          }
+        };
+        if (need_mask) exps(std::false_type{});   // masked scores are -inf: the SFU gives exactly 0
+        else exps(std::true_type{});
+        float ra, rb, rc, rd;
+        f2unpack(r2[0], ra, rb);
+        f2unpack(r2[1], rc, rd);
+        const float rs = (ra + rb) + (rc + rd);
         if (warp == 4 && lane == 0) FTR(j, 4);
         // lazy rescale of this half's accumulator row, once PV(j-1) has finished accumulating into it (the
         // parity wait is safe at any time: s_full(j) implies PV(j-2) complete).  tcgen05.ld / st are

@@ -238,6 +238,51 @@ __device__ __forceinline__ void tmem_st8_nowait(uint32_t taddr, const uint32_t (
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// ---- packed fp32 pairs (FFMA2 / FADD2 on sm_100)
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// 2^x for a pair on the FMA pipe (offloads the SFU, which bounds the softmax): Cody-Waite split
+// x = j + f by the 1.5*2^23 rounding constant (j = round(x), f in [-0.5, 0.5]), 2^f by a degree-3
+// polynomial fitted on relative error (max 3.0e-4, below the bf16 resolution of P), 2^j added into the
+// exponent field.  x is clamped at -127 (2^-127 ~ 6e-39 instead of 0: only for unmasked scores).
+__device__ __forceinline__ void ex2_poly2(uint64_t x2, float& p0, float& p1) {
+  float x0, x1;
+  f2unpack(x2, x0, x1);
+  x2 = f2pack(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
+  const uint64_t MAGIC = f2pack(12582912.f, 12582912.f);
+  const uint64_t t = f2add(x2, MAGIC);
+  const uint64_t f = f2sub(x2, f2sub(t, MAGIC));
+  uint64_t p = f2fma(f, f2pack(0.0529366061f, 0.0529366061f), f2pack(0.2416405529f, 0.2416405529f));
+  p = f2fma(p, f, f2pack(0.6935356259f, 0.6935356259f));
+  p = f2fma(p, f, f2pack(1.f, 1.f));
+  float q0, q1, t0, t1;
+  f2unpack(p, q0, q1);
+  f2unpack(t, t0, t1);
+  p0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
+  p1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
+}
+
 // 2^x on the SFU, flush-to-zero (one MUFU.EX2; 2^-inf = +0).  Softmax probabilities below 2^-126 are
 // flushed, which is below bf16 resolution of the row sum anyway.
 __device__ __forceinline__ float ex2(float x) {
