@@ -16,6 +16,7 @@
  *   the neighbouring layer's compute on side streams (mixed buffering).  With
  *   P > 1, layer i lives on pipeline stage i mod P (modular pipeline) and
  *   activations / their gradients cross stages after every layer.
+ *   LGA_FLAG_* select the memory-rich variants and the contiguous pipeline map.
  *
  * Rank grid: world = D * P ranks, one process per GPU.  stage = rank mod P,
  * replica = rank div P.  Replica r owns global micro-batches r*N ... r*N+N-1 and shard r
@@ -46,7 +47,7 @@
 extern "C" {
 #endif
 
-#define LGA_ABI_VERSION 1u
+#define LGA_ABI_VERSION 2u
 #define LGA_NCCL_ID_BYTES 128
 
 typedef enum {
@@ -79,6 +80,20 @@ typedef enum { LGA_LAYERED = 0, LGA_STANDARD = 1 } lga_schedule;
 #define LGA_FLAG_NO_GRAPH  0x2u  /* reserved */
 #define LGA_FLAG_PROFILE   0x4u  /* record CUDA events around every GEMM / attention / AdamW launch
                                     (on the stream it is launched on) for lga_timing_last */
+/* Memory-rich variants and the contiguous pipeline (N3).  All require
+ * LGA_LAYERED (INVALID_ARG otherwise); results are the same gradient / update up to rounding. */
+#define LGA_FLAG_KEEP_PARAMS   0x8u   /* N2a: keep each layer's forward all-gather until its backward
+                                         (L/P gathered layers resident): 1 all-gather + 1 reduce-scatter
+                                         per layer per step instead of 2 + 1 (reading A-6 relaxed) */
+#define LGA_FLAG_NO_RECOMPUTE  0x10u  /* N2c: keep every layer's intermediates for all N micro-batches
+                                         (about 28 d B per token per layer) and skip the backward's
+                                         forward recompute; recompute_units = 0 */
+#define LGA_FLAG_UNPARTITIONED 0x20u  /* N2b: no training-state partition: every replica holds the full
+                                         fp32 master / m / v of its stage's layers and all-reduces each
+                                         layer's gradient once per step; no all-gather */
+#define LGA_FLAG_CONTIGUOUS_PP 0x40u  /* N3: contiguous pipeline map, layer i on stage i / (L/P) (the
+                                         standard layout of P:71) instead of the modular i mod P;
+                                         activations cross stages only at block boundaries */
 
 typedef struct {
   uint32_t abi_version;    /* must be LGA_ABI_VERSION */
@@ -103,12 +118,16 @@ typedef struct {
 
 /* Exact per-rank integers (closed forms: DESIGN.md "Counters"; P:67, P:565, P:576, P:583,
  * P:598).  all-gather bytes = bytes this rank RECEIVES; reduce-scatter bytes = bytes it
- * SENDS; *_units count logical (micro-batch, layer) pairs regardless of `chunk`. */
+ * SENDS; *_units count logical (micro-batch, layer) pairs regardless of `chunk`.
+ * allreduce_calls counts the per-step loss all-reduce plus (LGA_FLAG_UNPARTITIONED) one
+ * gradient all-reduce per layer; allreduce_bytes = bytes a rank SENDS in the gradient
+ * all-reduces (ring: 2 (D-1)/D of the padded layer), the 8-byte loss excluded. */
 typedef struct {
   uint64_t steps;
   uint64_t ag_calls, rs_calls, p2p_send_calls, p2p_recv_calls, allreduce_calls;
   uint64_t ag_bytes, rs_bytes, p2p_send_bytes, p2p_recv_bytes;
   uint64_t fwd_units, bwd_units, recompute_units;
+  uint64_t allreduce_bytes;
 } lga_comm_stats;
 
 /* Device-measured timing of the last step (CUDA events on the library's streams). */
@@ -153,7 +172,8 @@ lga_status lga_nccl_unique_id(uint8_t* out);
  *                DESIGN.md "Canonical parameter layout"; each rank keeps only its stage's
  *                layers and its shard); NULL = on-device seeded init ("train" recipe,
  *                DESIGN.md "Inputs") from `seed`.
- * Errors: INVALID_ARG (d % heads, L % pp, world != dp*pp, N < pp, schedule/pp, chunk),
+ * Errors: INVALID_ARG (d % heads, L % pp, world != dp*pp, N < pp, schedule/pp, chunk,
+ *         a variant flag with LGA_STANDARD),
  *         UNSUPPORTED (bf16 with d % 64 != 0 or head size not 64/128; ffn_mult != 4),
  *         OUT_OF_MEMORY, CUDA, NCCL. */
 lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t device,
@@ -185,7 +205,8 @@ lga_status lga_params(lga_handle* h, float* out, uint64_t n, int32_t out_on_devi
 /* Counters for the last step and the running total (either may be NULL).  Host only. */
 lga_status lga_comm_bytes(const lga_handle* h, lga_comm_stats* last_step, lga_comm_stats* total);
 
-/* stage_of_layer[i] = i mod P for i < L; n must equal L. */
+/* stage_of_layer[i] = i mod P for i < L (modular), or i / (L/P) with
+ * LGA_FLAG_CONTIGUOUS_PP; n must equal L. */
 lga_status lga_layer_stage(const lga_handle* h, int32_t* stage_of_layer, int32_t n);
 
 /* Device timing of the last step (synchronises the step's completion event). */

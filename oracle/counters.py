@@ -17,6 +17,13 @@ Definitions (readings A-5, A-7, A-10, A-11):
   every layer in forward and their gradients in backward.
 * Bubble: (n_l - 1)/n_mu for a contiguous pipeline, divided by d_l/n_l for the
   modular one.
+* Variants: keeping the forward's gathered parameters until the
+  backward removes the second all-gather; without a partition there is no all-gather and
+  the gradient is all-reduced ("the gradient reduction (scatter-reduce + all-gather)",
+  P:565) -- both then move exactly the non-partitioned volume 8 (n_b - 1) p / n_gpu of
+  P:565; no recompute drops the recompute units; the contiguous pipeline ("the first
+  instance gets the first n_l layers" layout of P:71, the standard one) crosses stages only
+  at the P - 1 block boundaries.
 
 Byte counts are per rank per step: all-gather counts the bytes a rank RECEIVES,
 reduce-scatter the bytes it SENDS (ring algorithms send and receive the same
@@ -50,34 +57,47 @@ class StepShape:
     ffn_mult: int = 4
 
 
-def stage_of_layer(i: int, pp: int) -> int:
-    """Modular pipeline map, 0-indexed: layer i lives on stage i mod P."""
+def stage_of_layer(i: int, pp: int, layers: int | None = None, pipeline: str = "modular") -> int:
+    """Pipeline map, 0-indexed: modular, layer i on stage i mod P; contiguous, layer i on
+    stage i // (L/P)  (blocks of L/P consecutive layers, the standard layout of P:71)."""
+    if pipeline == "contiguous":
+        return i // (layers // pp)
     return i % pp
 
 
-def local_layers(stage: int, layers: int, pp: int) -> list[int]:
-    return [i for i in range(layers) if stage_of_layer(i, pp) == stage]
+def local_layers(stage: int, layers: int, pp: int, pipeline: str = "modular") -> list[int]:
+    return [i for i in range(layers) if stage_of_layer(i, pp, layers, pipeline) == stage]
 
 
 def comm_counters(sh: StepShape, stage: int = 0, schedule: str = "layered",
-                  param_bytes: int = 2, grad_bytes: int = 2, act_bytes: int = 4) -> dict:
+                  param_bytes: int = 2, grad_bytes: int = 2, act_bytes: int = 4,
+                  keep_params: bool = False, unpartitioned: bool = False, no_recompute: bool = False,
+                  pipeline: str = "modular") -> dict:
     """O8: exact integer counters for one step on one rank of the given pipeline stage."""
     L_loc = sh.layers // sh.pp
-    S_l = padded_layer_params(sh.d, sh.dp, sh.ffn_mult) // sh.dp
+    P_pad = padded_layer_params(sh.d, sh.dp, sh.ffn_mult)
+    S_l = P_pad // sh.dp
     k = 1 if schedule == "layered" else sh.n_micro
     out = dict(ag_calls=0, rs_calls=0, ag_bytes=0, rs_bytes=0,
                p2p_send_calls=0, p2p_recv_calls=0, p2p_send_bytes=0, p2p_recv_bytes=0,
-               allreduce_calls=1,
+               allreduce_calls=1, allreduce_bytes=0,
                fwd_units=sh.n_micro * L_loc, bwd_units=sh.n_micro * L_loc,
-               recompute_units=sh.n_micro * L_loc)
-    if sh.dp > 1:
-        out["ag_calls"] = 2 * L_loc * k
+               recompute_units=0 if no_recompute else sh.n_micro * L_loc)
+    if sh.dp > 1 and unpartitioned:
+        # one ring all-reduce of the padded layer gradient per layer per step: a rank sends
+        # 2 (D-1)/D of it (scatter-reduce + all-gather, P:565)
+        out["allreduce_calls"] += L_loc * k
+        out["allreduce_bytes"] = L_loc * k * 2 * (sh.dp - 1) * S_l * grad_bytes
+    elif sh.dp > 1:
+        out["ag_calls"] = (1 if keep_params else 2) * L_loc * k
         out["rs_calls"] = L_loc * k
         out["ag_bytes"] = out["ag_calls"] * (sh.dp - 1) * S_l * param_bytes
         out["rs_bytes"] = out["rs_calls"] * (sh.dp - 1) * S_l * grad_bytes
     if sh.pp > 1:
-        mine = local_layers(stage, sh.layers, sh.pp)
-        crossings = sum(1 for i in mine if i < sh.layers - 1) + sum(1 for i in mine if i > 0)
+        st = lambda i: stage_of_layer(i, sh.pp, sh.layers, pipeline)
+        mine = local_layers(stage, sh.layers, sh.pp, pipeline)
+        crossings = (sum(1 for i in mine if i < sh.layers - 1 and st(i + 1) != stage)
+                     + sum(1 for i in mine if i > 0 and st(i - 1) != stage))
         calls = sh.n_micro * crossings
         msg = sh.micro_batch * sh.seq * sh.d * act_bytes
         out.update(p2p_send_calls=calls, p2p_recv_calls=calls,

@@ -13,13 +13,17 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liblga.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 NCCL_ID_BYTES = 128
 
 LGA_FP32, LGA_BF16 = 0, 1
 LGA_LAYERED, LGA_STANDARD = 0, 1
 LGA_FLAG_NO_COMM = 0x1
 LGA_FLAG_PROFILE = 0x4
+LGA_FLAG_KEEP_PARAMS = 0x8       # N2a: 1 all-gather per layer per step
+LGA_FLAG_NO_RECOMPUTE = 0x10     # N2c: keep intermediates, no forward recompute
+LGA_FLAG_UNPARTITIONED = 0x20    # N2b: full state per replica, one all-reduce per layer
+LGA_FLAG_CONTIGUOUS_PP = 0x40    # N3: layer i on stage i // (L/P)
 
 STATUS = {0: "LGA_OK", 1: "LGA_ERR_INVALID_ARG", 2: "LGA_ERR_UNSUPPORTED", 3: "LGA_ERR_OUT_OF_MEMORY",
           4: "LGA_ERR_CUDA", 5: "LGA_ERR_NCCL", 6: "LGA_ERR_SIZE_MISMATCH", 7: "LGA_ERR_BAD_STATE"}
@@ -43,7 +47,8 @@ class lga_config(C.Structure):
 class lga_comm_stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "steps", "ag_calls", "rs_calls", "p2p_send_calls", "p2p_recv_calls", "allreduce_calls",
-        "ag_bytes", "rs_bytes", "p2p_send_bytes", "p2p_recv_bytes", "fwd_units", "bwd_units", "recompute_units")]
+        "ag_bytes", "rs_bytes", "p2p_send_bytes", "p2p_recv_bytes", "fwd_units", "bwd_units", "recompute_units",
+        "allreduce_bytes")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

@@ -70,6 +70,7 @@ struct Cfg {
   DT E, G;      // compute storage type; reduce-scatter / gradient staging type
   float lr, b1, b2, eps, wd, ln_eps;
   bool retain, no_comm, profile;
+  bool keep, norecomp, unpart, contig;   // LGA_FLAG_KEEP_PARAMS / NO_RECOMPUTE / UNPARTITIONED / CONTIGUOUS_PP
   // canonical offsets
   int64_t o_ln1w, o_ln1b, o_wqkv, o_bqkv, o_wo, o_bo, o_ln2w, o_ln2b, o_w1, o_b1, o_w2, o_b2;
 };
@@ -99,6 +100,9 @@ static lga_status validate(const lga_config* c, int world, Cfg* out) {
       !(c->ln_eps > 0.f))
     return ERR(LGA_ERR_INVALID_ARG, "bad optimizer / LayerNorm hyper-parameter");
   if ((int64_t)c->micro_batch * c->seq_len * c->n_micro > (int64_t)1 << 30) return ERR(LGA_ERR_UNSUPPORTED, "batch too large");
+  const uint32_t variants = LGA_FLAG_KEEP_PARAMS | LGA_FLAG_NO_RECOMPUTE | LGA_FLAG_UNPARTITIONED | LGA_FLAG_CONTIGUOUS_PP;
+  if ((c->flags & variants) && c->schedule != LGA_LAYERED)
+    return ERR(LGA_ERR_INVALID_ARG, "variant flags 0x%x require LGA_LAYERED", c->flags & variants);
 
   Cfg g{};
   g.L = c->layers; g.d = c->d_model; g.H = c->heads; g.dh = dh; g.s = c->seq_len; g.b = c->micro_batch;
@@ -110,7 +114,11 @@ static lga_status validate(const lga_config* c, int world, Cfg* out) {
   g.pl = 12LL * g.d * g.d + 13LL * g.d;
   const int64_t q = 64LL * g.D;
   g.plpad = (g.pl + q - 1) / q * q;
-  g.S = g.plpad / g.D;
+  g.unpart = (c->flags & LGA_FLAG_UNPARTITIONED) != 0;
+  g.S = g.unpart ? g.plpad : g.plpad / g.D;   // state elements per layer on this rank
+  g.keep = (c->flags & LGA_FLAG_KEEP_PARAMS) != 0;
+  g.norecomp = (c->flags & LGA_FLAG_NO_RECOMPUTE) != 0;
+  g.contig = (c->flags & LGA_FLAG_CONTIGUOUS_PP) != 0;
   g.bf16 = c->precision == LGA_BF16;
   g.layered = c->schedule == LGA_LAYERED;
   g.causal = c->causal != 0;
@@ -151,6 +159,13 @@ struct PeerInfo {
 };
 static_assert(sizeof(PeerInfo) % 16 == 0, "PeerInfo size");
 
+// Forward intermediates of a chunk that the backward reads (pointers at the chunk's first token).
+struct Ws {
+  void *a = nullptr, *qkv = nullptr, *o = nullptr, *cn = nullptr, *u = nullptr, *g = nullptr;
+  float *h1 = nullptr, *lse = nullptr;
+  float2 *st1 = nullptr, *st2 = nullptr;
+};
+
 }  // namespace lga
 
 using namespace lga;
@@ -165,7 +180,7 @@ struct lga_handle {
   // training state, per local layer j: [Lloc][S]
   float *master = nullptr, *mom = nullptr, *var = nullptr, *gkeep = nullptr, *gshard_acc = nullptr;
   void* pshard = nullptr;
-  void* slot[2] = {nullptr, nullptr};
+  std::vector<void*> slot;   // gathered full layers: 2 (mixed buffering) or L/P (LGA_FLAG_KEEP_PARAMS)
   float* gacc = nullptr;
   void* gstage[2] = {nullptr, nullptr};
   // activations
@@ -173,11 +188,12 @@ struct lga_handle {
   float* yout = nullptr;  // [N][M][d] on the stage owning layer L-1
   float* dY = nullptr;    // [N][M][d]
   float* dscratch = nullptr;  // [c][M][d] sink for dX of layer 0
-  // chunk workspace
-  void *a = nullptr, *qkv = nullptr, *o = nullptr, *cn = nullptr, *u = nullptr, *g = nullptr, *dYe = nullptr,
-       *dh1e = nullptr, *dO = nullptr, *dqkv = nullptr;
-  float *h1 = nullptr, *dC = nullptr, *dh1 = nullptr, *lse = nullptr, *dsum = nullptr, *partial = nullptr;
-  float2 *st1 = nullptr, *st2 = nullptr;
+  // forward intermediates the backward reads: one chunk-sized set, or (LGA_FLAG_NO_RECOMPUTE) one set
+  // per local layer covering all N micro-batches
+  std::vector<Ws> ws;
+  // backward temporaries (chunk-sized)
+  void *dYe = nullptr, *dh1e = nullptr, *dO = nullptr, *dqkv = nullptr;
+  float *dC = nullptr, *dh1 = nullptr, *dsum = nullptr, *partial = nullptr;
   double *mse_partial = nullptr, *loss_dev = nullptr, *loss_host = nullptr;
   float *xin = nullptr, *tin = nullptr;  // device copies for lga_step_host
   unsigned long long* flags = nullptr;   // [0] fwd receive count, [1] bwd receive count
@@ -189,7 +205,8 @@ struct lga_handle {
   unsigned long long sent_fwd = 0, sent_bwd = 0, recv_fwd = 0, recv_bwd = 0;
   int64_t partial_floats = 0;
   // events
-  cudaEvent_t ev_in = nullptr, ev_ag[2] = {}, ev_slot_free[2] = {}, ev_grad[2] = {}, ev_adam[2] = {}, ev_comm_end = nullptr,
+  std::vector<cudaEvent_t> ev_ag, ev_slot_free;   // per slot
+  cudaEvent_t ev_in = nullptr, ev_grad[2] = {}, ev_adam[2] = {}, ev_comm_end = nullptr,
               ev_comp_end = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_fwd_end = nullptr;
   std::vector<cudaEvent_t> ev_wait0, ev_wait1;   // stall accounting pairs (s_comp)
   std::vector<int> wait_kind;
@@ -206,8 +223,13 @@ struct lga_handle {
 
 namespace lga {
 
-static int64_t local_to_global(const lga_handle* h, int j) { return (int64_t)h->stage + (int64_t)j * h->c.P; }
-static bool owns_last(const lga_handle* h) { return (h->c.L - 1) % h->c.P == h->stage; }
+// pipeline map: modular, layer i on stage i mod P; contiguous, stage i / (L/P)
+static int stage_of(const Cfg& c, int64_t i) { return c.contig ? (int)(i / c.Lloc) : (int)(i % c.P); }
+static int local_index(const Cfg& c, int64_t i) { return c.contig ? (int)(i % c.Lloc) : (int)(i / c.P); }
+static int64_t local_to_global(const lga_handle* h, int j) {
+  return h->c.contig ? (int64_t)h->stage * h->c.Lloc + j : (int64_t)h->stage + (int64_t)j * h->c.P;
+}
+static bool owns_last(const lga_handle* h) { return stage_of(h->c, h->c.L - 1) == h->stage; }
 static ncclDataType_t nccl_dt(DT t) { return t == DT::F32 ? ncclFloat32 : ncclBfloat16; }
 
 static char* eoff(void* p, DT t, int64_t i) { return static_cast<char*>(p) + i * (int64_t)dt_size(t); }
@@ -224,10 +246,9 @@ static void plan_arena(lga_handle* h) {
   h->pshard = A.take_bytes(Ll * S * e);
   h->gkeep = c.retain ? A.take<float>(Ll * S) : nullptr;
   h->gshard_acc = c.layered ? nullptr : A.take<float>(Ll * S);
-  if (c.D > 1) {
-    h->slot[0] = A.take_bytes(c.plpad * e);
-    h->slot[1] = A.take_bytes(c.plpad * e);
-  }
+  const int nslots = (c.D > 1 && !c.unpart) ? (c.keep ? (int)Ll : 2) : 0;
+  h->slot.assign(nslots, nullptr);
+  for (int k = 0; k < nslots; ++k) h->slot[k] = A.take_bytes(c.plpad * e);
   h->gacc = A.take<float>(c.plpad);
   h->gstage[0] = A.take_bytes(c.plpad * dt_size(c.G));
   h->gstage[1] = A.take_bytes(c.plpad * dt_size(c.G));
@@ -236,23 +257,28 @@ static void plan_arena(lga_handle* h) {
   h->yout = A.take<float>(act);
   h->dY = A.take<float>(act);
   h->dscratch = A.take<float>(T * d);
-  h->a = A.take_bytes(T * d * e);
-  h->qkv = A.take_bytes(T * 3 * d * e);
-  h->o = A.take_bytes(T * d * e);
-  h->cn = A.take_bytes(T * d * e);
-  h->u = A.take_bytes(T * f * e);
-  h->g = A.take_bytes(T * f * e);
+  const int nws = c.norecomp ? (int)Ll : 1;
+  const int64_t Tw = c.norecomp ? (int64_t)c.N * c.M : T;   // tokens per workspace set
+  h->ws.assign(nws, Ws{});
+  for (Ws& w : h->ws) {
+    w.a = A.take_bytes(Tw * d * e);
+    w.qkv = A.take_bytes(Tw * 3 * d * e);
+    w.o = A.take_bytes(Tw * d * e);
+    w.cn = A.take_bytes(Tw * d * e);
+    w.u = A.take_bytes(Tw * f * e);
+    w.g = A.take_bytes(Tw * f * e);
+    w.h1 = A.take<float>(Tw * d);
+    w.lse = A.take<float>(Tw / c.s * c.H * c.s);
+    w.st1 = A.take<float2>(Tw);
+    w.st2 = A.take<float2>(Tw);
+  }
   h->dYe = A.take_bytes(T * d * e);
   h->dh1e = A.take_bytes(T * d * e);
   h->dO = A.take_bytes(T * d * e);
   h->dqkv = A.take_bytes(T * 3 * d * e);
-  h->h1 = A.take<float>(T * d);
   h->dC = A.take<float>(T * d);
   h->dh1 = A.take<float>(T * d);
-  h->lse = A.take<float>((int64_t)c.c * c.b * c.H * c.s);
   h->dsum = A.take<float>((int64_t)c.c * c.b * c.H * c.s);
-  h->st1 = A.take<float2>(T);
-  h->st2 = A.take<float2>(T);
   const int64_t pcol = (int64_t)colsum_blocks((int)T) * f;
   const int64_t pln = (int64_t)ln_bwd_blocks((int)T) * 2 * d;
   h->partial_floats = std::max(pcol, pln);
@@ -346,20 +372,20 @@ static void trace(lga_handle* h, const char* what, int64_t layer) {
 // ------------------------------------------------------------------ layer executor
 // Forward of local layer j over micro-batches [m0, m0+c) (module docstring of kernels.cuh).
 // x_in: [c][M][d] fp32; y_out: fp32 destination or nullptr (recompute: FFN2 not needed).
-static void layer_fwd(lga_handle* h, const void* W, const float* x_in, float* y_out, cudaStream_t st) {
+static void layer_fwd(lga_handle* h, const Ws& w, const void* W, const float* x_in, float* y_out, cudaStream_t st) {
   const Cfg& c = h->c;
   const int T = c.c * c.M;
   const int d = c.d;
   const DT E = c.E;
-  ln_fwd(x_in, eoff((void*)W, E, c.o_ln1w), eoff((void*)W, E, c.o_ln1b), E, h->a, E, h->st1, T, d, c.ln_eps, st);
+  ln_fwd(x_in, eoff((void*)W, E, c.o_ln1w), eoff((void*)W, E, c.o_ln1b), E, w.a, E, w.st1, T, d, c.ln_eps, st);
   KCHECK();
   {  // qkv = a Wqkv + bqkv
     GemmArgs g;
     g.M = T; g.N = 3 * d; g.K = d;
-    g.A = h->a; g.lda = d; g.a_kmajor = true;
+    g.A = w.a; g.lda = d; g.a_kmajor = true;
     g.B = eoff((void*)W, E, c.o_wqkv); g.ldb = 3 * d; g.b_kmajor = false;
     g.epi.kind = EPI_STORE; g.epi.bias = eoff((void*)W, E, c.o_bqkv); g.epi.bias_dt = E;
-    g.epi.out = h->qkv; g.epi.ldo = 3 * d; g.epi.out_dt = E;
+    g.epi.out = w.qkv; g.epi.ldo = 3 * d; g.epi.out_dt = E;
     gemm(h, g, st);
     trace(h, "  qkv gemm", -1);
   }
@@ -367,7 +393,7 @@ static void layer_fwd(lga_handle* h, const void* W, const float* x_in, float* y_
     AttnArgs a;
     a.nseq = c.c * c.b; a.seq = c.s; a.heads = c.H; a.dh = c.dh; a.d = d; a.causal = c.causal;
     a.scale = 1.0f / sqrtf((float)c.dh);
-    a.qkv = h->qkv; a.o = h->o; a.lse = h->lse;
+    a.qkv = w.qkv; a.o = w.o; a.lse = w.lse;
     const int p = prof_begin(h, st);
     if (c.bf16) CK(attn_fwd_bf16(a, st)); else attn_fwd_f32(a, st);
     KCHECK();
@@ -377,34 +403,34 @@ static void layer_fwd(lga_handle* h, const void* W, const float* x_in, float* y_
   {  // h1 = x + o Wo + bo
     GemmArgs g;
     g.M = T; g.N = d; g.K = d;
-    g.A = h->o; g.lda = d; g.a_kmajor = true;
+    g.A = w.o; g.lda = d; g.a_kmajor = true;
     g.B = eoff((void*)W, E, c.o_wo); g.ldb = d; g.b_kmajor = false;
     g.epi.kind = EPI_STORE; g.epi.bias = eoff((void*)W, E, c.o_bo); g.epi.bias_dt = E;
     g.epi.res = x_in; g.epi.ldr = d;
-    g.epi.out = h->h1; g.epi.ldo = d; g.epi.out_dt = DT::F32;
+    g.epi.out = w.h1; g.epi.ldo = d; g.epi.out_dt = DT::F32;
     gemm(h, g, st);
     trace(h, "  oproj gemm", -1);
   }
-  ln_fwd(h->h1, eoff((void*)W, E, c.o_ln2w), eoff((void*)W, E, c.o_ln2b), E, h->cn, E, h->st2, T, d, c.ln_eps, st);
+  ln_fwd(w.h1, eoff((void*)W, E, c.o_ln2w), eoff((void*)W, E, c.o_ln2b), E, w.cn, E, w.st2, T, d, c.ln_eps, st);
   KCHECK();
   {  // u = c W1 + b1 ; g = GELU(u)
     GemmArgs g;
     g.M = T; g.N = c.f; g.K = d;
-    g.A = h->cn; g.lda = d; g.a_kmajor = true;
+    g.A = w.cn; g.lda = d; g.a_kmajor = true;
     g.B = eoff((void*)W, E, c.o_w1); g.ldb = c.f; g.b_kmajor = false;
     g.epi.kind = EPI_GELU_FWD; g.epi.bias = eoff((void*)W, E, c.o_b1); g.epi.bias_dt = E;
-    g.epi.aux = h->u; g.epi.ldaux = c.f; g.epi.aux_dt = E;
-    g.epi.out = h->g; g.epi.ldo = c.f; g.epi.out_dt = E;
+    g.epi.aux = w.u; g.epi.ldaux = c.f; g.epi.aux_dt = E;
+    g.epi.out = w.g; g.epi.ldo = c.f; g.epi.out_dt = E;
     gemm(h, g, st);
     trace(h, "  ffn1 gemm", -1);
   }
   if (y_out) {  // y = h1 + g W2 + b2
     GemmArgs g;
     g.M = T; g.N = d; g.K = c.f;
-    g.A = h->g; g.lda = c.f; g.a_kmajor = true;
+    g.A = w.g; g.lda = c.f; g.a_kmajor = true;
     g.B = eoff((void*)W, E, c.o_w2); g.ldb = d; g.b_kmajor = false;
     g.epi.kind = EPI_STORE; g.epi.bias = eoff((void*)W, E, c.o_b2); g.epi.bias_dt = E;
-    g.epi.res = h->h1; g.epi.ldr = d;
+    g.epi.res = w.h1; g.epi.ldr = d;
     g.epi.out = y_out; g.epi.ldo = d; g.epi.out_dt = DT::F32;
     gemm(h, g, st);
     trace(h, "  ffn2 gemm", -1);
@@ -436,7 +462,7 @@ static void bias_grad(lga_handle* h, const void* X, DT xdt, int64_t ldx, int n, 
 // dx_out: where dX goes (in place over dY, the previous stage's buffer, or a scratch sink).
 // bf16: the GEMMs read dY as bf16 from h->dYe -- cast here unless dYe_ready (the previous layer's LN1
 // backward already wrote it next to its fp32 dX); dx_e_out: also write dX as bf16 there (or nullptr).
-static void layer_bwd(lga_handle* h, const void* W, const float* x_in, const float* dY, float* dx_out,
+static void layer_bwd(lga_handle* h, const Ws& w, const void* W, const float* x_in, const float* dY, float* dx_out,
                       int chunk_idx, int nchunks, int gb, cudaStream_t st, bool dYe_ready = false,
                       void* dx_e_out = nullptr) {
   const Cfg& c = h->c;
@@ -453,20 +479,20 @@ static void layer_bwd(lga_handle* h, const void* W, const float* x_in, const flo
   }
   auto dst = [&](int64_t off) { return grad_dst(h, chunk_idx, nchunks, gb, off); };
   // ---- FFN2: y = h1 + g W2 + b2
-  wgrad(h, h->g, f, dYe, d, f, d, T, dst(c.o_w2), c.o_w2, st);
+  wgrad(h, w.g, f, dYe, d, f, d, T, dst(c.o_w2), c.o_w2, st);
   bias_grad(h, dY, DT::F32, d, d, T, dst(c.o_b2), st);
   {  // dU = (dY W2^T) * GELU'(u), written over u
     GemmArgs g;
     g.M = T; g.N = f; g.K = d;
     g.A = dYe; g.lda = d; g.a_kmajor = true;
     g.B = eoff((void*)W, E, c.o_w2); g.ldb = d; g.b_kmajor = true;
-    g.epi.kind = EPI_GELU_BWD; g.epi.aux = h->u; g.epi.ldaux = f; g.epi.aux_dt = E;
-    g.epi.out = h->u; g.epi.ldo = f; g.epi.out_dt = E;
+    g.epi.kind = EPI_GELU_BWD; g.epi.aux = w.u; g.epi.ldaux = f; g.epi.aux_dt = E;
+    g.epi.out = w.u; g.epi.ldo = f; g.epi.out_dt = E;
     gemm(h, g, st);
   }
-  void* dU = h->u;
+  void* dU = w.u;
   // ---- FFN1: u = c W1 + b1
-  wgrad(h, h->cn, d, dU, f, d, f, T, dst(c.o_w1), c.o_w1, st);
+  wgrad(h, w.cn, d, dU, f, d, f, T, dst(c.o_w1), c.o_w1, st);
   bias_grad(h, dU, E, f, f, T, dst(c.o_b1), st);
   {  // dC = dU W1^T
     GemmArgs g;
@@ -478,7 +504,7 @@ static void layer_bwd(lga_handle* h, const void* W, const float* x_in, const flo
   }
   // ---- LN2 backward + residual: dh1 = dY + LN2'(dC)
   {
-    const int nblk = ln_bwd(h->dC, h->h1, h->st2, eoff((void*)W, E, c.o_ln2w), E, dY, h->dh1, c.bf16 ? h->dh1e : nullptr, E,
+    const int nblk = ln_bwd(h->dC, w.h1, w.st2, eoff((void*)W, E, c.o_ln2w), E, dY, h->dh1, c.bf16 ? h->dh1e : nullptr, E,
                             h->partial, T, d, st);
     KCHECK();
     GradDst gw = dst(c.o_ln2w), gbias = dst(c.o_ln2b);
@@ -488,7 +514,7 @@ static void layer_bwd(lga_handle* h, const void* W, const float* x_in, const flo
   }
   const void* dh1e = c.bf16 ? (const void*)h->dh1e : (const void*)h->dh1;
   // ---- O projection: h1 = x + o Wo + bo
-  wgrad(h, h->o, d, dh1e, d, d, d, T, dst(c.o_wo), c.o_wo, st);
+  wgrad(h, w.o, d, dh1e, d, d, d, T, dst(c.o_wo), c.o_wo, st);
   bias_grad(h, h->dh1, DT::F32, d, d, T, dst(c.o_bo), st);
   {  // dO = dh1 Wo^T
     GemmArgs g;
@@ -502,14 +528,14 @@ static void layer_bwd(lga_handle* h, const void* W, const float* x_in, const flo
     AttnArgs a;
     a.nseq = c.c * c.b; a.seq = c.s; a.heads = c.H; a.dh = c.dh; a.d = d; a.causal = c.causal;
     a.scale = 1.0f / sqrtf((float)c.dh);
-    a.qkv = h->qkv; a.o = h->o; a.lse = h->lse; a.dO = h->dO; a.dsum = h->dsum; a.dqkv = h->dqkv;
+    a.qkv = w.qkv; a.o = w.o; a.lse = w.lse; a.dO = h->dO; a.dsum = h->dsum; a.dqkv = h->dqkv;
     const int p = prof_begin(h, st);
     if (c.bf16) CK(attn_bwd_bf16(a, st)); else attn_bwd_f32(a, st);
     KCHECK();
     prof_end(h, p, st, FAM_ATTN, 2.0 * attn_flops_fwd(c, a.nseq));
   }
   // ---- QKV: qkv = a Wqkv + bqkv
-  wgrad(h, h->a, d, h->dqkv, 3 * d, d, 3 * d, T, dst(c.o_wqkv), c.o_wqkv, st);
+  wgrad(h, w.a, d, h->dqkv, 3 * d, d, 3 * d, T, dst(c.o_wqkv), c.o_wqkv, st);
   bias_grad(h, h->dqkv, E, 3 * d, 3 * d, T, dst(c.o_bqkv), st);
   {  // dA = dqkv Wqkv^T  (into dC, free now)
     GemmArgs g;
@@ -521,7 +547,7 @@ static void layer_bwd(lga_handle* h, const void* W, const float* x_in, const flo
   }
   // ---- LN1 backward + residual: dX = dh1 + LN1'(dA)
   {
-    const int nblk = ln_bwd(h->dC, x_in, h->st1, eoff((void*)W, E, c.o_ln1w), E, h->dh1, dx_out, dx_e_out, E, h->partial,
+    const int nblk = ln_bwd(h->dC, x_in, w.st1, eoff((void*)W, E, c.o_ln1w), E, h->dh1, dx_out, dx_e_out, E, h->partial,
                             T, d, st);
     KCHECK();
     GradDst gw = dst(c.o_ln1w), gbias = dst(c.o_ln1b);
@@ -553,13 +579,13 @@ static void count_wait_end(lga_handle* h) {
 }
 
 static const void* layer_weights(lga_handle* h, int j, int slot) {
-  if (h->c.D > 1) return h->slot[slot];
-  return eoff(h->pshard, h->c.E, (int64_t)j * h->c.S);
+  if (!h->slot.empty()) return h->slot[slot];
+  return eoff(h->pshard, h->c.E, (int64_t)j * h->c.S);   // D == 1 or unpartitioned: the local full layer
 }
 
 static void all_gather(lga_handle* h, int j, int slot) {
   const Cfg& c = h->c;
-  if (c.D <= 1) return;
+  if (h->slot.empty()) return;
   h->last.ag_calls++;
   h->last.ag_bytes += (uint64_t)(c.D - 1) * c.S * dt_size(c.E);
   if (c.no_comm) return;
@@ -580,10 +606,20 @@ static void adam_layer(lga_handle* h, int j, const void* g, DT gdt) {
   prof_end(h, p, h->s_comm, FAM_ADAM, per * (double)c.S);
 }
 
-// reduce-scatter of the staged gradient in place (once per layer per step); returns the shard
+// reduce-scatter of the staged gradient in place (once per layer per step); returns the shard.
+// Unpartitioned (N2b): all-reduce of the whole layer in place instead (scatter-reduce + all-gather,
+// P:565), every replica then updates the full layer.
 static void* reduce_scatter(lga_handle* h, int gb) {
   const Cfg& c = h->c;
   void* gs = h->gstage[gb];
+  if (c.unpart) {
+    if (c.D > 1) {
+      h->last.allreduce_calls++;
+      h->last.allreduce_bytes += 2ull * (c.D - 1) * (uint64_t)(c.plpad / c.D) * dt_size(c.G);
+      if (!c.no_comm) NK(ncclAllReduce(gs, gs, (size_t)c.plpad, nccl_dt(c.G), ncclSum, h->dp_comm, h->s_comm));
+    }
+    return gs;
+  }
   void* shard_g = eoff(gs, c.G, (int64_t)h->replica * c.S);
   if (c.D > 1) {
     h->last.rs_calls++;
@@ -600,40 +636,68 @@ static float* ckpt_ptr(lga_handle* h, int j, int m) {
 }
 static float* act_ptr(float* base, const Cfg& c, int m) { return base + (int64_t)m * c.M * c.d; }
 
+// forward intermediates of local layer j, micro-batches [m0, m0 + c): the shared chunk set, or (no
+// recompute) layer j's own set at token m0*M
+static Ws chunk_ws(lga_handle* h, int j, int m0) {
+  const Cfg& c = h->c;
+  if (!c.norecomp) return h->ws[0];
+  const Ws& b = h->ws[j];
+  const int64_t t = (int64_t)m0 * c.M, d = c.d, f = c.f;
+  const size_t e = dt_size(c.E);
+  Ws w;
+  w.a = static_cast<char*>(b.a) + t * d * e;
+  w.qkv = static_cast<char*>(b.qkv) + t * 3 * d * e;
+  w.o = static_cast<char*>(b.o) + t * d * e;
+  w.cn = static_cast<char*>(b.cn) + t * d * e;
+  w.u = static_cast<char*>(b.u) + t * f * e;
+  w.g = static_cast<char*>(b.g) + t * f * e;
+  w.h1 = b.h1 + t * d;
+  w.lse = b.lse + (int64_t)m0 * c.b * c.H * c.s;
+  w.st1 = b.st1 + t;
+  w.st2 = b.st2 + t;
+  return w;
+}
+
 // ------------------------------------------------------------------ the step (LAYERED, any D, any P)
+// Parameter slots: with mixed buffering (2 slots) the gather of layer j goes to slot agk % 2, agk counting
+// gathers over the step; with LGA_FLAG_KEEP_PARAMS layer j has slot j, filled once in the forward.
 static void step_layered(lga_handle* h, const float* x, const float* T) {
   const Cfg& c = h->c;
   const int nchunks = c.N / c.c;
-  const bool last_stage = owns_last(h);
   const int64_t mb = (int64_t)c.M * c.d;
-  int agk = 0;  // running all-gather index: slot = agk % 2
+  const bool dp_gather = !h->slot.empty();
+  auto slot_of = [&](int j, int agk) { return c.keep ? j : agk % 2; };
+  int agk = 0;  // running all-gather index
   // ---------------- forward: layer-major over all micro-batches
-  if (c.D > 1) {
-    CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[0], 0));
-    all_gather(h, 0, 0);
-    CK(cudaEventRecord(h->ev_ag[0], h->s_comm));
+  if (dp_gather) {
+    CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[slot_of(0, 0)], 0));
+    all_gather(h, 0, slot_of(0, 0));
+    CK(cudaEventRecord(h->ev_ag[slot_of(0, 0)], h->s_comm));
   }
   for (int j = 0; j < c.Lloc; ++j, ++agk) {
-    const int sl = agk % 2;
+    const int sl = slot_of(j, agk);
     const int64_t i = local_to_global(h, j);
-    if (c.D > 1 && j + 1 < c.Lloc) {  // prefetch Restore(i+P) while computing layer i
-      CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[(agk + 1) % 2], 0));
-      all_gather(h, j + 1, (agk + 1) % 2);
-      CK(cudaEventRecord(h->ev_ag[(agk + 1) % 2], h->s_comm));
+    if (dp_gather && j + 1 < c.Lloc) {  // prefetch Restore(next local layer) while computing layer i
+      const int sn = slot_of(j + 1, agk + 1);
+      CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[sn], 0));
+      all_gather(h, j + 1, sn);
+      CK(cudaEventRecord(h->ev_ag[sn], h->s_comm));
     }
-    if (c.D > 1) {
+    if (dp_gather) {
       count_wait(h, h->ev_ag[sl], 0);
       count_wait_end(h);
     }
     const void* W = layer_weights(h, j, sl);
+    const bool recv = c.P > 1 && i > 0 && stage_of(c, i - 1) != h->stage;        // x_i from another stage
+    const bool send = c.P > 1 && i < c.L - 1 && stage_of(c, i + 1) != h->stage;  // x_{i+1} to another stage
     for (int k = 0; k < nchunks; ++k) {
       const int m0 = k * c.c;
       const float* xin;
       if (i == 0) {
-        xin = x + m0 * mb;
+        xin = x + m0 * mb;   // layer 0 input is the caller's x (no copy)
       } else {
         xin = ckpt_ptr(h, j, m0);
-        if (c.P > 1) {  // pipeline receive: x_i[m0..m0+c) from stage (i-1) mod P
+        if (recv) {  // pipeline receive: x_i[m0..m0+c) written by the previous stage
           h->recv_fwd += c.c;
           h->last.p2p_recv_calls += c.c;
           h->last.p2p_recv_bytes += (uint64_t)c.c * mb * 4;
@@ -645,21 +709,18 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
           }
         }
       }
-      if (i == 0 && c.P == 1) {
-        // layer 0 input is the caller's x; keep a checkpoint pointer to it (no copy)
-      }
       float* yo;
       if (i == c.L - 1) {
         yo = act_ptr(h->yout, c, m0);
-      } else if (c.P == 1) {
+      } else if (!send) {
         yo = ckpt_ptr(h, j + 1, m0);
       } else {  // write x_{i+1} straight into the next stage's checkpoint buffer (fused p2p)
-        const int jn = (int)((i + 1) / c.P);
+        const int jn = local_index(c, i + 1);
         yo = c.no_comm ? h->dscratch : h->next_ckpt + ((int64_t)jn * c.N + m0) * mb;
       }
-      layer_fwd(h, W, xin, yo, h->s_comp);
+      layer_fwd(h, chunk_ws(h, j, m0), W, xin, yo, h->s_comp);
       h->last.fwd_units += c.c;
-      if (c.P > 1 && i < c.L - 1) {
+      if (send) {
         h->sent_fwd += c.c;
         h->last.p2p_send_calls += c.c;
         h->last.p2p_send_bytes += (uint64_t)c.c * mb * 4;
@@ -678,36 +739,42 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
         KCHECK();
       }
     }
-    CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
+    if (!c.keep) CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
     trace(h, "fwd", i);
   }
   CK(cudaEventRecord(h->ev_fwd_end, h->s_comp));
-  // ---------------- backward: layer-major, recompute + backward over all micro-batches
-  if (c.D > 1) {
+  // ---------------- backward: layer-major, (recompute +) backward over all micro-batches
+  if (dp_gather && !c.keep) {
     CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[agk % 2], 0));
     all_gather(h, c.Lloc - 1, agk % 2);
     CK(cudaEventRecord(h->ev_ag[agk % 2], h->s_comm));
   }
   for (int j = c.Lloc - 1; j >= 0; --j, ++agk) {
-    const int sl = agk % 2;
+    const int sl = slot_of(j, agk);
     const int64_t i = local_to_global(h, j);
     const int gb = j % 2;
-    if (c.D > 1 && j - 1 >= 0) {
+    if (dp_gather && !c.keep && j - 1 >= 0) {
       CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[(agk + 1) % 2], 0));
       all_gather(h, j - 1, (agk + 1) % 2);
       CK(cudaEventRecord(h->ev_ag[(agk + 1) % 2], h->s_comm));
     }
-    if (c.D > 1) {
+    if (dp_gather && !c.keep) {
       count_wait(h, h->ev_ag[sl], 0);
       count_wait_end(h);
     }
     CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));   // staging buffer gb free again
     const void* W = layer_weights(h, j, sl);
+    const bool recv = c.P > 1 && i < c.L - 1 && stage_of(c, i + 1) != h->stage;   // dY_i from another stage
+    const bool send = c.P > 1 && i > 0 && stage_of(c, i - 1) != h->stage;         // dX_i to another stage
+    // one chunk, and the next layer processed here is i-1: its bf16 dY comes out of this LN1 backward
+    const bool fuse_e = c.bf16 && nchunks == 1;
+    const bool dye_ready = fuse_e && i < c.L - 1 && !recv;
+    void* dx_e = (fuse_e && i > 0 && !send) ? h->dYe : nullptr;
     for (int k = 0; k < nchunks; ++k) {
       const int m0 = k * c.c;
       const float* xin = (i == 0) ? x + m0 * mb : ckpt_ptr(h, j, m0);
       float* dYc = act_ptr(h->dY, c, m0);
-      if (c.P > 1 && i < c.L - 1) {  // receive dY_i[m0..) from stage (i+1) mod P
+      if (recv) {  // receive dY_i[m0..) from the next stage
         h->recv_bwd += c.c;
         h->last.p2p_recv_calls += c.c;
         h->last.p2p_recv_bytes += (uint64_t)c.c * mb * 4;
@@ -718,18 +785,18 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
           count_wait_end(h);
         }
       }
-      layer_fwd(h, W, xin, nullptr, h->s_comp);   // recompute
-      h->last.recompute_units += c.c;
+      const Ws w = chunk_ws(h, j, m0);
+      if (!c.norecomp) {
+        layer_fwd(h, w, W, xin, nullptr, h->s_comp);   // recompute
+        h->last.recompute_units += c.c;
+      }
       float* dx;
       if (i == 0) dx = h->dscratch;
-      else if (c.P == 1) dx = dYc;
+      else if (!send) dx = dYc;
       else dx = c.no_comm ? h->dscratch : h->prev_dY + m0 * mb;
-      // one chunk on one stage: the LN1 backward also writes the bf16 dY of the next layer processed
-      const bool fuse_e = c.bf16 && c.P == 1 && nchunks == 1;
-      layer_bwd(h, W, xin, dYc, dx, k, nchunks, gb, h->s_comp, fuse_e && i < c.L - 1,
-                fuse_e && i > 0 ? h->dYe : nullptr);
+      layer_bwd(h, w, W, xin, dYc, dx, k, nchunks, gb, h->s_comp, dye_ready, dx_e);
       h->last.bwd_units += c.c;
-      if (c.P > 1 && i > 0) {
+      if (send) {
         h->sent_bwd += c.c;
         h->last.p2p_send_calls += c.c;
         h->last.p2p_send_bytes += (uint64_t)c.c * mb * 4;
@@ -747,7 +814,6 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
     adam_layer(h, j, shard_g, c.G);
     CK(cudaEventRecord(h->ev_adam[gb], h->s_comm));
   }
-  (void)last_stage;
 }
 
 // ------------------------------------------------------------------ STANDARD (comparison, P = 1)
@@ -769,7 +835,7 @@ static void step_standard(lga_handle* h, const float* x, const float* T) {
       }
       const float* xin = j == 0 ? x + m * mb : ckpt_ptr(h, j, m);
       float* yo = j == c.L - 1 ? act_ptr(h->yout, c, m) : ckpt_ptr(h, j + 1, m);
-      layer_fwd(h, layer_weights(h, j, sl), xin, yo, h->s_comp);
+      layer_fwd(h, h->ws[0], layer_weights(h, j, sl), xin, yo, h->s_comp);
       h->last.fwd_units++;
       CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
     }
@@ -791,9 +857,9 @@ static void step_standard(lga_handle* h, const float* x, const float* T) {
       const void* W = layer_weights(h, j, sl);
       const float* xin = j == 0 ? x + m * mb : ckpt_ptr(h, j, m);
       float* dYc = act_ptr(h->dY, c, m);
-      layer_fwd(h, W, xin, nullptr, h->s_comp);
+      layer_fwd(h, h->ws[0], W, xin, nullptr, h->s_comp);
       h->last.recompute_units++;
-      layer_bwd(h, W, xin, dYc, j == 0 ? h->dscratch : dYc, 0, 1, gb, h->s_comp);
+      layer_bwd(h, h->ws[0], W, xin, dYc, j == 0 ? h->dscratch : dYc, 0, 1, gb, h->s_comp);
       h->last.bwd_units++;
       CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
       CK(cudaEventRecord(h->ev_grad[gb], h->s_comp));
@@ -875,10 +941,13 @@ static void free_handle(lga_handle* h) {
   if (h->peer_prev_base && h->peer_prev_base != h->peer_next_base) cudaIpcCloseMemHandle(h->peer_prev_base);
   if (h->dp_comm) ncclCommDestroy(h->dp_comm);
   if (h->world_comm) ncclCommDestroy(h->world_comm);
-  cudaEvent_t evs[] = {h->ev_in, h->ev_ag[0], h->ev_ag[1], h->ev_slot_free[0], h->ev_slot_free[1], h->ev_grad[0],
-                       h->ev_grad[1], h->ev_adam[0], h->ev_adam[1], h->ev_comm_end, h->ev_comp_end, h->ev_t0, h->ev_t1,
-                       h->ev_fwd_end};
+  cudaEvent_t evs[] = {h->ev_in, h->ev_grad[0], h->ev_grad[1], h->ev_adam[0], h->ev_adam[1], h->ev_comm_end,
+                       h->ev_comp_end, h->ev_t0, h->ev_t1, h->ev_fwd_end};
   for (auto e : evs)
+    if (e) cudaEventDestroy(e);
+  for (auto e : h->ev_ag)
+    if (e) cudaEventDestroy(e);
+  for (auto e : h->ev_slot_free)
     if (e) cudaEventDestroy(e);
   for (auto e : h->ev_wait0) cudaEventDestroy(e);
   for (auto e : h->ev_wait1) cudaEventDestroy(e);
@@ -912,9 +981,16 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   CK(cudaStreamCreateWithPriority(&h->s_comp, cudaStreamNonBlocking, prio_lo));
   CK(cudaStreamCreateWithPriority(&h->s_comm, cudaStreamNonBlocking, prio_hi));   // comm first
-  cudaEvent_t* evs[] = {&h->ev_in, &h->ev_ag[0], &h->ev_ag[1], &h->ev_slot_free[0], &h->ev_slot_free[1], &h->ev_grad[0],
-                        &h->ev_grad[1], &h->ev_adam[0], &h->ev_adam[1], &h->ev_comm_end, &h->ev_comp_end};
+  cudaEvent_t* evs[] = {&h->ev_in, &h->ev_grad[0], &h->ev_grad[1], &h->ev_adam[0], &h->ev_adam[1], &h->ev_comm_end,
+                        &h->ev_comp_end};
   for (auto e : evs) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  const int nev = std::max(2, c.Lloc);   // one per parameter slot (2, or L/P with KEEP_PARAMS)
+  h->ev_ag.assign(nev, nullptr);
+  h->ev_slot_free.assign(nev, nullptr);
+  for (int k = 0; k < nev; ++k) {
+    CK(cudaEventCreateWithFlags(&h->ev_ag[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_slot_free[k], cudaEventDisableTiming));
+  }
   CK(cudaEventCreate(&h->ev_t0));
   CK(cudaEventCreate(&h->ev_t1));
   CK(cudaEventCreate(&h->ev_fwd_end));
@@ -950,7 +1026,7 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
     if (!init_params) CK(cudaMalloc(&dev_full, (size_t)c.pl * sizeof(float)));
     for (int j = 0; j < Ll; ++j) {
       const int64_t gl = local_to_global(h, j);
-      const int64_t lo = (int64_t)h->replica * c.S, hi = std::min<int64_t>(lo + c.S, c.pl);
+      const int64_t lo = c.unpart ? 0 : (int64_t)h->replica * c.S, hi = std::min<int64_t>(lo + c.S, c.pl);
       float* dst = h->master + (int64_t)j * c.S;
       if (init_params) {
         if (hi > lo)
@@ -1004,8 +1080,7 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
   // both "staging buffer free" events start completed
   CK(cudaEventRecord(h->ev_adam[0], h->s_comm));
   CK(cudaEventRecord(h->ev_adam[1], h->s_comm));
-  CK(cudaEventRecord(h->ev_slot_free[0], h->s_comp));
-  CK(cudaEventRecord(h->ev_slot_free[1], h->s_comp));
+  for (auto e : h->ev_slot_free) CK(cudaEventRecord(e, h->s_comp));
   if (world > 1) {  // all ranks' arenas are initialised before anyone writes into a peer
     double* tmp = h->loss_dev;
     NK(ncclAllReduce(tmp, tmp, 1, ncclFloat64, ncclSum, h->world_comm, h->s_comp));
@@ -1047,7 +1122,7 @@ static lga_status run_step(lga_handle* h, const float* x, const float* T, double
   // global loss: sum of this rank's micro-batch losses (slots 1..N), all-reduced, / (D N)
   mse_finish(h->loss_dev + 1, c.N, 1.0, h->loss_dev, h->s_comp);
   KCHECK();
-  h->last.allreduce_calls = 1;
+  h->last.allreduce_calls += 1;   // the loss (plus, unpartitioned, the per-layer gradient all-reduces)
   if (h->world > 1 && !c.no_comm) NK(ncclAllReduce(h->loss_dev, h->loss_dev, 1, ncclFloat64, ncclSum, h->world_comm, h->s_comp));
   CK(cudaMemcpyAsync(h->loss_host, h->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, h->s_comp));
   CK(cudaEventRecord(h->ev_comp_end, h->s_comp));
@@ -1063,7 +1138,7 @@ static lga_status run_step(lga_handle* h, const float* x, const float* T, double
   tt.p2p_recv_calls += h->last.p2p_recv_calls; tt.allreduce_calls += h->last.allreduce_calls;
   tt.ag_bytes += h->last.ag_bytes; tt.rs_bytes += h->last.rs_bytes; tt.p2p_send_bytes += h->last.p2p_send_bytes;
   tt.p2p_recv_bytes += h->last.p2p_recv_bytes; tt.fwd_units += h->last.fwd_units; tt.bwd_units += h->last.bwd_units;
-  tt.recompute_units += h->last.recompute_units;
+  tt.recompute_units += h->last.recompute_units; tt.allreduce_bytes += h->last.allreduce_bytes;
   if (loss_out) {
     CK(cudaEventSynchronize(h->ev_t1));
     *loss_out = h->loss_host[0] / ((double)c.D * (double)c.N);
@@ -1096,7 +1171,7 @@ static lga_status gather_state(lga_handle* h, const float* src_shards, float* ou
   for (int j = 0; j < c.Lloc; ++j) {
     const float* shard = src_shards + (int64_t)j * c.S;
     float* dst = full + (int64_t)j * c.plpad;
-    if (c.D > 1) {
+    if (c.D > 1 && !c.unpart) {
       NK(ncclAllGather(shard, dst, (size_t)c.S, ncclFloat32, h->dp_comm, h->s_comp));
     } else {
       CK(cudaMemcpyAsync(dst, shard, (size_t)c.S * sizeof(float), cudaMemcpyDeviceToDevice, h->s_comp));
@@ -1131,7 +1206,7 @@ lga_status lga_comm_bytes(const lga_handle* h, lga_comm_stats* last_step, lga_co
 lga_status lga_layer_stage(const lga_handle* h, int32_t* stage_of_layer, int32_t n) {
   if (!h || !stage_of_layer) return ERR(LGA_ERR_INVALID_ARG, "NULL argument");
   if (n != h->c.L) return ERR(LGA_ERR_SIZE_MISMATCH, "n = %d, expected L = %d", n, h->c.L);
-  for (int i = 0; i < n; ++i) stage_of_layer[i] = i % h->c.P;
+  for (int i = 0; i < n; ++i) stage_of_layer[i] = stage_of(h->c, i);   // P:127 (modular) / P:71 (contiguous)
   return LGA_OK;
 }
 

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--lr", type=float, default=1e-3)
+    ap.add_argument("--flags", type=int, default=0)   # LGA_FLAG_* variants
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -34,7 +35,7 @@ def main():
     init = synth.init_params(sh, style="parity")
     cfg = Config(layers=sh.layers, d_model=sh.d, heads=sh.heads, seq_len=sh.seq, micro_batch=sh.micro_batch,
                  n_micro=sh.n_micro, dp=sh.dp, pp=sh.pp, precision=a.precision, schedule=a.schedule, chunk=a.chunk,
-                 lr=a.lr, retain_grads=1)
+                 lr=a.lr, retain_grads=1, flags=a.flags)
     tr = Trainer(cfg, rank=rank, world=world, device=local, init_params=init)
     losses = []
     for k in range(a.steps):

@@ -28,7 +28,7 @@ def test_struct_layout_matches_header():
     from paper_2106_02679_b200 import _abi
     # lga_config: 1 uint32 + 13 int32 + 6 float + 1 int32 + 1 uint32 = 22 * 4 bytes
     assert C.sizeof(_abi.lga_config) == 22 * 4
-    assert C.sizeof(_abi.lga_comm_stats) == 13 * 8
+    assert C.sizeof(_abi.lga_comm_stats) == 14 * 8   # ABI v2: + allreduce_bytes
     assert C.sizeof(_abi.lga_timing) == 8 * 4 + 3 * 4 + 4 + 3 * 8 + 8   # incl. padding before the doubles
 
 

@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 _port = [29611]
 
 
-def _launch(tmp_path, sh, precision=0, schedule=0, chunk=0, steps=1):
+def _launch(tmp_path, sh, precision=0, schedule=0, chunk=0, steps=1, flags=0):
     world = sh.dp * sh.pp
     if NGPU < world:
         pytest.skip(f"needs {world} GPUs, have {NGPU}")
@@ -31,30 +31,40 @@ def _launch(tmp_path, sh, precision=0, schedule=0, chunk=0, steps=1):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_port[0]}", os.path.join(HERE, "dist_worker.py"),
            "--out", str(tmp_path), "--shape", shape, "--precision", str(precision), "--schedule", str(schedule),
-           "--chunk", str(chunk), "--steps", str(steps)]
+           "--chunk", str(chunk), "--steps", str(steps), "--flags", str(flags)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return [dict(np.load(os.path.join(tmp_path, f"rank{k}.npz"))) for k in range(world)]
 
 
-def _check(outs, sh, tol, steps=1, schedule="layered", elem=4):
+# LGA_FLAG_* variant bits (include/lga.h) -> oracle.counters keyword arguments
+KEEP, NORECOMP, UNPART, CONTIG = 0x8, 0x10, 0x20, 0x40
+
+
+def _variant(flags):
+    return dict(keep_params=bool(flags & KEEP), no_recompute=bool(flags & NORECOMP),
+                unpartitioned=bool(flags & UNPART), pipeline="contiguous" if flags & CONTIG else "modular")
+
+
+def _check(outs, sh, tol, steps=1, schedule="layered", elem=4, flags=0):
     batches = [synth.batch(sh, step=k) for k in range(steps)]
     init = synth.init_params(sh, style="parity")
     rp, rl, rg = oracle_run(sh, init, batches, lr=1e-3)
     pl = sh.d * sh.d * 12 + 13 * sh.d
     for o in outs:
         stage = int(o["stage"])
-        layers = oc.local_layers(stage, sh.layers, sh.pp)
+        var = _variant(flags)
+        layers = oc.local_layers(stage, sh.layers, sh.pp, var["pipeline"])
         sel = np.concatenate([np.arange(i * pl, (i + 1) * pl) for i in layers])
         g, p = o["grads"], o["params"]
         assert rel(g, rg[sel]) < tol, (stage, per_layer_rel(g, rg[sel], len(layers)))
         assert rel(p, rp[sel]) < tol
         np.testing.assert_allclose(o["losses"], rl, rtol=max(tol, 1e-6))
-        assert list(o["stages"]) == [oc.stage_of_layer(i, sh.pp) for i in range(sh.layers)]
+        assert list(o["stages"]) == [oc.stage_of_layer(i, sh.pp, sh.layers, var["pipeline"]) for i in range(sh.layers)]
         last = json.loads(str(o["last"]))
         ref = oc.comm_counters(oc.StepShape(layers=sh.layers, d=sh.d, seq=sh.seq, micro_batch=sh.micro_batch,
                                             n_micro=sh.n_micro, dp=sh.dp, pp=sh.pp),
-                               stage=stage, schedule=schedule, param_bytes=elem, grad_bytes=elem)
+                               stage=stage, schedule=schedule, param_bytes=elem, grad_bytes=elem, **var)
         for k, v in ref.items():
             assert last[k] == v, (k, last[k], v, stage)
 
@@ -99,3 +109,32 @@ def test_pp4_fp32_modular_pipeline(tmp_path):
 def test_pp4_bf16_modular_pipeline(tmp_path):
     sh = synth.Shape(layers=4, d=256, heads=2, seq=128, micro_batch=1, n_micro=4, dp=1, pp=4)
     _check(_launch(tmp_path, sh, precision=1), sh, 2e-2, elem=2)
+
+
+# ---- variants: N2a keep params, N2b unpartitioned, N2c no recompute, N3 contiguous pipeline
+@pytest.mark.parametrize("flags", [KEEP, UNPART, NORECOMP, KEEP | NORECOMP])
+def test_dp2_fp32_variants(tmp_path, flags):
+    sh = synth.Shape(layers=4, d=64, heads=4, seq=32, micro_batch=2, n_micro=4, dp=2)
+    _check(_launch(tmp_path, sh, chunk=2, steps=2, flags=flags), sh, 1e-5, steps=2, flags=flags)
+
+
+@pytest.mark.parametrize("flags", [KEEP | NORECOMP, UNPART])
+def test_dp2_bf16_variants(tmp_path, flags):
+    sh = synth.Shape(layers=2, d=256, heads=2, seq=128, micro_batch=1, n_micro=4, dp=2)
+    _check(_launch(tmp_path, sh, precision=1, flags=flags), sh, 2e-2, elem=2, flags=flags)
+
+
+def test_pp2_fp32_contiguous_pipeline(tmp_path):
+    sh = synth.Shape(layers=4, d=64, heads=4, seq=32, micro_batch=2, n_micro=4, dp=1, pp=2)
+    _check(_launch(tmp_path, sh, flags=CONTIG), sh, 1e-5, flags=CONTIG)
+
+
+def test_pp2_dp2_fp32_contiguous_unpartitioned(tmp_path):
+    sh = synth.Shape(layers=4, d=64, heads=4, seq=32, micro_batch=2, n_micro=4, dp=2, pp=2)
+    f = CONTIG | UNPART | NORECOMP
+    _check(_launch(tmp_path, sh, flags=f), sh, 1e-5, flags=f)
+
+
+def test_pp4_bf16_contiguous_pipeline(tmp_path):
+    sh = synth.Shape(layers=8, d=256, heads=2, seq=128, micro_batch=1, n_micro=4, dp=1, pp=4)
+    _check(_launch(tmp_path, sh, precision=1, flags=CONTIG), sh, 2e-2, elem=2, flags=CONTIG)

@@ -18,11 +18,12 @@ if not torch.cuda.is_available():
 from paper_2106_02679_b200 import LGA_BF16, LGA_FP32, LGA_LAYERED, LGA_STANDARD, Config, Trainer  # noqa: E402
 
 
-def _run(sh, precision=LGA_FP32, schedule=LGA_LAYERED, chunk=0, causal=1, steps=1, lr=1e-3, wd=0.0, style="parity"):
+def _run(sh, precision=LGA_FP32, schedule=LGA_LAYERED, chunk=0, causal=1, steps=1, lr=1e-3, wd=0.0, style="parity",
+         flags=0):
     init = synth.init_params(sh, style=style)
     cfg = Config(layers=sh.layers, d_model=sh.d, heads=sh.heads, seq_len=sh.seq, micro_batch=sh.micro_batch,
                  n_micro=sh.n_micro, precision=precision, schedule=schedule, chunk=chunk, causal=causal, lr=lr,
-                 weight_decay=wd, retain_grads=1)
+                 weight_decay=wd, retain_grads=1, flags=flags)
     tr = Trainer(cfg, rank=0, world=1, device=0, init_params=init)
     batches = [synth.batch(sh, step=k) for k in range(steps)]
     losses = []
@@ -137,3 +138,28 @@ def test_bf16_layered_equals_standard_on_gpu():
     assert rel(a["grads"], b["grads"]) < 1e-2
     # and the step counters differ exactly as the closed forms say (D = 1: no collectives)
     assert a["stats"]["fwd_units"] == b["stats"]["fwd_units"] == 8
+
+
+NO_RECOMPUTE, KEEP_PARAMS = 0x10, 0x8
+
+
+@pytest.mark.parametrize("chunk", [0, 2])
+def test_fp32_no_recompute_parity(chunk):
+    """N2c: intermediates kept per layer for all micro-batches, no forward recompute -- same result,
+    recompute_units = 0."""
+    out, (rp, rl, rg, init) = _run(C1, chunk=chunk, steps=2, flags=NO_RECOMPUTE)
+    assert rel(out["grads"], rg) < 1e-5 and rel(out["params"], rp) < 1e-5
+    assert out["stats"]["recompute_units"] == 0 and out["stats"]["bwd_units"] == C1.n_micro * C1.layers
+
+
+def test_bf16_no_recompute_parity_and_flags_without_dp():
+    sh = synth.Shape(layers=2, d=256, heads=2, seq=128, micro_batch=1, n_micro=4)
+    out, (rp, rl, rg, _) = _run(sh, precision=LGA_BF16, flags=NO_RECOMPUTE | KEEP_PARAMS)
+    assert rel(out["grads"], rg) < 2e-2 and rel(out["params"], rp) < 2e-2
+    assert out["stats"]["ag_calls"] == 0 and out["stats"]["recompute_units"] == 0
+
+
+def test_variant_flags_rejected_with_standard():
+    from paper_2106_02679_b200._abi import LgaError
+    with pytest.raises(LgaError):
+        _run(C1, schedule=LGA_STANDARD, flags=NO_RECOMPUTE)

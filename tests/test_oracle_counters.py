@@ -100,3 +100,49 @@ def test_forward_flops_are_two_per_token_per_weight():
     pairs = sum(i + 1 for i in range(s))
     assert oc.flops_per_token_forward(d, s, causal=True) == 2 * gemm_params + 4 * d * pairs / s
     assert oc.flops_per_token_hw(2, d, s) == 4 / 3 * oc.flops_per_token_model(2, d, s)
+
+
+# ---- variants ------------------------------------------------------------
+
+@pytest.mark.parametrize("D", [2, 4, 8])
+def test_keep_params_and_unpartitioned_move_the_nonpartitioned_volume(D):
+    """Keeping the forward gather (1 AG + 1 RS) or dropping the partition (1 all-reduce = scatter-
+    reduce + all-gather) moves exactly 8 (D-1) p / D in+out, the non-partitioned volume of P:565 --
+    i.e. the partition's +50% is exactly the second all-gather."""
+    sh = _shape(dp=D)
+    p = om.param_count(sh.d, sh.layers)
+    keep = oc.comm_counters(sh, keep_params=True)
+    assert 2 * (keep["ag_bytes"] + keep["rs_bytes"]) == oc.paper_dp_bytes_nonpartitioned(D, p, D)
+    assert (keep["ag_calls"], keep["rs_calls"]) == (24, 24)
+    unp = oc.comm_counters(sh, unpartitioned=True)
+    assert unp["ag_calls"] == unp["rs_calls"] == 0
+    assert unp["allreduce_calls"] == 1 + 24
+    assert 2 * unp["allreduce_bytes"] == oc.paper_dp_bytes_nonpartitioned(D, p, D)
+    full = oc.comm_counters(sh)
+    assert 2 * (full["ag_bytes"] + full["rs_bytes"]) == 1.5 * 2 * (keep["ag_bytes"] + keep["rs_bytes"])
+
+
+def test_no_recompute_units():
+    c = oc.comm_counters(_shape(), no_recompute=True)
+    assert c["recompute_units"] == 0 and c["fwd_units"] == c["bwd_units"] == 384
+    assert c["ag_bytes"] == oc.comm_counters(_shape())["ag_bytes"]   # communication unchanged
+
+
+def test_variants_without_data_parallelism_move_nothing():
+    for kw in (dict(keep_params=True), dict(unpartitioned=True)):
+        c = oc.comm_counters(_shape(dp=1), **kw)
+        assert c["ag_bytes"] == c["rs_bytes"] == c["allreduce_bytes"] == 0 and c["allreduce_calls"] == 1
+
+
+def test_contiguous_stage_map_and_crossings():
+    """Contiguous blocks of L/P layers: activations cross stages only at the P-1 block
+    boundaries, 2 N (P-1) crossings per step in total (vs 2 N (L-1) for the modular map)."""
+    assert [oc.stage_of_layer(i, 4, 8, "contiguous") for i in range(8)] == [0, 0, 1, 1, 2, 2, 3, 3]
+    assert oc.local_layers(1, 8, 4, "contiguous") == [2, 3]
+    sh = _shape(layers=48, d=4096, n_micro=32, dp=2, pp=4)
+    per = [oc.comm_counters(sh, stage=s, pipeline="contiguous") for s in range(4)]
+    assert [c["p2p_send_calls"] for c in per] == [32, 64, 64, 32]
+    assert sum(c["p2p_send_calls"] for c in per) == 2 * 32 * (4 - 1)
+    assert [c["p2p_recv_calls"] for c in per] == [32, 64, 64, 32]
+    modular = sum(c["p2p_send_calls"] for c in (oc.comm_counters(sh, stage=s) for s in range(4)))
+    assert modular == 2 * 32 * 47
