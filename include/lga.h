@@ -77,7 +77,10 @@ typedef enum { LGA_LAYERED = 0, LGA_STANDARD = 1 } lga_schedule;
 /* flags */
 #define LGA_FLAG_NO_COMM   0x1u  /* debug A/B timing only: skip every collective and p2p
                                     transfer (results are then wrong); counters still count */
-#define LGA_FLAG_NO_GRAPH  0x2u  /* reserved */
+#define LGA_FLAG_NO_GRAPH  0x2u  /* run every step eagerly.  By default lga_step captures the whole step
+                                    (all streams, NCCL calls included) into a CUDA graph at its second
+                                    call and replays it while x / target keep their pointers; the first
+                                    call and lga_step_host run eagerly */
 #define LGA_FLAG_PROFILE   0x4u  /* record CUDA events around every GEMM / attention / AdamW launch
                                     (on the stream it is launched on) for lga_timing_last */
 /* Memory-rich variants and the contiguous pipeline (N3).  All require

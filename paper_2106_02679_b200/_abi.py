@@ -19,6 +19,7 @@ NCCL_ID_BYTES = 128
 LGA_FP32, LGA_BF16 = 0, 1
 LGA_LAYERED, LGA_STANDARD = 0, 1
 LGA_FLAG_NO_COMM = 0x1
+LGA_FLAG_NO_GRAPH = 0x2         # every step eager (default: CUDA graph from the second lga_step)
 LGA_FLAG_PROFILE = 0x4
 LGA_FLAG_KEEP_PARAMS = 0x8       # N2a: 1 all-gather per layer per step
 LGA_FLAG_NO_RECOMPUTE = 0x10     # N2c: keep intermediates, no forward recompute

@@ -140,7 +140,10 @@ template <typename GE, typename PE>
 __global__ void __launch_bounds__(256) adamw_kernel(const GE* __restrict__ gin, float gscale, float* __restrict__ master,
                                                     float* __restrict__ m, float* __restrict__ v, PE* __restrict__ pout,
                                                     float* __restrict__ keep, int64_t n, float lr, float b1, float b2,
-                                                    float eps, float wd, float bc1, float bc2) {
+                                                    float eps, float wd, const long long* __restrict__ tstep) {
+  // bias corrections of step t (from 1), read on the device so that a captured step graph replays them
+  const float t = (float)*tstep;
+  const float bc1 = 1.0f - powf(b1, t), bc2 = 1.0f - powf(b2, t);
   const int64_t n4 = n / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
@@ -185,10 +188,10 @@ __global__ void __launch_bounds__(256) adamw_kernel(const GE* __restrict__ gin, 
 
 void adamw(const void* gin, DT gdt, float gscale, float* master, float* m, float* v,
            void* param_out, DT pdt, float* keep, int64_t n, float lr, float beta1, float beta2,
-           float eps, float wd, float bc1, float bc2, cudaStream_t st) {
+           float eps, float wd, const long long* tstep, cudaStream_t st) {
   if (n <= 0) return;
   const int grid = (int)std::min<int64_t>((n / 4 + 255) / 256 + 1, (int64_t)num_sms() * 8);
-#define AD(GE, PE) note_launch(), adamw_kernel<GE, PE><<<grid, 256, 0, st>>>((const GE*)gin, gscale, master, m, v, (PE*)param_out, keep, n, lr, beta1, beta2, eps, wd, bc1, bc2)
+#define AD(GE, PE) note_launch(), adamw_kernel<GE, PE><<<grid, 256, 0, st>>>((const GE*)gin, gscale, master, m, v, (PE*)param_out, keep, n, lr, beta1, beta2, eps, wd, tstep)
   if (gdt == DT::F32 && pdt == DT::F32) AD(float, float);
   else if (gdt == DT::F32) AD(float, __nv_bfloat16);
   else if (pdt == DT::F32) AD(__nv_bfloat16, float);
@@ -282,7 +285,11 @@ void init_params_device(float* out, int64_t n_layers, int d, int ffn_mult, int L
 }
 
 // =============================================================== pipeline flags
-__global__ void wait_flag_kernel(const volatile unsigned long long* flag, unsigned long long target) {
+// Pipeline flags count transfers since lga_init.  Targets are (t - 1) * per_step + k with t the device
+// step counter, so a captured step graph waits for / publishes the right values on every replay.
+__global__ void wait_flag_kernel(const volatile unsigned long long* flag, const long long* tstep,
+                                 unsigned long long per_step, unsigned long long k) {
+  const unsigned long long target = (unsigned long long)(*tstep - 1) * per_step + k;
   unsigned long long v;
   while (true) {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
@@ -290,16 +297,23 @@ __global__ void wait_flag_kernel(const volatile unsigned long long* flag, unsign
     __nanosleep(200);
   }
 }
-void wait_flag(const volatile unsigned long long* flag, unsigned long long target, cudaStream_t st) {
-  note_launch(), wait_flag_kernel<<<1, 1, 0, st>>>(flag, target);
+void wait_flag(const volatile unsigned long long* flag, const long long* tstep, unsigned long long per_step,
+               unsigned long long k, cudaStream_t st) {
+  note_launch(), wait_flag_kernel<<<1, 1, 0, st>>>(flag, tstep, per_step, k);
 }
-__global__ void set_flag_kernel(unsigned long long* flag, unsigned long long value) {
+__global__ void set_flag_kernel(unsigned long long* flag, const long long* tstep, unsigned long long per_step,
+                                unsigned long long k) {
+  const unsigned long long value = (unsigned long long)(*tstep - 1) * per_step + k;
   __threadfence_system();
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
 }
-void set_flag(unsigned long long* flag, unsigned long long value, cudaStream_t st) {
-  note_launch(), set_flag_kernel<<<1, 1, 0, st>>>(flag, value);
+void set_flag(unsigned long long* flag, const long long* tstep, unsigned long long per_step, unsigned long long k,
+              cudaStream_t st) {
+  note_launch(), set_flag_kernel<<<1, 1, 0, st>>>(flag, tstep, per_step, k);
 }
+// the step counter t (AdamW bias corrections, flag epochs): incremented first thing in every step
+__global__ void step_begin_kernel(long long* tstep) { *tstep += 1; }
+void step_begin(long long* tstep, cudaStream_t st) { note_launch(), step_begin_kernel<<<1, 1, 0, st>>>(tstep); }
 
 static std::atomic<unsigned long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }

@@ -107,7 +107,7 @@ void mse_finish(const double* partial, int nblk, double scale, double* out, cuda
 // param_out (E) = theta; keep (fp32, optional) = g.
 void adamw(const void* gin, DT gdt, float gscale, float* master, float* m, float* v,
            void* param_out, DT pdt, float* keep, int64_t n, float lr, float beta1, float beta2,
-           float eps, float wd, float bc1, float bc2, cudaStream_t st);
+           float eps, float wd, const long long* tstep, cudaStream_t st);
 
 // STANDARD schedule: acc[i] = (first ? 0 : acc[i]) + g[i]   (per-micro-batch reduced shard)
 void shard_accumulate(const void* g, DT gdt, float* acc, int64_t n, bool first, cudaStream_t st);
@@ -121,8 +121,11 @@ void fill_f32(float* p, float v, int64_t n, cudaStream_t st);
 void init_params_device(float* out, int64_t n_layers, int d, int ffn_mult, int L_total,
                         int64_t first_layer, uint64_t seed, cudaStream_t st);
 // Spin until *flag >= target (system-scope acquire); used for pipeline receives.
-void wait_flag(const volatile unsigned long long* flag, unsigned long long target, cudaStream_t st);
+void wait_flag(const volatile unsigned long long* flag, const long long* tstep, unsigned long long per_step,
+               unsigned long long k, cudaStream_t st);
 // *flag = value (system-scope release) after all prior work on the stream.
-void set_flag(unsigned long long* flag, unsigned long long value, cudaStream_t st);
+void set_flag(unsigned long long* flag, const long long* tstep, unsigned long long per_step, unsigned long long k,
+              cudaStream_t st);
+void step_begin(long long* tstep, cudaStream_t st);
 
 }  // namespace lga

@@ -71,6 +71,7 @@ struct Cfg {
   float lr, b1, b2, eps, wd, ln_eps;
   bool retain, no_comm, profile;
   bool keep, norecomp, unpart, contig;   // LGA_FLAG_KEEP_PARAMS / NO_RECOMPUTE / UNPARTITIONED / CONTIGUOUS_PP
+  bool graph_off;                        // LGA_FLAG_NO_GRAPH
   // canonical offsets
   int64_t o_ln1w, o_ln1b, o_wqkv, o_bqkv, o_wo, o_bo, o_ln2w, o_ln2b, o_w1, o_b1, o_w2, o_b2;
 };
@@ -119,6 +120,7 @@ static lga_status validate(const lga_config* c, int world, Cfg* out) {
   g.keep = (c->flags & LGA_FLAG_KEEP_PARAMS) != 0;
   g.norecomp = (c->flags & LGA_FLAG_NO_RECOMPUTE) != 0;
   g.contig = (c->flags & LGA_FLAG_CONTIGUOUS_PP) != 0;
+  g.graph_off = (c->flags & LGA_FLAG_NO_GRAPH) != 0;
   g.bf16 = c->precision == LGA_BF16;
   g.layered = c->schedule == LGA_LAYERED;
   g.causal = c->causal != 0;
@@ -174,7 +176,8 @@ struct lga_handle {
   Cfg c{};
   int rank = 0, world = 1, stage = 0, replica = 0, dev = 0;
   bool bad = false;
-  cudaStream_t user = nullptr, s_comp = nullptr, s_comm = nullptr;
+  cudaStream_t user = nullptr, s_comp = nullptr, s_comm = nullptr, s_copy = nullptr;
+  bool tin_pending = false;   // lga_step_host: the target copy (on s_copy) not yet awaited by the loss
   ncclComm_t world_comm = nullptr, dp_comm = nullptr;
   Arena arena;
   // training state, per local layer j: [Lloc][S]
@@ -202,11 +205,25 @@ struct lga_handle {
   char* peer_prev_base = nullptr;  // stage (s-1) mod P
   float *next_ckpt = nullptr, *prev_dY = nullptr;
   unsigned long long *next_flags = nullptr, *prev_flags = nullptr;
-  unsigned long long sent_fwd = 0, sent_bwd = 0, recv_fwd = 0, recv_bwd = 0;
+  unsigned long long sent_fwd = 0, sent_bwd = 0, recv_fwd = 0, recv_bwd = 0;   // this step's transfers so far
+  unsigned long long k_send_fwd = 0, k_send_bwd = 0, k_recv_fwd = 0, k_recv_bwd = 0;   // per step (stage map)
+  long long* tstep = nullptr;   // device step counter t (from 1): AdamW bias corrections, flag epochs
+  // cross-step event waits are redundant (every step starts after the previous one completed) and illegal
+  // inside a stream capture: only wait on events recorded earlier in the same step
+  bool rec_adam[2] = {false, false};
+  std::vector<char> rec_slot;
+  // CUDA graph of lga_step (captured at the second call, replayed while x / target keep their pointers)
+  bool capturing = false, graph_broken = false;
+  int eager_steps = 0;
+  cudaGraphExec_t gexec = nullptr;
+  const float *g_x = nullptr, *g_T = nullptr;
+  lga_comm_stats g_last{};
+  int g_nwait = 0, g_nprof = 0;
+  unsigned long long g_launches = 0;
   int64_t partial_floats = 0;
   // events
   std::vector<cudaEvent_t> ev_ag, ev_slot_free;   // per slot
-  cudaEvent_t ev_in = nullptr, ev_grad[2] = {}, ev_adam[2] = {}, ev_comm_end = nullptr,
+  cudaEvent_t ev_in = nullptr, ev_tin = nullptr, ev_grad[2] = {}, ev_adam[2] = {}, ev_comm_end = nullptr,
               ev_comp_end = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_fwd_end = nullptr;
   std::vector<cudaEvent_t> ev_wait0, ev_wait1;   // stall accounting pairs (s_comp)
   std::vector<int> wait_kind;
@@ -288,6 +305,13 @@ static void plan_arena(lga_handle* h) {
   h->xin = A.take<float>(act);
   h->tin = A.take<float>(act);
   h->flags = A.take<unsigned long long>(8);
+  h->tstep = A.take<long long>(1);
+}
+
+// timing events: plain records, or event-record nodes (cudaEventRecordExternal) inside a step capture
+static void rec_time(lga_handle* h, cudaEvent_t ev, cudaStream_t st) {
+  if (h->capturing) CK(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal));
+  else CK(cudaEventRecord(ev, st));
 }
 
 // ------------------------------------------------------------------ profiling
@@ -303,12 +327,12 @@ static int prof_begin(lga_handle* h, cudaStream_t st) {
     h->prof_fam.push_back(0);
     h->prof_work.push_back(0.0);
   }
-  CK(cudaEventRecord(h->prof0[h->n_prof], st));
+  rec_time(h, h->prof0[h->n_prof], st);
   return h->n_prof++;
 }
 static void prof_end(lga_handle* h, int idx, cudaStream_t st, int fam, double work) {
   if (idx < 0) return;
-  CK(cudaEventRecord(h->prof1[idx], st));
+  rec_time(h, h->prof1[idx], st);
   h->prof_fam[idx] = fam;
   h->prof_work[idx] = work;
 }
@@ -569,12 +593,12 @@ static void count_wait(lga_handle* h, cudaEvent_t ev, int kind) {
     h->wait_kind.push_back(kind);
   }
   h->wait_kind[h->n_wait] = kind;
-  CK(cudaEventRecord(h->ev_wait0[h->n_wait], h->s_comp));
+  rec_time(h, h->ev_wait0[h->n_wait], h->s_comp);
   if (ev) CK(cudaStreamWaitEvent(h->s_comp, ev, 0));
   return;
 }
 static void count_wait_end(lga_handle* h) {
-  CK(cudaEventRecord(h->ev_wait1[h->n_wait], h->s_comp));
+  rec_time(h, h->ev_wait1[h->n_wait], h->s_comp);
   h->n_wait++;
 }
 
@@ -595,12 +619,11 @@ static void all_gather(lga_handle* h, int j, int slot) {
 // AdamW on this rank's shard of local layer j (update "as soon as possible", A-12)
 static void adam_layer(lga_handle* h, int j, const void* g, DT gdt) {
   const Cfg& c = h->c;
-  const float bc1 = 1.0f - powf(c.b1, (float)h->t), bc2 = 1.0f - powf(c.b2, (float)h->t);
   const float gscale = 1.0f / ((float)c.D * (float)c.N);   // gradient of the mean loss (A-3)
   const int64_t off = (int64_t)j * c.S;
   const int p = prof_begin(h, h->s_comm);
   adamw(g, gdt, gscale, h->master + off, h->mom + off, h->var + off, eoff(h->pshard, c.E, off), c.E,
-        c.retain ? h->gkeep + off : nullptr, c.S, c.lr, c.b1, c.b2, c.eps, c.wd, bc1, bc2, h->s_comm);
+        c.retain ? h->gkeep + off : nullptr, c.S, c.lr, c.b1, c.b2, c.eps, c.wd, h->tstep, h->s_comm);
   KCHECK();
   const double per = (double)dt_size(gdt) + 24.0 + (double)dt_size(c.E) + (c.retain ? 4.0 : 0.0);
   prof_end(h, p, h->s_comm, FAM_ADAM, per * (double)c.S);
@@ -658,6 +681,13 @@ static Ws chunk_ws(lga_handle* h, int j, int m0) {
   return w;
 }
 
+// lga_step_host copies the target on its own stream, overlapped with the forward; the first loss waits
+static void await_target(lga_handle* h) {
+  if (!h->tin_pending) return;
+  CK(cudaStreamWaitEvent(h->s_comp, h->ev_tin, 0));
+  h->tin_pending = false;
+}
+
 // ------------------------------------------------------------------ the step (LAYERED, any D, any P)
 // Parameter slots: with mixed buffering (2 slots) the gather of layer j goes to slot agk % 2, agk counting
 // gathers over the step; with LGA_FLAG_KEEP_PARAMS layer j has slot j, filled once in the forward.
@@ -670,7 +700,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
   int agk = 0;  // running all-gather index
   // ---------------- forward: layer-major over all micro-batches
   if (dp_gather) {
-    CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[slot_of(0, 0)], 0));
+    if (h->rec_slot[slot_of(0, 0)]) CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[slot_of(0, 0)], 0));
     all_gather(h, 0, slot_of(0, 0));
     CK(cudaEventRecord(h->ev_ag[slot_of(0, 0)], h->s_comm));
   }
@@ -679,7 +709,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
     const int64_t i = local_to_global(h, j);
     if (dp_gather && j + 1 < c.Lloc) {  // prefetch Restore(next local layer) while computing layer i
       const int sn = slot_of(j + 1, agk + 1);
-      CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[sn], 0));
+      if (h->rec_slot[sn]) CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[sn], 0));
       all_gather(h, j + 1, sn);
       CK(cudaEventRecord(h->ev_ag[sn], h->s_comm));
     }
@@ -703,7 +733,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
           h->last.p2p_recv_bytes += (uint64_t)c.c * mb * 4;
           if (!c.no_comm) {
             count_wait(h, nullptr, 1);
-            wait_flag(h->flags + 0, h->recv_fwd, h->s_comp);
+            wait_flag(h->flags + 0, h->tstep, h->k_recv_fwd, h->recv_fwd, h->s_comp);
             KCHECK();
             count_wait_end(h);
           }
@@ -725,12 +755,13 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
         h->last.p2p_send_calls += c.c;
         h->last.p2p_send_bytes += (uint64_t)c.c * mb * 4;
         if (!c.no_comm) {
-          set_flag(h->next_flags + 0, h->sent_fwd, h->s_comp);
+          set_flag(h->next_flags + 0, h->tstep, h->k_send_fwd, h->sent_fwd, h->s_comp);
           KCHECK();
         }
       }
       if (i == c.L - 1) {  // loss of this chunk + seed gradient
         const int64_t n = (int64_t)c.c * mb;
+        await_target(h);
         mse_fwd_bwd(act_ptr(h->yout, c, m0), T + m0 * mb, act_ptr(h->dY, c, m0), h->mse_partial + 0, n,
                     1.0f / (float)mb, h->s_comp);
         KCHECK();
@@ -739,13 +770,13 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
         KCHECK();
       }
     }
-    if (!c.keep) CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
+    if (!c.keep) { CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp)); h->rec_slot[sl] = 1; }
     trace(h, "fwd", i);
   }
-  CK(cudaEventRecord(h->ev_fwd_end, h->s_comp));
+  rec_time(h, h->ev_fwd_end, h->s_comp);
   // ---------------- backward: layer-major, (recompute +) backward over all micro-batches
   if (dp_gather && !c.keep) {
-    CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[agk % 2], 0));
+    if (h->rec_slot[agk % 2]) CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[agk % 2], 0));
     all_gather(h, c.Lloc - 1, agk % 2);
     CK(cudaEventRecord(h->ev_ag[agk % 2], h->s_comm));
   }
@@ -754,7 +785,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
     const int64_t i = local_to_global(h, j);
     const int gb = j % 2;
     if (dp_gather && !c.keep && j - 1 >= 0) {
-      CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[(agk + 1) % 2], 0));
+      if (h->rec_slot[(agk + 1) % 2]) CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[(agk + 1) % 2], 0));
       all_gather(h, j - 1, (agk + 1) % 2);
       CK(cudaEventRecord(h->ev_ag[(agk + 1) % 2], h->s_comm));
     }
@@ -762,7 +793,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
       count_wait(h, h->ev_ag[sl], 0);
       count_wait_end(h);
     }
-    CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));   // staging buffer gb free again
+    if (h->rec_adam[gb]) CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));   // staging buffer gb free again
     const void* W = layer_weights(h, j, sl);
     const bool recv = c.P > 1 && i < c.L - 1 && stage_of(c, i + 1) != h->stage;   // dY_i from another stage
     const bool send = c.P > 1 && i > 0 && stage_of(c, i - 1) != h->stage;         // dX_i to another stage
@@ -780,7 +811,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
         h->last.p2p_recv_bytes += (uint64_t)c.c * mb * 4;
         if (!c.no_comm) {
           count_wait(h, nullptr, 1);
-          wait_flag(h->flags + 1, h->recv_bwd, h->s_comp);
+          wait_flag(h->flags + 1, h->tstep, h->k_recv_bwd, h->recv_bwd, h->s_comp);
           KCHECK();
           count_wait_end(h);
         }
@@ -801,18 +832,18 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
         h->last.p2p_send_calls += c.c;
         h->last.p2p_send_bytes += (uint64_t)c.c * mb * 4;
         if (!c.no_comm) {
-          set_flag(h->prev_flags + 1, h->sent_bwd, h->s_comp);
+          set_flag(h->prev_flags + 1, h->tstep, h->k_send_bwd, h->sent_bwd, h->s_comp);
           KCHECK();
         }
       }
     }
-    CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
+    { CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp)); h->rec_slot[sl] = 1; }
     trace(h, "bwd", i);
     CK(cudaEventRecord(h->ev_grad[gb], h->s_comp));
     CK(cudaStreamWaitEvent(h->s_comm, h->ev_grad[gb], 0));
     void* shard_g = reduce_scatter(h, gb);
     adam_layer(h, j, shard_g, c.G);
-    CK(cudaEventRecord(h->ev_adam[gb], h->s_comm));
+    { CK(cudaEventRecord(h->ev_adam[gb], h->s_comm)); h->rec_adam[gb] = true; }
   }
 }
 
@@ -827,7 +858,7 @@ static void step_standard(lga_handle* h, const float* x, const float* T) {
     for (int j = 0; j < c.L; ++j, ++agk) {
       const int sl = agk % 2;
       if (c.D > 1) {
-        CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[sl], 0));
+        if (h->rec_slot[sl]) CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[sl], 0));
         all_gather(h, j, sl);
         CK(cudaEventRecord(h->ev_ag[sl], h->s_comm));
         count_wait(h, h->ev_ag[sl], 0);
@@ -837,8 +868,9 @@ static void step_standard(lga_handle* h, const float* x, const float* T) {
       float* yo = j == c.L - 1 ? act_ptr(h->yout, c, m) : ckpt_ptr(h, j + 1, m);
       layer_fwd(h, h->ws[0], layer_weights(h, j, sl), xin, yo, h->s_comp);
       h->last.fwd_units++;
-      CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
+      { CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp)); h->rec_slot[sl] = 1; }
     }
+    await_target(h);
     mse_fwd_bwd(act_ptr(h->yout, c, m), T + m * mb, act_ptr(h->dY, c, m), h->mse_partial, mb, 1.0f / (float)mb, h->s_comp);
     KCHECK();
     mse_finish(h->mse_partial, mse_blocks(mb), 0.5 / (double)mb, h->loss_dev + 1 + m, h->s_comp);
@@ -847,13 +879,13 @@ static void step_standard(lga_handle* h, const float* x, const float* T) {
       const int sl = agk % 2;
       const int gb = j % 2;
       if (c.D > 1) {
-        CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[sl], 0));
+        if (h->rec_slot[sl]) CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[sl], 0));
         all_gather(h, j, sl);
         CK(cudaEventRecord(h->ev_ag[sl], h->s_comm));
         count_wait(h, h->ev_ag[sl], 0);
         count_wait_end(h);
       }
-      CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));
+      if (h->rec_adam[gb]) CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));
       const void* W = layer_weights(h, j, sl);
       const float* xin = j == 0 ? x + m * mb : ckpt_ptr(h, j, m);
       float* dYc = act_ptr(h->dY, c, m);
@@ -861,7 +893,7 @@ static void step_standard(lga_handle* h, const float* x, const float* T) {
       h->last.recompute_units++;
       layer_bwd(h, h->ws[0], W, xin, dYc, j == 0 ? h->dscratch : dYc, 0, 1, gb, h->s_comp);
       h->last.bwd_units++;
-      CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp));
+      { CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp)); h->rec_slot[sl] = 1; }
       CK(cudaEventRecord(h->ev_grad[gb], h->s_comp));
       CK(cudaStreamWaitEvent(h->s_comm, h->ev_grad[gb], 0));
       // reduce-scatter this micro-batch's gradient, accumulate it on the shard (fixed order over m)
@@ -870,7 +902,7 @@ static void step_standard(lga_handle* h, const float* x, const float* T) {
       shard_accumulate(shard_g, c.G, acc, c.S, m == 0, h->s_comm);
       KCHECK();
       if (m == c.N - 1) adam_layer(h, j, acc, DT::F32);
-      CK(cudaEventRecord(h->ev_adam[gb], h->s_comm));
+      { CK(cudaEventRecord(h->ev_adam[gb], h->s_comm)); h->rec_adam[gb] = true; }
     }
   }
 }
@@ -937,11 +969,13 @@ static void free_handle(lga_handle* h) {
   cudaSetDevice(h->dev);
   if (h->s_comp) cudaStreamSynchronize(h->s_comp);
   if (h->s_comm) cudaStreamSynchronize(h->s_comm);
+  if (h->s_copy) cudaStreamSynchronize(h->s_copy);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->peer_next_base) cudaIpcCloseMemHandle(h->peer_next_base);
   if (h->peer_prev_base && h->peer_prev_base != h->peer_next_base) cudaIpcCloseMemHandle(h->peer_prev_base);
   if (h->dp_comm) ncclCommDestroy(h->dp_comm);
   if (h->world_comm) ncclCommDestroy(h->world_comm);
-  cudaEvent_t evs[] = {h->ev_in, h->ev_grad[0], h->ev_grad[1], h->ev_adam[0], h->ev_adam[1], h->ev_comm_end,
+  cudaEvent_t evs[] = {h->ev_in, h->ev_tin, h->ev_grad[0], h->ev_grad[1], h->ev_adam[0], h->ev_adam[1], h->ev_comm_end,
                        h->ev_comp_end, h->ev_t0, h->ev_t1, h->ev_fwd_end};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
@@ -953,6 +987,7 @@ static void free_handle(lga_handle* h) {
   for (auto e : h->ev_wait1) cudaEventDestroy(e);
   if (h->s_comp) cudaStreamDestroy(h->s_comp);
   if (h->s_comm) cudaStreamDestroy(h->s_comm);
+  if (h->s_copy) cudaStreamDestroy(h->s_copy);
   if (h->arena.base) cudaFree(h->arena.base);
   if (h->loss_host) cudaFreeHost(h->loss_host);
   delete h;
@@ -981,7 +1016,8 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   CK(cudaStreamCreateWithPriority(&h->s_comp, cudaStreamNonBlocking, prio_lo));
   CK(cudaStreamCreateWithPriority(&h->s_comm, cudaStreamNonBlocking, prio_hi));   // comm first
-  cudaEvent_t* evs[] = {&h->ev_in, &h->ev_grad[0], &h->ev_grad[1], &h->ev_adam[0], &h->ev_adam[1], &h->ev_comm_end,
+  CK(cudaStreamCreateWithPriority(&h->s_copy, cudaStreamNonBlocking, prio_lo));
+  cudaEvent_t* evs[] = {&h->ev_in, &h->ev_tin, &h->ev_grad[0], &h->ev_grad[1], &h->ev_adam[0], &h->ev_adam[1], &h->ev_comm_end,
                         &h->ev_comp_end};
   for (auto e : evs) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   const int nev = std::max(2, c.Lloc);   // one per parameter slot (2, or L/P with KEEP_PARAMS)
@@ -990,6 +1026,13 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
   for (int k = 0; k < nev; ++k) {
     CK(cudaEventCreateWithFlags(&h->ev_ag[k], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->ev_slot_free[k], cudaEventDisableTiming));
+  }
+  h->rec_slot.assign(nev, 0);
+  // pipeline transfers per step on this stage (flag epochs): chunks of every layer boundary it crosses
+  for (int j = 0; j < c.Lloc && c.P > 1; ++j) {
+    const int64_t i = local_to_global(h, j);
+    if (i > 0 && stage_of(c, i - 1) != h->stage) h->k_recv_fwd += c.N, h->k_send_bwd += c.N;
+    if (i < c.L - 1 && stage_of(c, i + 1) != h->stage) h->k_send_fwd += c.N, h->k_recv_bwd += c.N;
   }
   CK(cudaEventCreate(&h->ev_t0));
   CK(cudaEventCreate(&h->ev_t1));
@@ -1091,6 +1134,87 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
   ABI_CATCH
 }
 
+// Issue one step on s_comp / s_comm / s_copy: from "s_comp, s_comm start after ev_in" to "s_comp has joined
+// every stream".  Host-side counters (h->last, the event indices) are rebuilt on every issue.
+static void issue_step(lga_handle* h, const float* x, const float* T, bool host_inputs) {
+  const Cfg& c = h->c;
+  const bool need_x = h->stage == 0, need_t = owns_last(h);
+  h->last = lga_comm_stats{};
+  h->n_wait = 0;
+  h->n_prof = 0;
+  h->sent_fwd = h->sent_bwd = h->recv_fwd = h->recv_bwd = 0;
+  h->rec_adam[0] = h->rec_adam[1] = false;
+  std::fill(h->rec_slot.begin(), h->rec_slot.end(), 0);
+  step_begin(h->tstep, h->s_comp);   // t += 1 before anything reads it
+  KCHECK();
+  CK(cudaEventRecord(h->ev_in, h->s_comp));
+  CK(cudaStreamWaitEvent(h->s_comm, h->ev_in, 0));
+  const int64_t act = (int64_t)c.N * c.M * c.d;
+  if (host_inputs) {
+    if (need_x) CK(cudaMemcpyAsync(h->xin, x, act * sizeof(float), cudaMemcpyHostToDevice, h->s_comp));
+    if (need_t) {  // needed only at the loss: copy on s_copy, overlapped with the forward
+      CK(cudaStreamWaitEvent(h->s_copy, h->ev_in, 0));
+      CK(cudaMemcpyAsync(h->tin, T, act * sizeof(float), cudaMemcpyHostToDevice, h->s_copy));
+      CK(cudaEventRecord(h->ev_tin, h->s_copy));
+      h->tin_pending = true;
+    }
+    x = need_x ? h->xin : nullptr;
+    T = need_t ? h->tin : nullptr;
+  }
+  CK(cudaMemsetAsync(h->loss_dev, 0, (c.N + 8) * sizeof(double), h->s_comp));
+  rec_time(h, h->ev_fwd_end, h->s_comp);   // re-recorded at the forward/backward boundary (LAYERED)
+  if (c.layered) step_layered(h, x, T);
+  else step_standard(h, x, T);
+  await_target(h);
+  // global loss: sum of this rank's micro-batch losses (slots 1..N), all-reduced, / (D N)
+  mse_finish(h->loss_dev + 1, c.N, 1.0, h->loss_dev, h->s_comp);
+  KCHECK();
+  h->last.allreduce_calls += 1;   // the loss (plus, unpartitioned, the per-layer gradient all-reduces)
+  if (h->world > 1 && !c.no_comm) NK(ncclAllReduce(h->loss_dev, h->loss_dev, 1, ncclFloat64, ncclSum, h->world_comm, h->s_comp));
+  CK(cudaMemcpyAsync(h->loss_host, h->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, h->s_comp));
+  CK(cudaEventRecord(h->ev_comm_end, h->s_comm));
+  CK(cudaStreamWaitEvent(h->s_comp, h->ev_comm_end, 0));
+}
+
+// Capture issue_step into a graph (LGA_FLAG_NO_GRAPH off, device inputs).  False on any capture failure
+// (the step then runs eagerly and capture is not retried).
+static bool capture_step(lga_handle* h, const float* x, const float* T) {
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamBeginCapture(h->s_comp, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  h->capturing = true;
+  const unsigned long long l0 = launch_count();
+  bool ok = true;
+  try {
+    issue_step(h, x, T, false);
+  } catch (const StatusError&) {
+    ok = false;
+  }
+  h->capturing = false;
+  cudaError_t e = cudaStreamEndCapture(h->s_comp, &graph);
+  if (!ok || e != cudaSuccess || !graph) {
+    cudaGetLastError();
+    if (graph) cudaGraphDestroy(graph);
+    return false;
+  }
+  e = cudaGraphInstantiateWithFlags(&h->gexec, graph, cudaGraphInstantiateFlagUseNodePriority);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    h->gexec = nullptr;
+    return false;
+  }
+  h->g_x = x;
+  h->g_T = T;
+  h->g_last = h->last;
+  h->g_nwait = h->n_wait;
+  h->g_nprof = h->n_prof;
+  h->g_launches = launch_count() - l0;
+  return true;
+}
+
 static lga_status run_step(lga_handle* h, const float* x, const float* T, double* loss_out, bool host_inputs) {
   if (!h) return ERR(LGA_ERR_INVALID_ARG, "handle is NULL");
   if (h->bad) return ERR(LGA_ERR_BAD_STATE, "handle latched after an earlier CUDA/NCCL error");
@@ -1099,38 +1223,37 @@ static lga_status run_step(lga_handle* h, const float* x, const float* T, double
   if ((need_x && !x) || (need_t && !T)) return ERR(LGA_ERR_INVALID_ARG, "x / target NULL on a stage that reads it");
   ABI_TRY
   CK(cudaSetDevice(h->dev));
-  h->last = lga_comm_stats{};
-  h->n_wait = 0;
-  h->n_prof = 0;
-  h->launches_at_start = launch_count();
   h->t += 1;
   CK(cudaEventRecord(h->ev_t0, h->user));
-  CK(cudaEventRecord(h->ev_in, h->user));
-  CK(cudaStreamWaitEvent(h->s_comp, h->ev_in, 0));
-  CK(cudaStreamWaitEvent(h->s_comm, h->ev_in, 0));
-  const int64_t act = (int64_t)c.N * c.M * c.d;
-  if (host_inputs) {
-    if (need_x) CK(cudaMemcpyAsync(h->xin, x, act * sizeof(float), cudaMemcpyHostToDevice, h->s_comp));
-    if (need_t) CK(cudaMemcpyAsync(h->tin, T, act * sizeof(float), cudaMemcpyHostToDevice, h->s_comp));
-    x = need_x ? h->xin : nullptr;
-    T = need_t ? h->tin : nullptr;
+  // CUDA graph of the whole step: captured at the second device-input call, replayed while the input
+  // pointers stay the same; the first call (lazy initialisation) and host-input calls run eagerly
+  const bool graph_ok = !host_inputs && !c.graph_off && !h->graph_broken && h->eager_steps >= 1;
+  if (graph_ok && h->gexec && (x != h->g_x || T != h->g_T)) {
+    CK(cudaGraphExecDestroy(h->gexec));
+    h->gexec = nullptr;
   }
-  CK(cudaMemsetAsync(h->loss_dev, 0, (c.N + 8) * sizeof(double), h->s_comp));
-  CK(cudaEventRecord(h->ev_fwd_end, h->s_comp));   // re-recorded at the forward/backward boundary (LAYERED)
-  if (c.layered) step_layered(h, x, T);
-  else step_standard(h, x, T);
-  // global loss: sum of this rank's micro-batch losses (slots 1..N), all-reduced, / (D N)
-  mse_finish(h->loss_dev + 1, c.N, 1.0, h->loss_dev, h->s_comp);
-  KCHECK();
-  h->last.allreduce_calls += 1;   // the loss (plus, unpartitioned, the per-layer gradient all-reduces)
-  if (h->world > 1 && !c.no_comm) NK(ncclAllReduce(h->loss_dev, h->loss_dev, 1, ncclFloat64, ncclSum, h->world_comm, h->s_comp));
-  CK(cudaMemcpyAsync(h->loss_host, h->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, h->s_comp));
-  CK(cudaEventRecord(h->ev_comp_end, h->s_comp));
-  CK(cudaEventRecord(h->ev_comm_end, h->s_comm));
-  CK(cudaStreamWaitEvent(h->user, h->ev_comp_end, 0));
-  CK(cudaStreamWaitEvent(h->user, h->ev_comm_end, 0));
+  if (graph_ok && !h->gexec) {
+    CK(cudaEventRecord(h->ev_in, h->user));          // order the capture's stream after the caller
+    CK(cudaStreamWaitEvent(h->s_comp, h->ev_in, 0));
+    if (!capture_step(h, x, T)) h->graph_broken = true;
+  }
+  if (graph_ok && h->gexec) {
+    CK(cudaGraphLaunch(h->gexec, h->user));
+    h->last = h->g_last;
+    h->n_wait = h->g_nwait;
+    h->n_prof = h->g_nprof;
+    h->launches_last = h->g_launches;
+  } else {
+    const unsigned long long l0 = launch_count();
+    CK(cudaEventRecord(h->ev_in, h->user));
+    CK(cudaStreamWaitEvent(h->s_comp, h->ev_in, 0));
+    issue_step(h, x, T, host_inputs);
+    CK(cudaEventRecord(h->ev_comp_end, h->s_comp));
+    CK(cudaStreamWaitEvent(h->user, h->ev_comp_end, 0));
+    h->launches_last = launch_count() - l0;
+    h->eager_steps += 1;
+  }
   CK(cudaEventRecord(h->ev_t1, h->user));
-  h->launches_last = launch_count() - h->launches_at_start;
   h->last.steps = 1;
   lga_comm_stats& tt = h->total;
   tt.steps += 1;
@@ -1164,6 +1287,7 @@ static lga_status gather_state(lga_handle* h, const float* src_shards, float* ou
   if (!out) return ERR(LGA_ERR_INVALID_ARG, "out is NULL");
   ABI_TRY
   CK(cudaSetDevice(h->dev));
+  CK(cudaEventSynchronize(h->ev_t1));   // the last step (a replayed graph runs on the caller's stream)
   CK(cudaStreamSynchronize(h->s_comp));
   CK(cudaStreamSynchronize(h->s_comm));
   float* full = nullptr;
