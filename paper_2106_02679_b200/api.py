@@ -132,6 +132,19 @@ class Trainer:
         check(lib().lga_params(self._h, out.ctypes.data_as(C.c_void_p), out.size, 0))
         return out
 
+    def grads_device(self):
+        """lga_grads into a CUDA fp32 tensor (no host round trip; full-size models)."""
+        import torch
+        out = torch.empty(self._local_count(), dtype=torch.float32, device="cuda")
+        check(lib().lga_grads(self._h, C.c_void_p(out.data_ptr()), out.numel(), 1))
+        return out
+
+    def params_device(self):
+        import torch
+        out = torch.empty(self._local_count(), dtype=torch.float32, device="cuda")
+        check(lib().lga_params(self._h, C.c_void_p(out.data_ptr()), out.numel(), 1))
+        return out
+
     def comm_stats(self):
         last, tot = _abi.lga_comm_stats(), _abi.lga_comm_stats()
         check(lib().lga_comm_bytes(self._h, C.byref(last), C.byref(tot)))
