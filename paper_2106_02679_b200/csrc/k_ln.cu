@@ -8,6 +8,8 @@
 // finisher sums the partials in a fixed order too -- no float atomics, bitwise reproducible.
 #include "kernels.cuh"
 
+#include <algorithm>
+
 namespace lga {
 
 __device__ __forceinline__ float4 ld4(const void* p, DT t, int64_t i) {
@@ -193,9 +195,118 @@ __global__ void __launch_bounds__(256) ln_bwd_block(const float* __restrict__ do
   }
 }
 
+// =============================================================== backward, fused (d = 256 * CPL)
+// dx AND the dgamma / dbeta column partials in one pass over dout and x: warp w owns columns
+// [256 w, 256 w + 256), CPL per lane; a block takes groups of LNF_ROWS rows (grid-stride), holds them in
+// registers, reduces each row's two sums across the 8 warps in a fixed order through shared memory, writes
+// dx, and accumulates dgamma / dbeta for its columns in registers -- one partial per block (fixed grid,
+// fixed row order: bitwise reproducible).
+constexpr int LNF_ROWS = 4;
+static int lnf_grid(int rows) { return std::max(1, std::min((rows + LNF_ROWS - 1) / LNF_ROWS, num_sms() * 2)); }
+
+template <int CPL>
+__global__ void __launch_bounds__(256, 2) ln_bwd_fused(const float* __restrict__ dout, const float* __restrict__ x,
+                                                    const float2* __restrict__ stats, const void* gamma, DT pdt,
+                                                    const float* __restrict__ resid, float* __restrict__ dx,
+                                                    void* dx_e, DT edt, float* __restrict__ partial, int rows, int d) {
+  __shared__ float2 red[LNF_ROWS][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = warp * (32 * CPL) + lane * CPL;
+  float g[CPL], dg[CPL], db[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; k += 4) {
+    const float4 t = ld4(gamma, pdt, c0 + k);
+    g[k] = t.x, g[k + 1] = t.y, g[k + 2] = t.z, g[k + 3] = t.w;
+  }
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) dg[k] = 0.f, db[k] = 0.f;
+  const float inv_d = 1.f / (float)d;
+  for (int r0 = blockIdx.x * LNF_ROWS; r0 < rows; r0 += gridDim.x * LNF_ROWS) {
+    float go[LNF_ROWS][CPL], xc[LNF_ROWS][CPL];
+    float2 sr[LNF_ROWS];
+#pragma unroll
+    for (int rr = 0; rr < LNF_ROWS; ++rr) {
+      const int r = min(r0 + rr, rows - 1);   // past-the-end rows: recomputed, never stored
+      sr[rr] = stats[r];
+      const int64_t base = (int64_t)r * d + c0;
+#pragma unroll
+      for (int k = 0; k < CPL; k += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(dout + base + k);
+        const float4 b = *reinterpret_cast<const float4*>(x + base + k);
+        go[rr][k] = a.x, go[rr][k + 1] = a.y, go[rr][k + 2] = a.z, go[rr][k + 3] = a.w;
+        xc[rr][k] = b.x, xc[rr][k + 1] = b.y, xc[rr][k + 2] = b.z, xc[rr][k + 3] = b.w;
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < LNF_ROWS; ++rr) {
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        xc[rr][k] -= sr[rr].x;   // x - mean
+        const float t = go[rr][k] * g[k];
+        s1 += t;
+        s2 += t * xc[rr][k];
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) red[rr][warp] = make_float2(s1, s2);
+    }
+    __syncthreads();
+    float m1[LNF_ROWS], m2[LNF_ROWS];
+#pragma unroll
+    for (int rr = 0; rr < LNF_ROWS; ++rr) {
+      float a = 0.f, b = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) a += red[rr][w].x, b += red[rr][w].y;   // fixed warp order
+      m1[rr] = a * inv_d;
+      m2[rr] = b * sr[rr].y * inv_d;
+    }
+    __syncthreads();   // red reusable by the next row group
+#pragma unroll
+    for (int rr = 0; rr < LNF_ROWS; ++rr) {
+      const int r = r0 + rr;
+      if (r >= rows) break;
+      const int64_t base = (int64_t)r * d + c0;
+      const float rstd = sr[rr].y;
+#pragma unroll
+      for (int k = 0; k < CPL; k += 4) {
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float xh = xc[rr][k + e] * rstd;
+          v[e] = rstd * (go[rr][k + e] * g[k + e] - m1[rr] - xh * m2[rr]);
+          dg[k + e] += go[rr][k + e] * xh;
+          db[k + e] += go[rr][k + e];
+        }
+        float4 o = make_float4(v[0], v[1], v[2], v[3]);
+        if (resid) {
+          const float4 q = *reinterpret_cast<const float4*>(resid + base + k);
+          o.x += q.x, o.y += q.y, o.z += q.z, o.w += q.w;
+        }
+        *reinterpret_cast<float4*>(dx + base + k) = o;
+        if (dx_e) st4(dx_e, edt, base + k, o);
+      }
+    }
+  }
+  float* pg = partial + (int64_t)blockIdx.x * 2 * d + c0;
+#pragma unroll
+  for (int k = 0; k < CPL; k += 4) {
+    *reinterpret_cast<float4*>(pg + k) = make_float4(dg[k], dg[k + 1], dg[k + 2], dg[k + 3]);
+    *reinterpret_cast<float4*>(pg + d + k) = make_float4(db[k], db[k + 1], db[k + 2], db[k + 3]);
+  }
+}
+
+#ifdef LGA_NO_LN_FUSED
+static bool lnf_ok(int) { return false; }
+#else
+static bool lnf_ok(int d) { return d == 1024 || d == 2048; }   // d = 4096 would spill at 2 blocks / SM
+#endif
+
 // =============================================================== backward: dgamma / dbeta column partials
 constexpr int LN_COL_ROWS = 64;
-int ln_bwd_blocks(int rows) { return (rows + LN_COL_ROWS - 1) / LN_COL_ROWS; }
+int ln_bwd_blocks(int rows, int d) {
+  return lnf_ok(d) ? lnf_grid(rows) : (rows + LN_COL_ROWS - 1) / LN_COL_ROWS;
+}
 
 __global__ void __launch_bounds__(256) ln_col_partial(const float* __restrict__ dout, const float* __restrict__ x,
                                                       const float2* __restrict__ stats, float* __restrict__ partial,
@@ -218,6 +329,14 @@ __global__ void __launch_bounds__(256) ln_col_partial(const float* __restrict__ 
 int ln_bwd(const float* dout, const float* x, const float2* stats, const void* gamma, DT pdt, const float* resid,
            float* dx, void* dx_e, DT edt, float* partial, int rows, int d, cudaStream_t st) {
   if (rows <= 0) return 0;
+  if (lnf_ok(d)) {
+    const int grid = lnf_grid(rows);
+#define LFU(C) note_launch(), ln_bwd_fused<C><<<grid, 256, 0, st>>>(dout, x, stats, gamma, pdt, resid, dx, dx_e, edt, partial, rows, d)
+    if (d == 1024) LFU(4);
+    else LFU(8);
+#undef LFU
+    return grid;
+  }
   bool done = false;
   if (d % 128 == 0 && d <= 4096) {
     const int grid = (rows + 7) / 8;
@@ -239,7 +358,7 @@ int ln_bwd(const float* dout, const float* x, const float2* stats, const void* g
     else if (vpt <= 8) LB(8); else if (vpt <= 16) LB(16); else LB(32);
 #undef LB
   }
-  const int nblk = ln_bwd_blocks(rows);
+  const int nblk = ln_bwd_blocks(rows, d);
   dim3 grid((d + 255) / 256, nblk);
   note_launch(), ln_col_partial<<<grid, 256, 0, st>>>(dout, x, stats, partial, rows, d);
   return nblk;

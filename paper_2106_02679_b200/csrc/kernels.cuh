@@ -82,7 +82,7 @@ void ln_fwd(const float* x, const void* gamma, const void* beta, DT pdt, void* y
 int ln_bwd(const float* dout, const float* x, const float2* stats, const void* gamma, DT pdt,
            const float* resid, float* dx, void* dx_e, DT edt, float* partial, int rows, int d,
            cudaStream_t st);
-int ln_bwd_blocks(int rows);
+int ln_bwd_blocks(int rows, int d);
 
 // ------------------------------------------------------------------ column sums (bias grads)
 // partial[blk][n] = sum over the block's rows of X[r][n]   (fixed row blocks, deterministic)

@@ -297,7 +297,7 @@ static void plan_arena(lga_handle* h) {
   h->dh1 = A.take<float>(T * d);
   h->dsum = A.take<float>((int64_t)c.c * c.b * c.H * c.s);
   const int64_t pcol = (int64_t)colsum_blocks((int)T) * f;
-  const int64_t pln = (int64_t)ln_bwd_blocks((int)T) * 2 * d;
+  const int64_t pln = (int64_t)ln_bwd_blocks((int)T, (int)d) * 2 * d;
   h->partial_floats = std::max(pcol, pln);
   h->partial = A.take<float>(h->partial_floats);
   h->mse_partial = A.take<double>(mse_blocks(act) + 64);
