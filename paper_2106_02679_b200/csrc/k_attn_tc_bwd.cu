@@ -30,10 +30,10 @@ constexpr int NT = (4 + EW_WARPS) * 32;
 #define LGA_BWD_NST_DKV128 4
 #endif
 #ifndef LGA_BWD_NST_DQ64
-#define LGA_BWD_NST_DQ64 8
+#define LGA_BWD_NST_DQ64 4
 #endif
 #ifndef LGA_BWD_NST_DQ128
-#define LGA_BWD_NST_DQ128 5
+#define LGA_BWD_NST_DQ128 2
 #endif
 constexpr float LOG2E = 1.4426950408889634f;
 
@@ -370,22 +370,26 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 // =============================================================================== dQ
-// TMEM: S[2] at 0 / 64, dP[2] at 128 / 192, dQ at 256, dS[2] (bf16 packed, 32 columns) at 384 / 416.
+// One CTA per 128-query tile, 128-key iterations.  S = Q K^T and dP = dO V^T are M=128, N=128 MMAs (operand
+// bandwidth and math balanced; N=64 tiles were bound by shared-memory operand reads), single-buffered in
+// TMEM: all 16 element-wise warps load S(j) / dP(j) first thing and release them, so S(j+1) runs on the
+// tensor pipe while they compute dS(j).  TMEM: S at 0, dP at 128, dQ at 256, dS[2] (bf16 packed, 64
+// columns each) at 384 / 448.  dQ += dS K with A = dS from TMEM, K read MN-major from its K-major tile.
 constexpr int QB2 = 128;  // queries per CTA
-constexpr int KB2 = 64;   // keys per iteration
+constexpr int KB2 = 128;  // keys per iteration
 
 template <int DH>
 struct DqSmem {
   static constexpr int SUB128 = 128 * 128;
-  static constexpr int SUB64 = 64 * 128;
   static constexpr int QT = DH / 64 * SUB128;   // Q (or dO) [128][DH]
-  static constexpr int KT = DH / 64 * SUB64;    // K (or V) [64][DH]
+  static constexpr int KT = DH / 64 * SUB128;   // K (or V) [128][DH]
   static constexpr int Q_OFF = 0;
   static constexpr int G_OFF = Q_OFF + QT;
-  static constexpr int NST = DH == 64 ? LGA_BWD_NST_DQ64 : LGA_BWD_NST_DQ128;   // K / V ring depth
-  static constexpr int K_OFF = G_OFF + QT;      // [NST]
-  static constexpr int V_OFF = K_OFF + NST * KT;  // [NST]
-  static constexpr int BAR_OFF = V_OFF + NST * KT;
+  // K is read by S and by dQ (freed late), V only by dP (freed when S / dP complete): separate rings
+  static constexpr int NK = DH == 64 ? 4 : 3, NV = DH == 64 ? 3 : 2;
+  static constexpr int K_OFF = G_OFF + QT;      // [NK]
+  static constexpr int V_OFF = K_OFF + NK * KT; // [NV]
+  static constexpr int BAR_OFF = V_OFF + NV * KT;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
@@ -397,15 +401,18 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps shared provenance
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
-  constexpr int NST = SM::NST;
+  constexpr int NK = SM::NK, NV = SM::NV;
+  constexpr int EW_ALL = EW_WARPS * 32;
   uint64_t* qg_full = bars + 0;
-  uint64_t* kv_full = bars + 1;             // [NST]
-  uint64_t* kv_empty = kv_full + NST;       // [NST]
-  uint64_t* s_full = kv_empty + NST;        // [2] per group
-  uint64_t* s_empty = s_full + 2;           // [2] (GRP_THREADS)
-  uint64_t* p_full = s_empty + 2;           // [2] (GRP_THREADS)
-  uint64_t* g_done = p_full + 2;            // [2] per dS buffer
-  constexpr int NBAR = 2 * NST + 9;
+  uint64_t* k_full = bars + 1;              // [NK]
+  uint64_t* k_empty = k_full + NK;          // [NK]
+  uint64_t* v_full = k_empty + NK;          // [NV]
+  uint64_t* v_empty = v_full + NV;          // [NV]
+  uint64_t* s_full = v_empty + NV;          // S(j), dP(j) in TMEM
+  uint64_t* s_empty = s_full + 1;           // ... loaded by every element-wise thread (EW_ALL)
+  uint64_t* p_full = s_empty + 1;           // [2] per dS buffer (EW_ALL)
+  uint64_t* g_done = p_full + 2;            // [2] per dS buffer: dQ MMAs done
+  constexpr int NBAR = 2 * NK + 2 * NV + 7;
   static_assert(NBAR * 8 + 4 <= 256, "barrier area");
   static_assert(SM::TOTAL <= 232448, "shared memory");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
@@ -422,7 +429,7 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < NBAR; ++i) {
       const bool ew = (&bars[i] >= s_empty && &bars[i] < g_done);
-      mbar_init(&bars[i], ew ? GRP_THREADS : 1);
+      mbar_init(&bars[i], ew ? EW_ALL : 1);
     }
     mbar_fence_init();
     prefetch_tmap(&tm_q);
@@ -434,10 +441,8 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   fence_after();
   const uint32_t tb = *tmem_slot;
-  auto t_s = [&](int b) { return tb + 64 * b; };
-  auto t_dp = [&](int b) { return tb + 128 + 64 * b; };
-  auto t_ds = [&](int b) { return tb + 384 + 32 * b; };
-  const uint32_t t_dq = tb + 256;
+  const uint32_t t_s = tb, t_dp = tb + 128, t_dq = tb + 256;
+  auto t_ds = [&](int b) { return tb + 384 + 64 * b; };
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer
@@ -448,15 +453,19 @@ __global__ void __launch_bounds__(NT, 1)
         tma_load_3d(smem + SM::G_OFF + c * SM::SUB128, &tm_g, qg_full, h * DH + 64 * c, q0, sq);
       }
       for (int j = 0; j < nk; ++j) {
-        const int st = j % NST;
-        mbar_wait(&kv_empty[st], ((j / NST) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * SM::KT);
+        const int sk = j % NK, sv = j % NV;
+        mbar_wait(&k_empty[sk], ((j / NK) & 1) ^ 1);
+        mbar_expect_tx(&k_full[sk], SM::KT);
 #pragma unroll
-        for (int c = 0; c < DH / 64; ++c) {
-          tma_load_3d(smem + SM::K_OFF + st * SM::KT + c * SM::SUB64, &tm_kv, &kv_full[st], d + h * DH + 64 * c, j * KB2, sq);
-          tma_load_3d(smem + SM::V_OFF + st * SM::KT + c * SM::SUB64, &tm_kv, &kv_full[st], 2 * d + h * DH + 64 * c,
+        for (int c = 0; c < DH / 64; ++c)
+          tma_load_3d(smem + SM::K_OFF + sk * SM::KT + c * SM::SUB128, &tm_kv, &k_full[sk], d + h * DH + 64 * c,
                       j * KB2, sq);
-        }
+        mbar_wait(&v_empty[sv], ((j / NV) & 1) ^ 1);
+        mbar_expect_tx(&v_full[sv], SM::KT);
+#pragma unroll
+        for (int c = 0; c < DH / 64; ++c)
+          tma_load_3d(smem + SM::V_OFF + sv * SM::KT + c * SM::SUB128, &tm_kv, &v_full[sv], 2 * d + h * DH + 64 * c,
+                      j * KB2, sq);
       }
     }
   } else if (warp == 1) {  // ===== MMA issuer (whole warp; one elected lane issues)
@@ -467,45 +476,47 @@ __global__ void __launch_bounds__(NT, 1)
     const uint64_t dG = make_desc(smem_u32(smem + SM::G_OFF), 16, 1024);
     const uint64_t dK = make_desc(smem_u32(smem + SM::K_OFF), 16, 1024);
     const uint64_t dV = make_desc(smem_u32(smem + SM::V_OFF), 16, 1024);
-    const uint64_t dKm = make_desc(smem_u32(smem + SM::K_OFF), SM::SUB64, 1024);   // K, MN-major
+    const uint64_t dKm = make_desc(smem_u32(smem + SM::K_OFF), SM::SUB128, 1024);   // K, MN-major
     mbar_wait(qg_full, 0);
-    for (int j = 0; j < nk + 2; ++j) {
+    // issue order S(0), S(1), dQ(0), S(2), dQ(1), ...: S(j+1) only needs S(j) loaded by the element-wise
+    // warps, dQ(j) needs dS(j)
+    for (int j = 0; j < nk + 1; ++j) {
       if (j < nk) {  // S(j), dP(j)
-        const int st = j % NST, b = j & 1;
-        mbar_wait(&kv_full[st], (j / NST) & 1);
-        mbar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);
+        const int sk = j % NK, sv = j % NV;
+        mbar_wait(&k_full[sk], (j / NK) & 1);
+        mbar_wait(&v_full[sv], (j / NV) & 1);
+        if (j > 0) mbar_wait(s_empty, (j - 1) & 1);
         fence_after();
-        const uint64_t dk = desc_add(dK, st * SM::KT), dv = desc_add(dV, st * SM::KT);
+        const uint64_t dk = desc_add(dK, sk * SM::KT), dv = desc_add(dV, sv * SM::KT);
         if (leader) {
 #pragma unroll
           for (int kk = 0; kk < DH / 16; ++kk) {
-            const uint32_t oa = (kk >> 2) * SM::SUB128 + (kk & 3) * 32, ob = (kk >> 2) * SM::SUB64 + (kk & 3) * 32;
-            umma_f16(t_s(b), desc_add(dQ, oa), desc_add(dk, ob), idesc_s, kk > 0);
-            umma_f16(t_dp(b), desc_add(dG, oa), desc_add(dv, ob), idesc_s, kk > 0);
+            const uint32_t o = (kk >> 2) * SM::SUB128 + (kk & 3) * 32;
+            umma_f16(t_s, desc_add(dQ, o), desc_add(dk, o), idesc_s, kk > 0);
+            umma_f16(t_dp, desc_add(dG, o), desc_add(dv, o), idesc_s, kk > 0);
           }
-          umma_commit(&s_full[b]);
+          umma_commit(s_full);
+          umma_commit(&v_empty[sv]);   // V consumed by dP
         }
         __syncwarp();
       }
-      if (j >= 2) {  // dQ += dS K of iteration j-2 (A = dS from TMEM)
-        const int jj = j - 2, st = jj % NST, pb = jj & 1;
+      if (j >= 1) {  // dQ += dS K of iteration j-1 (A = dS from TMEM)
+        const int jj = j - 1, sk = jj % NK, pb = jj & 1;
         mbar_wait(&p_full[pb], (jj >> 1) & 1);
         fence_after();
-        const uint64_t dk = desc_add(dKm, st * SM::KT);
+        const uint64_t dk = desc_add(dKm, sk * SM::KT);
         if (leader) {
 #pragma unroll
-          for (int kk = 0; kk < KB2 / 16; ++kk)
-            umma_f16_ts(t_dq, t_ds(pb) + 16 * (kk >> 1) + 8 * (kk & 1), desc_add(dk, kk * 16 * 128), idesc_q,
-                        (jj > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < KB2 / 16; ++kk)   // 16 keys = 8 packed dS columns, 16 K rows
+            umma_f16_ts(t_dq, t_ds(pb) + 8 * kk, desc_add(dk, kk * 16 * 128), idesc_q, (jj > 0 || kk > 0) ? 1u : 0u);
           umma_commit(&g_done[pb]);
-          umma_commit(&kv_empty[st]);
+          umma_commit(&k_empty[sk]);
         }
         __syncwarp();
       }
     }
-  } else if (warp >= 4) {  // ===== element-wise: ping-pong groups, one query row per 2 threads of a group
-    const int grp = (warp - 4) >> 3;
-    const int hf = ((warp - 4) >> 2) & 1;       // half (32 columns) of the 64 key columns
+  } else if (warp >= 4) {  // ===== element-wise: one query row per 4 threads, 32 key columns each
+    const int cg = (warp - 4) >> 2;             // key-column group 0..3
     const int qd = warp & 3;
     const int r = qd * 32 + lane;
     const int q = q0 + r;
@@ -514,25 +525,26 @@ __global__ void __launch_bounds__(NT, 1)
     const int64_t rb = ((int64_t)sq * a.heads + h) * s;
     const float lse2 = q < s ? a.lse[rb + q] * LOG2E : 0.f;
     const float Dq = q < s ? a.dsum[rb + q] : 0.f;
-    for (int j = grp; j < nk; j += 2) {
-      const int ka = j * KB2 + hf * 32;
+    for (int j = 0; j < nk; ++j) {
+      const int ka = j * KB2 + cg * 32;
       const bool need_mask = q >= s || ka + 32 > s || (a.causal && ka + 31 > q0 + qd * 32);
-      mbar_wait(&s_full[grp], (j >> 1) & 1);
+      mbar_wait(s_full, j & 1);
       fence_after();
+      uint32_t rsv[2][16], rdp[2][16];
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        tmem_ld16_nowait(t_s + lrow + cg * 32 + ch * 16, rsv[ch]);
+        tmem_ld16_nowait(t_dp + lrow + cg * 32 + ch * 16, rdp[ch]);
+      }
+      tmem_wait_ld();
+      fence_before();
+      mbar_arrive(s_empty);   // S / dP buffer free for S(j+1)
       uint32_t pd[16];
 #pragma unroll
       for (int ch = 0; ch < 2; ++ch) {
-        uint32_t rsv[16], rdp[16];
-        tmem_ld16_nowait(t_s(grp) + lrow + hf * 32 + ch * 16, rsv);
-        tmem_ld16_nowait(t_dp(grp) + lrow + hf * 32 + ch * 16, rdp);
-        tmem_wait_ld();
-        if (ch == 1) {
-          fence_before();
-          mbar_arrive(&s_empty[grp]);
-        }
         float sc[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -lse2);
+        for (int c = 0; c < 16; ++c) sc[c] = fmaf(__uint_as_float(rsv[ch][c]), sl2, -lse2);
         if (need_mask) {
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
@@ -544,24 +556,25 @@ __global__ void __launch_bounds__(NT, 1)
         for (int c = 0; c < 16; c += 2) {
           float g[2];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) g[e] = ex2(sc[c + e]) * (__uint_as_float(rdp[c + e]) - Dq) * a.scale;
+          for (int e = 0; e < 2; ++e) g[e] = ex2(sc[c + e]) * (__uint_as_float(rdp[ch][c + e]) - Dq) * a.scale;
           pd[ch * 8 + c / 2] = pack_bf16x2(g[0], g[1]);
         }
       }
+      const int pb = j & 1;
       if (j >= 2) {
-        mbar_wait(&g_done[grp], ((j >> 1) & 1) ^ 1);   // dQ MMAs of iteration j-2 done: dS buffer free
+        mbar_wait(&g_done[pb], ((j >> 1) & 1) ^ 1);   // dQ MMAs of iteration j-2 done: dS buffer free
         fence_after();
       }
-      tmem_st16_nowait(t_ds(grp) + lrow + hf * 16, pd);
+      tmem_st16_nowait(t_ds(pb) + lrow + cg * 16, pd);
       tmem_wait_st();
       fence_before();
-      mbar_arrive(&p_full[grp]);
+      mbar_arrive(&p_full[pb]);
     }
-    wait_all_done(g_done, grp, nk);
+    mbar_wait(&g_done[(nk - 1) & 1], ((nk - 1) >> 1) & 1);   // the last dQ MMAs (and all before) done
+    fence_after();
     constexpr int OC = DH / 4;
-    const int oq = grp * 2 + hf;
-    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + q) * 3 * d + h * DH + oq * OC;
-    store_row_bf16_global(out, t_dq + lrow + oq * OC, OC, 1.f, q < s);
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + q) * 3 * d + h * DH + cg * OC;
+    store_row_bf16_global(out, t_dq + lrow + cg * OC, OC, 1.f, q < s);
   }
   fence_before();
   __syncthreads();
@@ -575,7 +588,7 @@ template <int DH>
 static cudaError_t run(const AttnArgs& a, cudaStream_t st) {
   const int64_t rows = (int64_t)a.nseq * a.seq * a.heads;
   note_launch(), dsum_kernel<<<(unsigned)((rows * (a.dh / 8) + 255) / 256), 256, 0, st>>>(a);
-  CUtensorMap kv128, q64, g64, q128, g128, kv64;
+  CUtensorMap kv128, q64, g64, q128, g128;
   cudaError_t e;
   const uint64_t ld = 3ull * a.d;
   if ((e = map3d_bf16(&kv128, a.qkv, ld, a.seq, a.nseq, 128)) != cudaSuccess) return e;
@@ -583,7 +596,7 @@ static cudaError_t run(const AttnArgs& a, cudaStream_t st) {
   if ((e = map3d_bf16(&g64, a.dO, a.d, a.seq, a.nseq, 64)) != cudaSuccess) return e;
   if ((e = map3d_bf16(&q128, a.qkv, ld, a.seq, a.nseq, 128)) != cudaSuccess) return e;
   if ((e = map3d_bf16(&g128, a.dO, a.d, a.seq, a.nseq, 128)) != cudaSuccess) return e;
-  if ((e = map3d_bf16(&kv64, a.qkv, ld, a.seq, a.nseq, 64)) != cudaSuccess) return e;
+
   static bool set = false;
   if (!set) {
     if ((e = cudaFuncSetAttribute(dkdv_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvSmem<DH>::TOTAL)))
@@ -595,7 +608,7 @@ static cudaError_t run(const AttnArgs& a, cudaStream_t st) {
   dim3 gk((a.seq + KB - 1) / KB, a.heads, a.nseq);
   note_launch(), dkdv_kernel<DH><<<gk, NT, DkvSmem<DH>::TOTAL, st>>>(kv128, q64, g64, a);
   dim3 gq((a.seq + QB2 - 1) / QB2, a.heads, a.nseq);
-  note_launch(), dq_kernel<DH><<<gq, NT, DqSmem<DH>::TOTAL, st>>>(q128, g128, kv64, a);
+  note_launch(), dq_kernel<DH><<<gq, NT, DqSmem<DH>::TOTAL, st>>>(q128, g128, kv128, a);
   return cudaGetLastError();
 }
 

@@ -1,2 +1,5 @@
 cd $GRAFT_REPO_ROOT
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:ln_bwd -c 4 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e 2>&1 | grep -E "ln_bwd|duration|bytes" | head -16
+timeout 400 python -m pytest tests/test_gpu_kernels.py -q -x -k attention 2>&1 | tail -2
+timeout 60 python tools/kbench.py attn 2>&1 | grep -v "^$"; timeout 60 python tools/kbench.py attn --dh 64 --heads 32 2>&1 | grep "bwd\|tcgen"
+timeout 300 python -m pytest tests/test_gpu_step.py -q -x 2>&1 | tail -2
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"dq_kernel|dkdv_kernel" -c 4 python tools/kbench.py attn 2>&1 | grep -E "dq_k|dkdv_k|duration" | head -8
