@@ -192,6 +192,7 @@ def main():
     ap.add_argument("--unpartitioned", action="store_true", help="N2b: no ZeRO partition, all-reduce per layer")
     ap.add_argument("--no-recompute", action="store_true", help="N2c: keep intermediates, no forward recompute")
     ap.add_argument("--pipeline", default="modular", choices=["modular", "contiguous"], help="N3: stage map")
+    ap.add_argument("--nccl-dp", action="store_true", help="N1 baseline: NCCL all-gather / reduce-scatter")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -223,10 +224,12 @@ def main():
     precision = LGA_FP32 if args.workload == "tiny" else LGA_BF16
     flags = _abi.LGA_FLAG_PROFILE | (_abi.LGA_FLAG_NO_COMM if args.no_comm else 0)
     variant = [n for n, on in (("keep_params", args.keep_params), ("unpartitioned", args.unpartitioned),
-                               ("no_recompute", args.no_recompute), ("contiguous_pp", args.pipeline == "contiguous")) if on]
+                               ("no_recompute", args.no_recompute), ("contiguous_pp", args.pipeline == "contiguous"),
+                               ("nccl_dp", args.nccl_dp)) if on]
     flags |= ((_abi.LGA_FLAG_KEEP_PARAMS if args.keep_params else 0) | (_abi.LGA_FLAG_UNPARTITIONED if args.unpartitioned else 0)
               | (_abi.LGA_FLAG_NO_RECOMPUTE if args.no_recompute else 0)
-              | (_abi.LGA_FLAG_CONTIGUOUS_PP if args.pipeline == "contiguous" else 0))
+              | (_abi.LGA_FLAG_CONTIGUOUS_PP if args.pipeline == "contiguous" else 0)
+              | (_abi.LGA_FLAG_NCCL_DP if args.nccl_dp else 0))
     cfg = Config(dp=dp, pp=pp, precision=precision, chunk=args.chunk,
                  schedule=LGA_LAYERED if args.schedule == "layered" else LGA_STANDARD, flags=flags, **shape)
     tr = Trainer(cfg, rank=rank, world=world, device=local, init_params=None, seed=1234)
@@ -348,7 +351,7 @@ def main():
                    "tokens_per_step": tokens_per_step, "schedule": args.schedule,
                    "chunk": cfg.chunk or ("N" if pp == 1 else 1), "parallelism": f"dp{dp}" + (f"xpp{pp}" if pp > 1 else ""),
                    "l2": f"inputs larger than L2 (x and target {in_bytes / 1e6:.0f} MB each per replica, reused)",
-                   "no_comm": bool(args.no_comm), "variant": variant or "paper default (partitioned, recompute, modular)"},
+                   "no_comm": bool(args.no_comm), "variant": variant or "paper default (partitioned, recompute, modular); DP over NVLink peer memory"},
         "exposed_comm_ms_per_step": prof["comm_wait_ms"] / args.steps,
         "p2p_wait_ms_per_step": prof["p2p_wait_ms"] / args.steps,
         "model_tflops_per_gpu": value * fpt / world / 1e12,

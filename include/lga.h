@@ -94,6 +94,10 @@ typedef enum { LGA_LAYERED = 0, LGA_STANDARD = 1 } lga_schedule;
 #define LGA_FLAG_UNPARTITIONED 0x20u  /* N2b: no training-state partition: every replica holds the full
                                          fp32 master / m / v of its stage's layers and all-reduces each
                                          layer's gradient once per step; no all-gather */
+#define LGA_FLAG_NCCL_DP       0x80u  /* baseline for A/B: data-parallel all-gather / reduce-scatter with NCCL.
+                                         Default (partitioned LAYERED, D > 1): over NVLink peer memory --
+                                         copy-engine all-gathers, reduce-scatter fused into the AdamW kernel
+                                         (fixed rank order), per-layer peer flags */
 #define LGA_FLAG_CONTIGUOUS_PP 0x40u  /* N3: contiguous pipeline map, layer i on stage i / (L/P) (the
                                          standard layout of P:71) instead of the modular i mod P;
                                          activations cross stages only at block boundaries */

@@ -186,6 +186,83 @@ __global__ void __launch_bounds__(256) adamw_kernel(const GE* __restrict__ gin, 
     adamw_one(gin, gscale, master, m, v, pout, keep, i, lr, b1, b2, eps, wd, bc1, bc2);
 }
 
+// Reduce-scatter fused with AdamW over NVLink peer memory: this rank's shard of the layer
+// gradient is the sum, in fixed rank order p = 0..D-1, of the same slice of every data-parallel peer's
+// staging buffer (gbase[p] + goff, read uncached: written by the peer since the last step); then AdamW as
+// above.  n % 4 == 0 (shards are multiples of 64 elements).
+template <typename GE>
+__device__ __forceinline__ void ld4_cv(const GE* p, int64_t i, float (&g)[4]) {
+  if (sizeof(GE) == 4) {
+    float4 t;
+    asm volatile("ld.global.cv.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
+                 : "l"(reinterpret_cast<const float4*>(p) + i));
+    g[0] = t.x, g[1] = t.y, g[2] = t.z, g[3] = t.w;
+  } else {
+    uint32_t a, b;
+    asm volatile("ld.global.cv.v2.u32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "l"(reinterpret_cast<const uint2*>(p) + i));
+    g[0] = __uint_as_float(a << 16), g[1] = __uint_as_float(a & 0xFFFF0000u);
+    g[2] = __uint_as_float(b << 16), g[3] = __uint_as_float(b & 0xFFFF0000u);
+  }
+}
+
+template <typename GE, typename PE>
+__global__ void __launch_bounds__(256) adamw_rs_kernel(const void* const* __restrict__ gbase, int64_t goff, int D,
+                                                       float gscale, float* __restrict__ master, float* __restrict__ m,
+                                                       float* __restrict__ v, PE* __restrict__ pout,
+                                                       float* __restrict__ keep, int64_t n, float lr, float b1,
+                                                       float b2, float eps, float wd, const long long* __restrict__ tstep) {
+  const float t = (float)*tstep;
+  const float bc1 = 1.0f - powf(b1, t), bc2 = 1.0f - powf(b2, t);
+  const int64_t n4 = n / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float g[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int p = 0; p < D; ++p) {   // fixed rank order: bitwise reproducible
+      float q[4];
+      ld4_cv(static_cast<const GE*>(gbase[p]) + goff, i, q);
+      g[0] += q[0], g[1] += q[1], g[2] += q[2], g[3] += q[3];
+    }
+    float4 th = reinterpret_cast<float4*>(master)[i];
+    float4 mi = reinterpret_cast<float4*>(m)[i];
+    float4 vi = reinterpret_cast<float4*>(v)[i];
+    float* thp = &th.x;
+    float* mp = &mi.x;
+    float* vp = &vi.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float gg = g[e] * gscale;
+      g[e] = gg;
+      float tt = thp[e] * (1.0f - lr * wd);
+      mp[e] = b1 * mp[e] + (1.0f - b1) * gg;
+      vp[e] = b2 * vp[e] + (1.0f - b2) * gg * gg;
+      thp[e] = tt - lr * (mp[e] / bc1) / (sqrtf(vp[e] / bc2) + eps);
+    }
+    reinterpret_cast<float4*>(master)[i] = th;
+    reinterpret_cast<float4*>(m)[i] = mi;
+    reinterpret_cast<float4*>(v)[i] = vi;
+    if (sizeof(PE) == 4) {
+      reinterpret_cast<float4*>(pout)[i] = th;
+    } else {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(th.x, th.y), hi = __floats2bfloat162_rn(th.z, th.w);
+      reinterpret_cast<uint2*>(pout)[i] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    }
+    if (keep) reinterpret_cast<float4*>(keep)[i] = make_float4(g[0], g[1], g[2], g[3]);
+  }
+}
+
+void adamw_rs(const void* const* gbase, int64_t goff, int D, DT gdt, float gscale, float* master, float* m, float* v,
+              void* param_out, DT pdt, float* keep, int64_t n, float lr, float beta1, float beta2, float eps, float wd,
+              const long long* tstep, cudaStream_t st) {
+  if (n <= 0) return;
+  const int grid = (int)std::min<int64_t>((n / 4 + 255) / 256 + 1, (int64_t)num_sms() * 8);
+#define AR(GE, PE) note_launch(), adamw_rs_kernel<GE, PE><<<grid, 256, 0, st>>>(gbase, goff, D, gscale, master, m, v, (PE*)param_out, keep, n, lr, beta1, beta2, eps, wd, tstep)
+  if (gdt == DT::F32 && pdt == DT::F32) AR(float, float);
+  else if (gdt == DT::F32) AR(float, __nv_bfloat16);
+  else if (pdt == DT::F32) AR(__nv_bfloat16, float);
+  else AR(__nv_bfloat16, __nv_bfloat16);
+#undef AR
+}
+
 void adamw(const void* gin, DT gdt, float gscale, float* master, float* m, float* v,
            void* param_out, DT pdt, float* keep, int64_t n, float lr, float beta1, float beta2,
            float eps, float wd, const long long* tstep, cudaStream_t st) {
@@ -311,6 +388,17 @@ void set_flag(unsigned long long* flag, const long long* tstep, unsigned long lo
               cudaStream_t st) {
   note_launch(), set_flag_kernel<<<1, 1, 0, st>>>(flag, tstep, per_step, k);
 }
+// counter idx += 1 in every data-parallel peer's flag array (fbase[p], system-scope release after all
+// prior work on the stream): "my gradient of layer j is staged" / "my shard j is updated" / "I read it"
+__global__ void dp_signal_kernel(unsigned long long* const* fbase, int D, int idx) {
+  if ((int)threadIdx.x >= D) return;
+  __threadfence_system();
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(fbase[threadIdx.x] + idx), "l"(1ull) : "memory");
+}
+void dp_signal(unsigned long long* const* fbase, int D, int idx, cudaStream_t st) {
+  note_launch(), dp_signal_kernel<<<1, 32, 0, st>>>(fbase, D, idx);
+}
+
 // the step counter t (AdamW bias corrections, flag epochs): incremented first thing in every step
 __global__ void step_begin_kernel(long long* tstep) { *tstep += 1; }
 void step_begin(long long* tstep, cudaStream_t st) { note_launch(), step_begin_kernel<<<1, 1, 0, st>>>(tstep); }

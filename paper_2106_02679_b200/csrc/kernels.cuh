@@ -127,5 +127,10 @@ void wait_flag(const volatile unsigned long long* flag, const long long* tstep, 
 void set_flag(unsigned long long* flag, const long long* tstep, unsigned long long per_step, unsigned long long k,
               cudaStream_t st);
 void step_begin(long long* tstep, cudaStream_t st);
+// reduce-scatter over peer memory fused with AdamW (gbase: device array of the D peers' staging bases)
+void adamw_rs(const void* const* gbase, int64_t goff, int D, DT gdt, float gscale, float* master, float* m, float* v,
+              void* param_out, DT pdt, float* keep, int64_t n, float lr, float beta1, float beta2, float eps, float wd,
+              const long long* tstep, cudaStream_t st);
+void dp_signal(unsigned long long* const* fbase, int D, int idx, cudaStream_t st);
 
 }  // namespace lga

@@ -72,6 +72,7 @@ struct Cfg {
   bool retain, no_comm, profile;
   bool keep, norecomp, unpart, contig;   // LGA_FLAG_KEEP_PARAMS / NO_RECOMPUTE / UNPARTITIONED / CONTIGUOUS_PP
   bool graph_off;                        // LGA_FLAG_NO_GRAPH
+  bool dp_ipc;                           // DP all-gather / reduce-scatter over NVLink peer memory (not NCCL)
   // canonical offsets
   int64_t o_ln1w, o_ln1b, o_wqkv, o_bqkv, o_wo, o_bo, o_ln2w, o_ln2b, o_w1, o_b1, o_w2, o_b2;
 };
@@ -121,6 +122,8 @@ static lga_status validate(const lga_config* c, int world, Cfg* out) {
   g.norecomp = (c->flags & LGA_FLAG_NO_RECOMPUTE) != 0;
   g.contig = (c->flags & LGA_FLAG_CONTIGUOUS_PP) != 0;
   g.graph_off = (c->flags & LGA_FLAG_NO_GRAPH) != 0;
+  // N1: partitioned LAYERED data parallelism over peer memory unless LGA_FLAG_NCCL_DP asks for NCCL
+  g.dp_ipc = g.D > 1 && g.layered && !g.unpart && !(c->flags & LGA_FLAG_NCCL_DP);
   g.bf16 = c->precision == LGA_BF16;
   g.layered = c->schedule == LGA_LAYERED;
   g.causal = c->causal != 0;
@@ -156,8 +159,9 @@ struct Arena {
 
 struct PeerInfo {
   cudaIpcMemHandle_t handle;
-  uint64_t off_ckpt, off_dY, off_flags;
-  uint64_t pad[5];
+  uint64_t off_ckpt, off_dY, off_flags;   // pipeline
+  uint64_t off_gst, off_psh, off_dpf;     // data parallelism over peer memory (N1)
+  uint64_t pad[2];
 };
 static_assert(sizeof(PeerInfo) % 16 == 0, "PeerInfo size");
 
@@ -185,7 +189,14 @@ struct lga_handle {
   void* pshard = nullptr;
   std::vector<void*> slot;   // gathered full layers: 2 (mixed buffering) or L/P (LGA_FLAG_KEEP_PARAMS)
   float* gacc = nullptr;
-  void* gstage[2] = {nullptr, nullptr};
+  void* gstage[2] = {nullptr, nullptr};   // staging of the reduced-precision layer gradient (alternating layers)
+  void* gst_layers = nullptr;             // dp_ipc: one staging buffer per local layer [Lloc][plpad]
+  // dp_ipc: per-layer counters [3][Lloc] (gradient staged / shard updated / shard read), written by peers
+  unsigned long long* dpf = nullptr;
+  void** dp_gst_dev = nullptr;                   // device [D]: every DP peer's staging base (replica order)
+  unsigned long long** dp_flag_dev = nullptr;    // device [D]: every DP peer's dpf
+  std::vector<char*> dp_base;                    // host: IPC-mapped arena base of every DP peer (self: own)
+  std::vector<char*> dp_psh;                     // host: every DP peer's pshard
   // activations
   float* ckpt = nullptr;  // [Lloc][N][M][d]
   float* yout = nullptr;  // [N][M][d] on the stage owning layer L-1
@@ -267,8 +278,15 @@ static void plan_arena(lga_handle* h) {
   h->slot.assign(nslots, nullptr);
   for (int k = 0; k < nslots; ++k) h->slot[k] = A.take_bytes(c.plpad * e);
   h->gacc = A.take<float>(c.plpad);
-  h->gstage[0] = A.take_bytes(c.plpad * dt_size(c.G));
-  h->gstage[1] = A.take_bytes(c.plpad * dt_size(c.G));
+  if (c.dp_ipc) {   // a layer's staged gradient stays readable by the peers until the next step
+    h->gst_layers = A.take_bytes(Ll * c.plpad * dt_size(c.G));
+    h->dpf = A.take<unsigned long long>(3 * Ll);
+    h->dp_gst_dev = A.take<void*>(c.D);
+    h->dp_flag_dev = A.take<unsigned long long*>(c.D);
+  } else {
+    h->gstage[0] = A.take_bytes(c.plpad * dt_size(c.G));
+    h->gstage[1] = A.take_bytes(c.plpad * dt_size(c.G));
+  }
   const int64_t act = (int64_t)c.N * c.M * d;
   h->ckpt = A.take<float>(Ll * act);
   h->yout = A.take<float>(act);
@@ -363,12 +381,17 @@ struct GradDst {
   void* out;            // fp32 accumulator (not last) or the staging buffer (last)
   DT out_dt;
 };
-static GradDst grad_dst(lga_handle* h, int chunk_idx, int nchunks, int gb, int64_t off) {
+// staging buffer of the gradient of local layer j: per layer (dp_ipc) or alternating
+static void* stage_buf(lga_handle* h, int j) {
+  if (h->gst_layers) return eoff(h->gst_layers, h->c.G, (int64_t)j * h->c.plpad);
+  return h->gstage[j % 2];
+}
+static GradDst grad_dst(lga_handle* h, int chunk_idx, int nchunks, int j, int64_t off) {
   const bool first = chunk_idx == 0, last = chunk_idx == nchunks - 1;
   GradDst r;
   r.acc_in = first ? nullptr : h->gacc + off;
   if (last) {
-    r.out = eoff(h->gstage[gb], h->c.G, off);
+    r.out = eoff(stage_buf(h, j), h->c.G, off);
     r.out_dt = h->c.G;
   } else {
     r.out = h->gacc + off;
@@ -487,7 +510,7 @@ static void bias_grad(lga_handle* h, const void* X, DT xdt, int64_t ldx, int n, 
 // bf16: the GEMMs read dY as bf16 from h->dYe -- cast here unless dYe_ready (the previous layer's LN1
 // backward already wrote it next to its fp32 dX); dx_e_out: also write dX as bf16 there (or nullptr).
 static void layer_bwd(lga_handle* h, const Ws& w, const void* W, const float* x_in, const float* dY, float* dx_out,
-                      int chunk_idx, int nchunks, int gb, cudaStream_t st, bool dYe_ready = false,
+                      int chunk_idx, int nchunks, int jl, cudaStream_t st, bool dYe_ready = false,
                       void* dx_e_out = nullptr) {
   const Cfg& c = h->c;
   const int T = c.c * c.M;
@@ -501,7 +524,7 @@ static void layer_bwd(lga_handle* h, const Ws& w, const void* W, const float* x_
     }
     dYe = h->dYe;
   }
-  auto dst = [&](int64_t off) { return grad_dst(h, chunk_idx, nchunks, gb, off); };
+  auto dst = [&](int64_t off) { return grad_dst(h, chunk_idx, nchunks, jl, off); };
   // ---- FFN2: y = h1 + g W2 + b2
   wgrad(h, w.g, f, dYe, d, f, d, T, dst(c.o_w2), c.o_w2, st);
   bias_grad(h, dY, DT::F32, d, d, T, dst(c.o_b2), st);
@@ -607,12 +630,27 @@ static const void* layer_weights(lga_handle* h, int j, int slot) {
   return eoff(h->pshard, h->c.E, (int64_t)j * h->c.S);   // D == 1 or unpartitioned: the local full layer
 }
 
+enum { DPF_GRAD = 0, DPF_PARAM = 1, DPF_READ = 2 };   // dpf[kind * Lloc + j]
+
 static void all_gather(lga_handle* h, int j, int slot) {
   const Cfg& c = h->c;
   if (h->slot.empty()) return;
   h->last.ag_calls++;
   h->last.ag_bytes += (uint64_t)(c.D - 1) * c.S * dt_size(c.E);
   if (c.no_comm) return;
+  if (c.dp_ipc) {
+    // every replica's AdamW of layer j of the previous step is done (D (t-1) signals), then pull the D
+    // shards over NVLink on the copy engines and tell each owner that its shard j has been read
+    wait_flag(h->dpf + DPF_PARAM * c.Lloc + j, h->tstep, (unsigned long long)c.D, 0ull, h->s_comm);
+    KCHECK();
+    const size_t bytes = (size_t)c.S * dt_size(c.E);
+    for (int p = 0; p < c.D; ++p)
+      CK(cudaMemcpyAsync(eoff(h->slot[slot], c.E, (int64_t)p * c.S), eoff(h->dp_psh[p], c.E, (int64_t)j * c.S), bytes,
+                         cudaMemcpyDeviceToDevice, h->s_comm));
+    dp_signal(h->dp_flag_dev, c.D, DPF_READ * c.Lloc + j, h->s_comm);
+    KCHECK();
+    return;
+  }
   NK(ncclAllGather(eoff(h->pshard, c.E, (int64_t)j * c.S), h->slot[slot], (size_t)c.S, nccl_dt(c.E), h->dp_comm, h->s_comm));
 }
 
@@ -632,9 +670,9 @@ static void adam_layer(lga_handle* h, int j, const void* g, DT gdt) {
 // reduce-scatter of the staged gradient in place (once per layer per step); returns the shard.
 // Unpartitioned (N2b): all-reduce of the whole layer in place instead (scatter-reduce + all-gather,
 // P:565), every replica then updates the full layer.
-static void* reduce_scatter(lga_handle* h, int gb) {
+static void* reduce_scatter(lga_handle* h, int j) {
   const Cfg& c = h->c;
-  void* gs = h->gstage[gb];
+  void* gs = stage_buf(h, j);
   if (c.unpart) {
     if (c.D > 1) {
       h->last.allreduce_calls++;
@@ -651,6 +689,44 @@ static void* reduce_scatter(lga_handle* h, int gb) {
       NK(ncclReduceScatter(gs, shard_g, (size_t)c.S, nccl_dt(c.G), ncclSum, h->dp_comm, h->s_comm));
   }
   return shard_g;
+}
+
+// N1: reduce-scatter fused with AdamW over peer memory.  Announce this rank's staged gradient of layer j to
+// every replica, wait until all D are staged (D t signals) and every replica has read this rank's shard j
+// in this step (R D t; R = all-gathers of a layer per step), then sum the D slices in fixed rank order
+// inside the AdamW kernel, and announce the updated shard.
+static void rs_adam_peer(lga_handle* h, int j) {
+  const Cfg& c = h->c;
+  h->last.rs_calls++;
+  h->last.rs_bytes += (uint64_t)(c.D - 1) * c.S * dt_size(c.G);
+  const unsigned long long D = (unsigned long long)c.D, R = c.keep ? 1ull : 2ull;
+  if (!c.no_comm) {
+    dp_signal(h->dp_flag_dev, c.D, DPF_GRAD * c.Lloc + j, h->s_comm);
+    KCHECK();
+    wait_flag(h->dpf + DPF_GRAD * c.Lloc + j, h->tstep, D, D, h->s_comm);
+    KCHECK();
+    wait_flag(h->dpf + DPF_READ * c.Lloc + j, h->tstep, R * D, R * D, h->s_comm);
+    KCHECK();
+  }
+  const float gscale = 1.0f / ((float)c.D * (float)c.N);   // gradient of the mean loss (A-3)
+  const int64_t off = (int64_t)j * c.S;
+  const int64_t goff = (int64_t)j * c.plpad + (int64_t)h->replica * c.S;
+  const int p = prof_begin(h, h->s_comm);
+  if (c.no_comm)
+    adamw(eoff(stage_buf(h, j), c.G, (int64_t)h->replica * c.S), c.G, gscale, h->master + off, h->mom + off,
+          h->var + off, eoff(h->pshard, c.E, off), c.E, c.retain ? h->gkeep + off : nullptr, c.S, c.lr, c.b1, c.b2,
+          c.eps, c.wd, h->tstep, h->s_comm);
+  else
+    adamw_rs(h->dp_gst_dev, goff, c.D, c.G, gscale, h->master + off, h->mom + off, h->var + off,
+             eoff(h->pshard, c.E, off), c.E, c.retain ? h->gkeep + off : nullptr, c.S, c.lr, c.b1, c.b2, c.eps, c.wd,
+             h->tstep, h->s_comm);
+  KCHECK();
+  const double per = (double)c.D * dt_size(c.G) + 24.0 + (double)dt_size(c.E) + (c.retain ? 4.0 : 0.0);
+  prof_end(h, p, h->s_comm, FAM_ADAM, per * (double)c.S);
+  if (!c.no_comm) {
+    dp_signal(h->dp_flag_dev, c.D, DPF_PARAM * c.Lloc + j, h->s_comm);
+    KCHECK();
+  }
 }
 
 static float* ckpt_ptr(lga_handle* h, int j, int m) {
@@ -793,7 +869,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
       count_wait(h, h->ev_ag[sl], 0);
       count_wait_end(h);
     }
-    if (h->rec_adam[gb]) CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));   // staging buffer gb free again
+    if (!c.dp_ipc && h->rec_adam[gb]) CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));   // staging gb free again
     const void* W = layer_weights(h, j, sl);
     const bool recv = c.P > 1 && i < c.L - 1 && stage_of(c, i + 1) != h->stage;   // dY_i from another stage
     const bool send = c.P > 1 && i > 0 && stage_of(c, i - 1) != h->stage;         // dX_i to another stage
@@ -825,7 +901,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
       if (i == 0) dx = h->dscratch;
       else if (!send) dx = dYc;
       else dx = c.no_comm ? h->dscratch : h->prev_dY + m0 * mb;
-      layer_bwd(h, w, W, xin, dYc, dx, k, nchunks, gb, h->s_comp, dye_ready, dx_e);
+      layer_bwd(h, w, W, xin, dYc, dx, k, nchunks, j, h->s_comp, dye_ready, dx_e);
       h->last.bwd_units += c.c;
       if (send) {
         h->sent_bwd += c.c;
@@ -841,8 +917,12 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
     trace(h, "bwd", i);
     CK(cudaEventRecord(h->ev_grad[gb], h->s_comp));
     CK(cudaStreamWaitEvent(h->s_comm, h->ev_grad[gb], 0));
-    void* shard_g = reduce_scatter(h, gb);
-    adam_layer(h, j, shard_g, c.G);
+    if (c.dp_ipc) {
+      rs_adam_peer(h, j);
+    } else {
+      void* shard_g = reduce_scatter(h, j);
+      adam_layer(h, j, shard_g, c.G);
+    }
     { CK(cudaEventRecord(h->ev_adam[gb], h->s_comm)); h->rec_adam[gb] = true; }
   }
 }
@@ -891,13 +971,13 @@ static void step_standard(lga_handle* h, const float* x, const float* T) {
       float* dYc = act_ptr(h->dY, c, m);
       layer_fwd(h, h->ws[0], W, xin, nullptr, h->s_comp);
       h->last.recompute_units++;
-      layer_bwd(h, h->ws[0], W, xin, dYc, j == 0 ? h->dscratch : dYc, 0, 1, gb, h->s_comp);
+      layer_bwd(h, h->ws[0], W, xin, dYc, j == 0 ? h->dscratch : dYc, 0, 1, j, h->s_comp);
       h->last.bwd_units++;
       { CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp)); h->rec_slot[sl] = 1; }
       CK(cudaEventRecord(h->ev_grad[gb], h->s_comp));
       CK(cudaStreamWaitEvent(h->s_comm, h->ev_grad[gb], 0));
       // reduce-scatter this micro-batch's gradient, accumulate it on the shard (fixed order over m)
-      void* shard_g = reduce_scatter(h, gb);
+      void* shard_g = reduce_scatter(h, j);
       float* acc = h->gshard_acc + (int64_t)j * c.S;
       shard_accumulate(shard_g, c.G, acc, c.S, m == 0, h->s_comm);
       KCHECK();
@@ -973,6 +1053,8 @@ static void free_handle(lga_handle* h) {
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->peer_next_base) cudaIpcCloseMemHandle(h->peer_next_base);
   if (h->peer_prev_base && h->peer_prev_base != h->peer_next_base) cudaIpcCloseMemHandle(h->peer_prev_base);
+  for (char* b : h->dp_base)
+    if (b && b != h->arena.base) cudaIpcCloseMemHandle(b);
   if (h->dp_comm) ncclCommDestroy(h->dp_comm);
   if (h->world_comm) ncclCommDestroy(h->world_comm);
   cudaEvent_t evs[] = {h->ev_in, h->ev_tin, h->ev_grad[0], h->ev_grad[1], h->ev_adam[0], h->ev_adam[1], h->ev_comm_end,
@@ -1087,13 +1169,18 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
     cast_f32(h->master, h->pshard, c.E, Ll * c.S, h->s_comp);
     KCHECK();
   }
-  // pipeline peers: exchange IPC handles over the world communicator
-  if (c.P > 1) {
+  // pipeline / data-parallel peers: exchange IPC handles over the world communicator
+  if (c.P > 1 || c.dp_ipc) {
     PeerInfo me{};
     CK(cudaIpcGetMemHandle(&me.handle, h->arena.base));
     me.off_ckpt = (uint64_t)((char*)h->ckpt - h->arena.base);
     me.off_dY = (uint64_t)((char*)h->dY - h->arena.base);
     me.off_flags = (uint64_t)((char*)h->flags - h->arena.base);
+    if (c.dp_ipc) {
+      me.off_gst = (uint64_t)((char*)h->gst_layers - h->arena.base);
+      me.off_psh = (uint64_t)((char*)h->pshard - h->arena.base);
+      me.off_dpf = (uint64_t)((char*)h->dpf - h->arena.base);
+    }
     PeerInfo* dev_info = nullptr;
     CK(cudaMalloc(&dev_info, sizeof(PeerInfo) * (world + 1)));
     CK(cudaMemcpy(dev_info + world, &me, sizeof(me), cudaMemcpyHostToDevice));
@@ -1102,22 +1189,45 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
     CK(cudaMemcpyAsync(all.data(), dev_info, sizeof(PeerInfo) * world, cudaMemcpyDeviceToHost, h->s_comp));
     CK(cudaStreamSynchronize(h->s_comp));
     CK(cudaFree(dev_info));
-    const int next = h->replica * c.P + (h->stage + 1) % c.P;
-    const int prev = h->replica * c.P + (h->stage + c.P - 1) % c.P;
-    void* pn = nullptr;
-    CK(cudaIpcOpenMemHandle(&pn, all[next].handle, cudaIpcMemLazyEnablePeerAccess));
-    h->peer_next_base = (char*)pn;
-    if (prev == next) {
-      h->peer_prev_base = h->peer_next_base;
-    } else {
-      void* pp = nullptr;
-      CK(cudaIpcOpenMemHandle(&pp, all[prev].handle, cudaIpcMemLazyEnablePeerAccess));
-      h->peer_prev_base = (char*)pp;
+    if (c.P > 1) {
+      const int next = h->replica * c.P + (h->stage + 1) % c.P;
+      const int prev = h->replica * c.P + (h->stage + c.P - 1) % c.P;
+      void* pn = nullptr;
+      CK(cudaIpcOpenMemHandle(&pn, all[next].handle, cudaIpcMemLazyEnablePeerAccess));
+      h->peer_next_base = (char*)pn;
+      if (prev == next) {
+        h->peer_prev_base = h->peer_next_base;
+      } else {
+        void* pp = nullptr;
+        CK(cudaIpcOpenMemHandle(&pp, all[prev].handle, cudaIpcMemLazyEnablePeerAccess));
+        h->peer_prev_base = (char*)pp;
+      }
+      h->next_ckpt = (float*)(h->peer_next_base + all[next].off_ckpt);
+      h->next_flags = (unsigned long long*)(h->peer_next_base + all[next].off_flags);
+      h->prev_dY = (float*)(h->peer_prev_base + all[prev].off_dY);
+      h->prev_flags = (unsigned long long*)(h->peer_prev_base + all[prev].off_flags);
     }
-    h->next_ckpt = (float*)(h->peer_next_base + all[next].off_ckpt);
-    h->next_flags = (unsigned long long*)(h->peer_next_base + all[next].off_flags);
-    h->prev_dY = (float*)(h->peer_prev_base + all[prev].off_dY);
-    h->prev_flags = (unsigned long long*)(h->peer_prev_base + all[prev].off_flags);
+    if (c.dp_ipc) {  // the replicas of this stage, in replica order (self: own arena)
+      h->dp_base.assign(c.D, nullptr);
+      h->dp_psh.assign(c.D, nullptr);
+      std::vector<void*> gst(c.D);
+      std::vector<unsigned long long*> fl(c.D);
+      for (int r = 0; r < c.D; ++r) {
+        const int q = r * c.P + h->stage;
+        char* base = h->arena.base;
+        if (q != rank) {
+          void* pb = nullptr;
+          CK(cudaIpcOpenMemHandle(&pb, all[q].handle, cudaIpcMemLazyEnablePeerAccess));
+          base = (char*)pb;
+        }
+        h->dp_base[r] = base;
+        h->dp_psh[r] = base + all[q].off_psh;
+        gst[r] = base + all[q].off_gst;
+        fl[r] = (unsigned long long*)(base + all[q].off_dpf);
+      }
+      CK(cudaMemcpy(h->dp_gst_dev, gst.data(), c.D * sizeof(void*), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->dp_flag_dev, fl.data(), c.D * sizeof(unsigned long long*), cudaMemcpyHostToDevice));
+    }
   }
   CK(cudaStreamSynchronize(h->s_comp));
   // both "staging buffer free" events start completed

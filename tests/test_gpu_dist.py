@@ -38,7 +38,7 @@ def _launch(tmp_path, sh, precision=0, schedule=0, chunk=0, steps=1, flags=0):
 
 
 # LGA_FLAG_* variant bits (include/lga.h) -> oracle.counters keyword arguments
-KEEP, NORECOMP, UNPART, CONTIG = 0x8, 0x10, 0x20, 0x40
+KEEP, NORECOMP, UNPART, CONTIG, NCCL_DP = 0x8, 0x10, 0x20, 0x40, 0x80
 
 
 def _variant(flags):
@@ -138,3 +138,17 @@ def test_pp2_dp2_fp32_contiguous_unpartitioned(tmp_path):
 def test_pp4_bf16_contiguous_pipeline(tmp_path):
     sh = synth.Shape(layers=8, d=256, heads=2, seq=128, micro_batch=1, n_micro=4, dp=1, pp=4)
     _check(_launch(tmp_path, sh, precision=1, flags=CONTIG), sh, 2e-2, elem=2, flags=CONTIG)
+
+
+# ---- N1: the default data-parallel path is NVLink peer memory (copy-engine all-gathers, reduce-scatter fused
+# into AdamW); LGA_FLAG_NCCL_DP keeps NCCL as the A/B baseline -- both must meet the same bar
+@pytest.mark.parametrize("flags", [NCCL_DP, NCCL_DP | KEEP])
+def test_dp2_fp32_nccl_baseline(tmp_path, flags):
+    sh = synth.Shape(layers=4, d=64, heads=4, seq=32, micro_batch=2, n_micro=4, dp=2)
+    _check(_launch(tmp_path, sh, chunk=2, steps=2, flags=flags), sh, 1e-5, steps=2, flags=flags)
+
+
+def test_dp4_bf16_peer_memory_three_steps(tmp_path):
+    """Peer-memory DP over 3 steps (graph replay from step 2): flags and epochs across steps."""
+    sh = synth.Shape(layers=4, d=256, heads=2, seq=128, micro_batch=1, n_micro=4, dp=4)
+    _check(_launch(tmp_path, sh, precision=1, steps=3), sh, 2e-2, steps=3, elem=2)
