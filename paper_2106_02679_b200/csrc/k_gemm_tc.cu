@@ -187,6 +187,84 @@ __device__ __forceinline__ void epilogue_loop(const GemmArgs& g, const EpiMaps& 
   const uint32_t in_bytes = EPI_TILE * EPI_TILE * (uint32_t)dt_size(in_dt);
   uint32_t ephase = 0;
   int it = 0;
+  if (TMA_EPI && e.kind == EPI_GELU_BWD && dt_size(in_dt) == 2) {
+    // GELU backward: the 2 KB bf16 u box is rewritten in place, so the other half of the 4 KB staging area
+    // takes the next box -- the u load of box k+1 (also the next tile's first box, before its accumulator
+    // is ready) overlaps box k instead of exposing one load latency per box
+    constexpr int CH_PER = BN / 64;
+    auto box = [&](int tt, int cc, int& m0w_, int& n0_) {
+      int mb_, nb_;
+      tile_coords(tt, mb_, nb_);
+      m0w_ = mb_ * tile_m + m_off + q * 32;
+      n0_ = nb_ * BN + cc * 32;
+      return n0_ < g.N && m0w_ < g.M;
+    };
+    auto next_valid = [&](int tt, int cc, int& nt, int& nc) {   // next box of this warp inside the matrix
+      nt = tt, nc = cc;
+      while (true) {
+        if (++nc >= (half + 1) * CH_PER) {
+          nc = half * CH_PER;
+          nt += tstride;
+          if (nt >= num_tiles) return false;
+        }
+        int a, b;
+        if (box(nt, nc, a, b)) return true;
+      }
+    };
+    auto load = [&](int tt, int cc, int b) {
+      int a, n;
+      box(tt, cc, a, n);
+      mbar_expect_tx(&ebar[2 * ew + b], in_bytes);
+      tma_load_2d(sbuf + b * 2048, &em.in, &ebar[2 * ew + b], n, a);
+    };
+    uint32_t phb = 0;   // bit b: phase of buffer b's load barrier
+    int buf = 0;
+    if (lane == 0 && t0 < num_tiles) {
+      int ft = t0, fc = half * CH_PER, a, n;
+      if (box(ft, fc, a, n) || next_valid(t0, fc, ft, fc)) load(ft, fc, 0);
+    }
+    __syncwarp();
+    for (int t = t0; t < num_tiles; t += tstride, ++it) {
+      const int as = it & 1;
+      mbar_wait(&tfull[as], (it >> 1) & 1);
+      fence_after();
+      const uint32_t taddr = tmem_base + as * BN + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int ch = half * CH_PER; ch < (half + 1) * CH_PER; ++ch) {
+        int m0w, n0;
+        if (!box(t, ch, m0w, n0)) continue;   // whole box outside the matrix (warp-uniform)
+        if (lane == 0) {
+          bulk_wait_read0();   // the previous box's store has read the other buffer
+          int nt, nc;
+          if (next_valid(t, ch, nt, nc)) load(nt, nc, buf ^ 1);
+        }
+        __syncwarp();
+        uint32_t raw[32];
+        tmem_ld32_nowait(taddr + ch * 32, raw);
+        tmem_wait_ld();
+        mbar_wait(&ebar[2 * ew + buf], (phb >> buf) & 1u);
+        phb ^= 1u << buf;
+        uint8_t* sb = sbuf + buf * 2048;
+        float u[32], v[32];
+        stage_read_row(sb, in_dt, lane, u);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]) * gelu_grad_fast(u[i]);
+        stage_write_row(sb, e.out_dt, lane, v);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&em.out, sb, n0, m0w);
+          bulk_commit();
+        }
+        buf ^= 1;
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) release(as);
+    }
+    if (lane == 0) bulk_wait0();
+    return;
+  }
   for (int t = t0; t < num_tiles; t += tstride, ++it) {
     int mb, nb;
     tile_coords(t, mb, nb);
@@ -211,8 +289,8 @@ __device__ __forceinline__ void epilogue_loop(const GemmArgs& g, const EpiMaps& 
       if (lane == 0) {
         bulk_wait_read0();
         if (has_in) {
-          mbar_expect_tx(&ebar[ew], in_bytes);
-          tma_load_2d(sbuf, &em.in, &ebar[ew], n0, m0w);
+          mbar_expect_tx(&ebar[2 * ew], in_bytes);
+          tma_load_2d(sbuf, &em.in, &ebar[2 * ew], n0, m0w);
         }
       }
       __syncwarp();
@@ -223,7 +301,7 @@ __device__ __forceinline__ void epilogue_loop(const GemmArgs& g, const EpiMaps& 
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]);
       if (has_in) {
-        mbar_wait(&ebar[ew], ephase);
+        mbar_wait(&ebar[2 * ew], ephase);
         ephase ^= 1;
       }
       if (e.kind == EPI_STORE) {
@@ -289,8 +367,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* ebar = tempty + 2;   // [EPI_WARPS] staging-load barriers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + EPI_WARPS);
+  uint64_t* ebar = tempty + 2;   // [EPI_WARPS][2] staging-load barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 2 * EPI_WARPS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (g.M + BM - 1) / BM, num_n = (g.N + BN - 1) / BN;
@@ -301,7 +379,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS); }
-    for (int s = 0; s < EPI_WARPS; ++s) mbar_init(&ebar[s], 1);
+    for (int s = 0; s < 2 * EPI_WARPS; ++s) mbar_init(&ebar[s], 1);
     mbar_fence_init();
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
@@ -353,8 +431,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ===== MMA issuer (single thread)
+    {  // ===== MMA issuer: the whole warp runs the loop (uniform descriptor math), one elected lane issues
       constexpr uint32_t idesc = make_idesc(BM, BN, A_MN, B_MN);
+      // K-major: advance 16 elements = 32 B inside the swizzle span; MN-major: 16 K-rows = 2048 B
+      constexpr uint32_t KSTEP_A = A_MN ? UMMA_K * 128 : UMMA_K * 2, KSTEP_B = B_MN ? UMMA_K * 128 : UMMA_K * 2;
+      const bool leader = elect_one();
+      const uint64_t ad0 = A_MN ? make_desc(smem_u32(smem), 64 * BK * 2, 1024) : make_desc(smem_u32(smem), 16, 1024);
+      const uint64_t bd0 = B_MN ? make_desc(smem_u32(smem) + SM::A_BYTES, 64 * BK * 2, 1024)
+                                : make_desc(smem_u32(smem) + SM::A_BYTES, 16, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -367,21 +451,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full[stage], phase);
           fence_after();
-          const uint32_t sa = smem_u32(smem + stage * SM::STAGE_BYTES);
-          const uint32_t sb = sa + SM::A_BYTES;
+          const uint64_t ad = desc_add(ad0, stage * SM::STAGE_BYTES), bd = desc_add(bd0, stage * SM::STAGE_BYTES);
+          if (leader) {
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            // K-major: advance 16 elements = 32 B inside the swizzle span; MN-major: 16 K-rows = 2048 B
-            const uint64_t ad = A_MN ? make_desc(sa + k * UMMA_K * 128, 64 * BK * 2, 1024)
-                                     : make_desc(sa + k * UMMA_K * 2, 16, 1024);
-            const uint64_t bd = B_MN ? make_desc(sb + k * UMMA_K * 128, 64 * BK * 2, 1024)
-                                     : make_desc(sb + k * UMMA_K * 2, 16, 1024);
-            umma_f16(dtm, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < BK / UMMA_K; ++k)
+              umma_f16(dtm, desc_add(ad, k * KSTEP_A), desc_add(bd, k * KSTEP_B), idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_commit(&empty[stage]);   // frees the smem slot when these MMAs complete
           }
-          umma_commit(&empty[stage]);   // frees the smem slot when these MMAs complete
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull[as]);        // accumulator ready for the epilogue
+        if (leader) umma_commit(&tfull[as]);   // accumulator ready for the epilogue
+        __syncwarp();
       }
     }
   } else if (warp >= EPI_WARP0) {  // ===== epilogue: TMEM -> registers -> fused epilogue -> global
@@ -428,8 +509,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;                                        // leader: arrivals from both CTAs
-  uint64_t* ebar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + EPI_WARPS);
+  uint64_t* ebar = tempty + 2;                                         // [EPI_WARPS][2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 2 * EPI_WARPS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -442,7 +523,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * EPI_WARPS); }
-    for (int s = 0; s < EPI_WARPS; ++s) mbar_init(&ebar[s], 1);
+    for (int s = 0; s < 2 * EPI_WARPS; ++s) mbar_init(&ebar[s], 1);
     mbar_fence_init();
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
@@ -495,8 +576,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {  // ===== MMA issuer (leader CTA only)
+    if (rank == 0) {  // ===== MMA issuer (leader CTA only; whole warp, one elected lane issues)
       constexpr uint32_t idesc = make_idesc(2 * BM, PAIR_N, A_MN, B_MN);
+      constexpr uint32_t KSTEP_A = A_MN ? UMMA_K * 128 : UMMA_K * 2, KSTEP_B = B_MN ? UMMA_K * 128 : UMMA_K * 2;
+      const bool leader = elect_one();
+      const uint64_t ad0 = A_MN ? make_desc(smem_u32(smem), 64 * BK * 2, 1024) : make_desc(smem_u32(smem), 16, 1024);
+      const uint64_t bd0 = B_MN ? make_desc(smem_u32(smem) + SM::A_BYTES, 64 * BK * 2, 1024)
+                                : make_desc(smem_u32(smem) + SM::A_BYTES, 16, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -509,20 +595,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full[stage], phase);
           fence_after();
-          const uint32_t sa = smem_u32(smem + stage * SM::STAGE_BYTES);
-          const uint32_t sb = sa + SM::A_BYTES;
+          const uint64_t ad = desc_add(ad0, stage * SM::STAGE_BYTES), bd = desc_add(bd0, stage * SM::STAGE_BYTES);
+          if (leader) {
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            const uint64_t ad = A_MN ? make_desc(sa + k * UMMA_K * 128, 64 * BK * 2, 1024)
-                                     : make_desc(sa + k * UMMA_K * 2, 16, 1024);
-            const uint64_t bd = B_MN ? make_desc(sb + k * UMMA_K * 128, 64 * BK * 2, 1024)
-                                     : make_desc(sb + k * UMMA_K * 2, 16, 1024);
-            umma_f16_cg2(dtm, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < BK / UMMA_K; ++k)
+              umma_f16_cg2(dtm, desc_add(ad, k * KSTEP_A), desc_add(bd, k * KSTEP_B), idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_commit_cg2_mc(&empty[stage], 0x3);   // frees this smem slot in both CTAs
           }
-          umma_commit_cg2_mc(&empty[stage], 0x3);   // frees this smem slot in both CTAs
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit_cg2_mc(&tfull[as], 0x3);        // accumulator ready in both CTAs
+        if (leader) umma_commit_cg2_mc(&tfull[as], 0x3);        // accumulator ready in both CTAs
+        __syncwarp();
       }
     }
   } else if (warp >= EPI_WARP0) {  // ===== epilogue (both CTAs, each its own 128 rows)
