@@ -746,11 +746,19 @@ cudaError_t gemm_bf16_tc(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return cudaSuccess;
   if (g.K <= 0) return cudaErrorInvalidValue;
   const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
-  // BN = 256 when there are enough tiles to fill the machine, else 128
+  // Kernel choice by a wave-count cost model: per-SM work of one wave (pair tile: 128 x 256 per SM) times
+  // the number of waves, over the kernel's relative per-SM throughput (CTA pair 1.0, single-CTA 128 x 256
+  // 0.85, 128 x 128 0.70 -- measured kbench ratios).  A pair wave that leaves SMs idle can still beat a
+  // second, partly empty wave of smaller tiles (the O-projection weight gradient: 64 pair tiles).
+  const int ns = num_sms();
   const int tiles256 = ((g.M + 127) / 128) * ((g.N + 255) / 256);
-  const bool wide = g.N > 128 && tiles256 >= num_sms();
+  const int tiles128 = ((g.M + 127) / 128) * ((g.N + 127) / 128);
   const int pair_tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256);
-  if (gemm_mode() == 1 && g.N > 128 && pair_tiles >= num_sms() / 2)
+  const double c_pair = (double)((pair_tiles + ns / 2 - 1) / (ns / 2)) * 2.0 / 1.0;
+  const double c_256 = (double)((tiles256 + ns - 1) / ns) * 2.0 / 0.85;
+  const double c_128 = (double)((tiles128 + ns - 1) / ns) * 1.0 / 0.70;
+  const bool wide = g.N > 128 && c_256 < c_128;
+  if (gemm_mode() == 1 && g.N > 128 && c_pair <= std::min(c_256, c_128))
     return amn ? (bmn ? tc::launch2<true, true>(g, st) : tc::launch2<true, false>(g, st))
                : (bmn ? tc::launch2<false, true>(g, st) : tc::launch2<false, false>(g, st));
 #define L(BN) (amn ? (bmn ? tc::launch<BN, true, true>(g, st) : tc::launch<BN, true, false>(g, st)) \
