@@ -87,12 +87,17 @@ __device__ __forceinline__ void store_row_bf16_global(__nv_bfloat16* dst, uint32
 
 #ifdef LGA_BWD_TRACE
 // Timing-only instrumentation (development builds): SM clock64() at pipeline events of the 16 dK/dV CTAs
-// of (sequence 0, head 0): [kt][i][event], row 39 = CTA start / K,V landed / end.
+// of (sequence 0, head 0): [kt][i][event], row 39 = CTA start / K,V landed / end; dQ kernel: CTA 0 of
+// (sequence 0, head 0) into g_dq_trace[j][event].
 __device__ long long g_bwd_trace[16][40][8];
+__device__ long long g_dq_trace[40][8];
 #define BTR(i, k) \
   if (blockIdx.y == 0 && blockIdx.z == 0 && blockIdx.x < 16) g_bwd_trace[blockIdx.x][i][k] = clock64()
+#define QTR(j, k) \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 40) g_dq_trace[j][k] = clock64()
 #else
 #define BTR(i, k)
+#define QTR(j, k)
 #endif
 
 // 4-byte cp.async global -> shared (zero-filled when !valid) and its completion arriving on an mbarrier
@@ -484,8 +489,10 @@ __global__ void __launch_bounds__(NT, 1)
       if (j < nk) {  // S(j), dP(j)
         const int sk = j % NK, sv = j % NV;
         mbar_wait(&k_full[sk], (j / NK) & 1);
+        QTR(j, 0);
         mbar_wait(&v_full[sv], (j / NV) & 1);
         if (j > 0) mbar_wait(s_empty, (j - 1) & 1);
+        QTR(j, 1);
         fence_after();
         const uint64_t dk = desc_add(dK, sk * SM::KT), dv = desc_add(dV, sv * SM::KT);
         if (leader) {
@@ -503,6 +510,7 @@ __global__ void __launch_bounds__(NT, 1)
       if (j >= 1) {  // dQ += dS K of iteration j-1 (A = dS from TMEM)
         const int jj = j - 1, sk = jj % NK, pb = jj & 1;
         mbar_wait(&p_full[pb], (jj >> 1) & 1);
+        QTR(jj, 2);
         fence_after();
         const uint64_t dk = desc_add(dKm, sk * SM::KT);
         if (leader) {
@@ -529,6 +537,7 @@ __global__ void __launch_bounds__(NT, 1)
       const int ka = j * KB2 + cg * 32;
       const bool need_mask = q >= s || ka + 32 > s || (a.causal && ka + 31 > q0 + qd * 32);
       mbar_wait(s_full, j & 1);
+      if (warp == 4 && lane == 0) QTR(j, 3);
       fence_after();
       uint32_t rsv[2][16], rdp[2][16];
 #pragma unroll
@@ -537,6 +546,7 @@ __global__ void __launch_bounds__(NT, 1)
         tmem_ld16_nowait(t_dp + lrow + cg * 32 + ch * 16, rdp[ch]);
       }
       tmem_wait_ld();
+      if (warp == 4 && lane == 0) QTR(j, 4);
       fence_before();
       mbar_arrive(s_empty);   // S / dP buffer free for S(j+1)
       uint32_t pd[16];
@@ -567,6 +577,8 @@ __global__ void __launch_bounds__(NT, 1)
       }
       tmem_st16_nowait(t_ds(pb) + lrow + cg * 16, pd);
       tmem_wait_st();
+      if (warp == 4 && lane == 0) QTR(j, 5);
+      if (warp == 19 && lane == 0) QTR(j, 6);
       fence_before();
       mbar_arrive(&p_full[pb]);
     }
@@ -617,6 +629,9 @@ static cudaError_t run(const AttnArgs& a, cudaStream_t st) {
 #ifdef LGA_BWD_TRACE
 extern "C" int lgatest_bwd_trace(long long* out) {
   return (int)cudaMemcpyFromSymbol(out, fatb::g_bwd_trace, sizeof(fatb::g_bwd_trace));
+}
+extern "C" int lgatest_dq_trace(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, fatb::g_dq_trace, sizeof(fatb::g_dq_trace));
 }
 #endif
 

@@ -50,3 +50,17 @@ for kt in kts:
         it = (r[0] - prev) if prev is not None else 0
         prev = r[0]
         print(f"  {i:2d} {r[3]:10d} {r[4]:10d} {r[5]:10d} {r[0]:12d} {r[2] if r[2] > 0 else 0:10d} | {ew:6d} {lat:6d} {it:6d}")
+
+# dQ kernel: CTA 0 of (sequence 0, head 0) -- the heaviest query tile (16 key tiles)
+if hasattr(L, "lgatest_dq_trace"):
+    qb = np.zeros((40, 8), dtype=np.int64)
+    L.lgatest_dq_trace.argtypes = [C.c_void_p]
+    assert L.lgatest_dq_trace(qb.ctypes.data) == 0
+    t0 = qb[0, 0]
+    print("dQ: j  K seen  S issue  |  EW: S seen  S loaded  P arrive(w4)  P arrive(w19) | p_full(MMA)  | EW dur  iter")
+    prev = None
+    for j in range(16):
+        r = qb[j] - t0
+        it = r[1] - prev if prev is not None else 0
+        prev = r[1]
+        print(f"  {j:2d} {r[0]:8d} {r[1]:8d} | {r[3]:8d} {r[4]:8d} {r[5]:8d} {r[6]:8d} | {r[2]:8d} | {r[5] - r[3]:6d} {it:5d}")
