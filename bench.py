@@ -263,6 +263,7 @@ def main():
             clocks.start()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        step_ms = []   # per-step device time (library events on the caller stream), for median / p90
         prof = dict(gemm_ms=0.0, gemm_flop=0.0, gemm_launches=0, attn_ms=0.0, attn_flop=0.0, adam_ms=0.0,
                     adam_bytes=0.0, comm_wait_ms=0.0, p2p_wait_ms=0.0, launches=0)
         e0.record(stream)
@@ -273,6 +274,7 @@ def main():
                       "comm_wait_ms", "p2p_wait_ms"):
                 prof[k] += t[k]
             prof["launches"] += int(t["kernel_launches"])
+            step_ms.append(float(t["step_ms"]))
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -352,6 +354,8 @@ def main():
                    "chunk": cfg.chunk or ("N" if pp == 1 else 1), "parallelism": f"dp{dp}" + (f"xpp{pp}" if pp > 1 else ""),
                    "l2": f"inputs larger than L2 (x and target {in_bytes / 1e6:.0f} MB each per replica, reused)",
                    "no_comm": bool(args.no_comm), "variant": variant or "paper default (partitioned, recompute, modular); DP over NVLink peer memory"},
+        "step_ms_median": statistics.median(step_ms) if step_ms else None,
+        "step_ms_p90": sorted(step_ms)[min(len(step_ms) - 1, int(0.9 * len(step_ms)))] if step_ms else None,
         "exposed_comm_ms_per_step": prof["comm_wait_ms"] / args.steps,
         "p2p_wait_ms_per_step": prof["p2p_wait_ms"] / args.steps,
         "model_tflops_per_gpu": value * fpt / world / 1e12,
