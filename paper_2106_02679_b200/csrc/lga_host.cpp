@@ -182,6 +182,8 @@ struct lga_handle {
   bool bad = false;
   cudaStream_t user = nullptr, s_comp = nullptr, s_comm = nullptr, s_copy = nullptr;
   bool tin_pending = false;   // lga_step_host: the target copy (on s_copy) not yet awaited by the loss
+  bool x_split = false;       // lga_step_host: x copied per micro-batch on s_copy (ev_x[m]); layer 0 follows
+  std::vector<cudaEvent_t> ev_x;
   ncclComm_t world_comm = nullptr, dp_comm = nullptr;
   Arena arena;
   // training state, per local layer j: [Lloc][S]
@@ -419,9 +421,12 @@ static void trace(lga_handle* h, const char* what, int64_t layer) {
 // ------------------------------------------------------------------ layer executor
 // Forward of local layer j over micro-batches [m0, m0+c) (module docstring of kernels.cuh).
 // x_in: [c][M][d] fp32; y_out: fp32 destination or nullptr (recompute: FFN2 not needed).
-static void layer_fwd(lga_handle* h, const Ws& w, const void* W, const float* x_in, float* y_out, cudaStream_t st) {
+// cc: micro-batches in this launch (default the configured chunk c)
+static void layer_fwd(lga_handle* h, const Ws& w, const void* W, const float* x_in, float* y_out, cudaStream_t st,
+                      int cc = -1) {
   const Cfg& c = h->c;
-  const int T = c.c * c.M;
+  if (cc < 0) cc = c.c;
+  const int T = cc * c.M;
   const int d = c.d;
   const DT E = c.E;
   ln_fwd(x_in, eoff((void*)W, E, c.o_ln1w), eoff((void*)W, E, c.o_ln1b), E, w.a, E, w.st1, T, d, c.ln_eps, st);
@@ -438,7 +443,7 @@ static void layer_fwd(lga_handle* h, const Ws& w, const void* W, const float* x_
   }
   {  // o = attention(q, k, v)
     AttnArgs a;
-    a.nseq = c.c * c.b; a.seq = c.s; a.heads = c.H; a.dh = c.dh; a.d = d; a.causal = c.causal;
+    a.nseq = cc * c.b; a.seq = c.s; a.heads = c.H; a.dh = c.dh; a.d = d; a.causal = c.causal;
     a.scale = 1.0f / sqrtf((float)c.dh);
     a.qkv = w.qkv; a.o = w.o; a.lse = w.lse;
     const int p = prof_begin(h, st);
@@ -796,17 +801,20 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
     const void* W = layer_weights(h, j, sl);
     const bool recv = c.P > 1 && i > 0 && stage_of(c, i - 1) != h->stage;        // x_i from another stage
     const bool send = c.P > 1 && i < c.L - 1 && stage_of(c, i + 1) != h->stage;  // x_{i+1} to another stage
-    for (int k = 0; k < nchunks; ++k) {
-      const int m0 = k * c.c;
+    const bool split0 = i == 0 && h->x_split;        // one micro-batch per launch, each after its copy
+    const int cw = split0 ? 1 : c.c, nch = split0 ? c.N : nchunks;
+    for (int k = 0; k < nch; ++k) {
+      const int m0 = k * cw;
       const float* xin;
       if (i == 0) {
         xin = x + m0 * mb;   // layer 0 input is the caller's x (no copy)
+        if (split0) CK(cudaStreamWaitEvent(h->s_comp, h->ev_x[k], 0));
       } else {
         xin = ckpt_ptr(h, j, m0);
         if (recv) {  // pipeline receive: x_i[m0..m0+c) written by the previous stage
-          h->recv_fwd += c.c;
-          h->last.p2p_recv_calls += c.c;
-          h->last.p2p_recv_bytes += (uint64_t)c.c * mb * 4;
+          h->recv_fwd += cw;
+          h->last.p2p_recv_calls += cw;
+          h->last.p2p_recv_bytes += (uint64_t)cw * mb * 4;
           if (!c.no_comm) {
             count_wait(h, nullptr, 1);
             wait_flag(h->flags + 0, h->tstep, h->k_recv_fwd, h->recv_fwd, h->s_comp);
@@ -824,19 +832,19 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
         const int jn = local_index(c, i + 1);
         yo = c.no_comm ? h->dscratch : h->next_ckpt + ((int64_t)jn * c.N + m0) * mb;
       }
-      layer_fwd(h, chunk_ws(h, j, m0), W, xin, yo, h->s_comp);
-      h->last.fwd_units += c.c;
+      layer_fwd(h, chunk_ws(h, j, m0), W, xin, yo, h->s_comp, cw);
+      h->last.fwd_units += cw;
       if (send) {
-        h->sent_fwd += c.c;
-        h->last.p2p_send_calls += c.c;
-        h->last.p2p_send_bytes += (uint64_t)c.c * mb * 4;
+        h->sent_fwd += cw;
+        h->last.p2p_send_calls += cw;
+        h->last.p2p_send_bytes += (uint64_t)cw * mb * 4;
         if (!c.no_comm) {
           set_flag(h->next_flags + 0, h->tstep, h->k_send_fwd, h->sent_fwd, h->s_comp);
           KCHECK();
         }
       }
       if (i == c.L - 1) {  // loss of this chunk + seed gradient
-        const int64_t n = (int64_t)c.c * mb;
+        const int64_t n = (int64_t)cw * mb;
         await_target(h);
         mse_fwd_bwd(act_ptr(h->yout, c, m0), T + m0 * mb, act_ptr(h->dY, c, m0), h->mse_partial + 0, n,
                     1.0f / (float)mb, h->s_comp);
@@ -1063,6 +1071,8 @@ static void free_handle(lga_handle* h) {
     if (e) cudaEventDestroy(e);
   for (auto e : h->ev_ag)
     if (e) cudaEventDestroy(e);
+  for (auto e : h->ev_x)
+    if (e) cudaEventDestroy(e);
   for (auto e : h->ev_slot_free)
     if (e) cudaEventDestroy(e);
   for (auto e : h->ev_wait0) cudaEventDestroy(e);
@@ -1110,6 +1120,8 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
     CK(cudaEventCreateWithFlags(&h->ev_slot_free[k], cudaEventDisableTiming));
   }
   h->rec_slot.assign(nev, 0);
+  h->ev_x.assign(c.N, nullptr);
+  for (auto& e : h->ev_x) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // pipeline transfers per step on this stage (flag epochs): chunks of every layer boundary it crosses
   for (int j = 0; j < c.Lloc && c.P > 1; ++j) {
     const int64_t i = local_to_global(h, j);
@@ -1253,6 +1265,7 @@ static void issue_step(lga_handle* h, const float* x, const float* T, bool host_
   h->n_wait = 0;
   h->n_prof = 0;
   h->sent_fwd = h->sent_bwd = h->recv_fwd = h->recv_bwd = 0;
+  h->x_split = false;
   h->rec_adam[0] = h->rec_adam[1] = false;
   std::fill(h->rec_slot.begin(), h->rec_slot.end(), 0);
   step_begin(h->tstep, h->s_comp);   // t += 1 before anything reads it
@@ -1261,9 +1274,20 @@ static void issue_step(lga_handle* h, const float* x, const float* T, bool host_
   CK(cudaStreamWaitEvent(h->s_comm, h->ev_in, 0));
   const int64_t act = (int64_t)c.N * c.M * c.d;
   if (host_inputs) {
-    if (need_x) CK(cudaMemcpyAsync(h->xin, x, act * sizeof(float), cudaMemcpyHostToDevice, h->s_comp));
-    if (need_t) {  // needed only at the loss: copy on s_copy, overlapped with the forward
+    if (need_x && c.layered) {   // per micro-batch on s_copy: layer 0 starts on the first one (forward rows are
+                                 // independent, so the per-micro-batch layer-0 launches give the same bits)
       CK(cudaStreamWaitEvent(h->s_copy, h->ev_in, 0));
+      const int64_t mb = (int64_t)c.M * c.d;
+      for (int m = 0; m < c.N; ++m) {
+        CK(cudaMemcpyAsync(h->xin + m * mb, x + m * mb, mb * sizeof(float), cudaMemcpyHostToDevice, h->s_copy));
+        CK(cudaEventRecord(h->ev_x[m], h->s_copy));
+      }
+      h->x_split = true;
+    } else if (need_x) {
+      CK(cudaMemcpyAsync(h->xin, x, act * sizeof(float), cudaMemcpyHostToDevice, h->s_comp));
+    }
+    if (need_t) {  // needed only at the loss: copy on s_copy, overlapped with the forward
+      if (!h->x_split) CK(cudaStreamWaitEvent(h->s_copy, h->ev_in, 0));
       CK(cudaMemcpyAsync(h->tin, T, act * sizeof(float), cudaMemcpyHostToDevice, h->s_copy));
       CK(cudaEventRecord(h->ev_tin, h->s_copy));
       h->tin_pending = true;

@@ -200,3 +200,27 @@ def test_bf16_d1024_parity():
     sh = synth.Shape(layers=2, d=1024, heads=8, seq=130, micro_batch=1, n_micro=2)
     out, (rp, rl, rg, _) = _run(sh, precision=LGA_BF16)
     assert rel(out["grads"], rg) < 2e-2 and rel(out["params"], rp) < 2e-2
+
+
+@pytest.mark.parametrize("precision", [LGA_FP32, LGA_BF16])
+def test_step_host_equals_step(precision):
+    """lga_step_host (x copied per micro-batch, layer 0 launched per micro-batch as each copy lands, target
+    copied on the side) computes exactly what lga_step computes from device inputs."""
+    sh = C1 if precision == LGA_FP32 else synth.Shape(layers=2, d=256, heads=2, seq=128, micro_batch=1, n_micro=4)
+    init = synth.init_params(sh, style="parity")
+    outs = []
+    for host in (False, True):
+        cfg = Config(layers=sh.layers, d_model=sh.d, heads=sh.heads, seq_len=sh.seq, micro_batch=sh.micro_batch,
+                     n_micro=sh.n_micro, precision=precision, lr=1e-3, retain_grads=1)
+        tr = Trainer(cfg, rank=0, world=1, device=0, init_params=init)
+        losses = []
+        for k in range(2):
+            X, T = synth.batch(sh, step=k)
+            if host:
+                losses.append(tr.step_host(np.ascontiguousarray(X[0]), np.ascontiguousarray(T[0])))
+            else:
+                losses.append(tr.step(torch.from_numpy(X[0]).cuda(), torch.from_numpy(T[0]).cuda()))
+        outs.append((tr.params(), losses, tr.comm_stats()[0]))
+        tr.close()
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1] and outs[0][2] == outs[1][2]
