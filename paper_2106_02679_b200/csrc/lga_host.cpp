@@ -941,14 +941,29 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
 static void step_standard(lga_handle* h, const float* x, const float* T) {
   const Cfg& c = h->c;
   const int64_t mb = (int64_t)c.M * c.d;
+  // the layer used by each successive compute pass: per micro-batch, layers ascending then descending.  The
+  // all-gather of use u+1 is prefetched into the other slot while use u computes (as in LAYERED: the
+  // comparison schedule gets the same overlap; only its N-fold volume differs)
+  std::vector<int> uses;
+  uses.reserve((size_t)2 * c.N * c.L);
+  for (int m = 0; m < c.N; ++m) {
+    for (int j = 0; j < c.L; ++j) uses.push_back(j);
+    for (int j = c.L - 1; j >= 0; --j) uses.push_back(j);
+  }
+  auto gather = [&](int u) {
+    if (c.D <= 1 || u >= (int)uses.size()) return;
+    const int sl = u % 2;
+    if (h->rec_slot[sl]) CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[sl], 0));
+    all_gather(h, uses[u], sl);
+    CK(cudaEventRecord(h->ev_ag[sl], h->s_comm));
+  };
+  gather(0);
   int agk = 0;
   for (int m = 0; m < c.N; ++m) {
     for (int j = 0; j < c.L; ++j, ++agk) {
       const int sl = agk % 2;
+      gather(agk + 1);
       if (c.D > 1) {
-        if (h->rec_slot[sl]) CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[sl], 0));
-        all_gather(h, j, sl);
-        CK(cudaEventRecord(h->ev_ag[sl], h->s_comm));
         count_wait(h, h->ev_ag[sl], 0);
         count_wait_end(h);
       }
@@ -966,10 +981,8 @@ static void step_standard(lga_handle* h, const float* x, const float* T) {
     for (int j = c.L - 1; j >= 0; --j, ++agk) {
       const int sl = agk % 2;
       const int gb = j % 2;
+      gather(agk + 1);
       if (c.D > 1) {
-        if (h->rec_slot[sl]) CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[sl], 0));
-        all_gather(h, j, sl);
-        CK(cudaEventRecord(h->ev_ag[sl], h->s_comm));
         count_wait(h, h->ev_ag[sl], 0);
         count_wait_end(h);
       }
