@@ -43,6 +43,10 @@ WORKLOADS = {
               dict(layers=12, d_model=768, heads=12, seq_len=1024, micro_batch=4, n_micro=8), 1),
     "10b": ("~10B L=48 d=4096 32 heads s=2048, b=1 x N=32, modular pipeline P=4 x data-parallel D",
             dict(layers=48, d_model=4096, heads=32, seq_len=2048, micro_batch=1, n_micro=32), 4),
+    # N4: the paper's own encoder family X_[x] (d_a = x/2 heads, d_h = 2x, d_l = x, d_s = 16x, d_m = x^2;
+    # P:444-452), bidirectional attention; pre-LN as everywhere (reading A-1)
+    "x32": ("X_32 encoder L=32 d=1024 16 heads s=512 non-causal, b=8 x N=8 per replica",
+            dict(layers=32, d_model=1024, heads=16, seq_len=512, micro_batch=8, n_micro=8, causal=0), 1),
     "tiny": ("tiny L=2 d=64 4 heads s=32, b=2 x N=4 (fp32)",
              dict(layers=2, d_model=64, heads=4, seq_len=32, micro_batch=2, n_micro=4), 1),
 }
@@ -124,7 +128,7 @@ def oracle_sample_seconds(shape: dict, repeats: int = 1):
                      micro_batch=shape["micro_batch"], n_micro=1)
     flat = synth.init_params(sh, style="train").astype(np.float64)
     X, T = synth.batch(sh, step=0)
-    cfg = om.LayerCfg(d=sh.d, heads=sh.heads, causal=True)
+    cfg = om.LayerCfg(d=sh.d, heads=sh.heads, causal=bool(shape.get("causal", 1)))
     try:
         from threadpoolctl import threadpool_info
         threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
