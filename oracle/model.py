@@ -26,6 +26,11 @@ The layer (per sequence x in R^{s x d}) -- O3 of SURVEY.md section 8(c):
     c  = LN(h1; g2, b2)
     u  = c W1 + b1 ;  g = u Phi(u)
     y  = h1 + g W2 + b2
+
+Post-LN option (``LayerCfg.post_ln``, reading A-16): the original transformer encoder that P:150
+follows ("following the original approach [Vaswani et al.]") normalises after each residual add,
+with the same parameters:
+    h1 = LN(x + Attn(x) Wo + bo; g1, b1) ;  y = LN(h1 + GELU(h1 W1 + b1) W2 + b2; g2, b2)
 """
 
 from __future__ import annotations
@@ -79,6 +84,7 @@ class LayerCfg:
     causal: bool = True
     ffn_mult: int = 4
     ln_eps: float = LN_EPS
+    post_ln: bool = False   # reading A-16: the "original approach" places LN after each residual add
 
     @property
     def dh(self) -> int:
@@ -163,6 +169,8 @@ def _merge_heads(t):
 
 def layer_forward(x: np.ndarray, flat: np.ndarray, cfg: LayerCfg):
     """Forward of one layer on x: [b, s, d] (fp64).  Returns (y, cache)."""
+    if cfg.post_ln:
+        return layer_forward_post(x, flat, cfg)
     p = unpack(flat, cfg.d, cfg.ffn_mult)
     d = cfg.d
     a, ln1c = layernorm_fwd(x, p["ln1_w"], p["ln1_b"], cfg.ln_eps)
@@ -183,6 +191,8 @@ def layer_forward(x: np.ndarray, flat: np.ndarray, cfg: LayerCfg):
 
 def layer_backward(dy: np.ndarray, cache: dict, flat: np.ndarray, cfg: LayerCfg):
     """Reverse mode through ``layer_forward``.  Returns (dx, dflat) with dflat in canonical layout."""
+    if cfg.post_ln:
+        return layer_backward_post(dy, cache, flat, cfg)
     p = unpack(flat, cfg.d, cfg.ffn_mult)
     d = cfg.d
     grads = np.zeros_like(flat)
@@ -215,6 +225,65 @@ def layer_backward(dy: np.ndarray, cache: dict, flat: np.ndarray, cfg: LayerCfg)
     da = dqkv @ p["Wqkv"].T
     dx, gv["ln1_w"][...], gv["ln1_b"][...] = layernorm_bwd(da, p["ln1_w"], cache["ln1c"])
     dx = dx + dh1
+    return dx, grads
+
+
+def _attn_block(a, p, cfg):
+    d = cfg.d
+    qkv = a @ p["Wqkv"] + p["bqkv"]
+    q = _split_heads(qkv[..., 0:d], cfg.heads)
+    k = _split_heads(qkv[..., d:2 * d], cfg.heads)
+    v = _split_heads(qkv[..., 2 * d:3 * d], cfg.heads)
+    oh, P = attention_fwd(q, k, v, cfg.causal)
+    return q, k, v, P, _merge_heads(oh)
+
+
+def layer_forward_post(x: np.ndarray, flat: np.ndarray, cfg: LayerCfg):
+    """Post-LN layer of the original transformer encoder (reading A-16), same parameters:
+    h1 = LN1(x + Attn(x) Wo + bo),  y = LN2(h1 + GELU(h1 W1 + b1) W2 + b2)."""
+    p = unpack(flat, cfg.d, cfg.ffn_mult)
+    q, k, v, P, o = _attn_block(x, p, cfg)
+    s1 = x + o @ p["Wo"] + p["bo"]
+    h1, ln1c = layernorm_fwd(s1, p["ln1_w"], p["ln1_b"], cfg.ln_eps)
+    u = h1 @ p["W1"] + p["b1"]
+    g = gelu(u)
+    s2 = h1 + g @ p["W2"] + p["b2"]
+    y, ln2c = layernorm_fwd(s2, p["ln2_w"], p["ln2_b"], cfg.ln_eps)
+    cache = dict(x=x, q=q, k=k, v=v, P=P, o=o, ln1c=ln1c, h1=h1, u=u, g=g, ln2c=ln2c)
+    return y, cache
+
+
+def layer_backward_post(dy: np.ndarray, cache: dict, flat: np.ndarray, cfg: LayerCfg):
+    """Reverse mode through ``layer_forward_post``."""
+    p = unpack(flat, cfg.d, cfg.ffn_mult)
+    grads = np.zeros_like(flat)
+    gv = unpack(grads, cfg.d, cfg.ffn_mult)
+
+    def flat2(t):
+        return t.reshape(-1, t.shape[-1])
+
+    # y = LN2(s2)
+    ds2, gv["ln2_w"][...], gv["ln2_b"][...] = layernorm_bwd(dy, p["ln2_w"], cache["ln2c"])
+    # s2 = h1 + g W2 + b2
+    gv["W2"][...] = flat2(cache["g"]).T @ flat2(ds2)
+    gv["b2"][...] = flat2(ds2).sum(axis=0)
+    du = (ds2 @ p["W2"].T) * gelu_grad(cache["u"])
+    # u = h1 W1 + b1
+    gv["W1"][...] = flat2(cache["h1"]).T @ flat2(du)
+    gv["b1"][...] = flat2(du).sum(axis=0)
+    dh1 = du @ p["W1"].T + ds2
+    # h1 = LN1(s1)
+    ds1, gv["ln1_w"][...], gv["ln1_b"][...] = layernorm_bwd(dh1, p["ln1_w"], cache["ln1c"])
+    # s1 = x + o Wo + bo
+    gv["Wo"][...] = flat2(cache["o"]).T @ flat2(ds1)
+    gv["bo"][...] = flat2(ds1).sum(axis=0)
+    do = ds1 @ p["Wo"].T
+    dq, dk, dv = attention_bwd(_split_heads(do, cfg.heads), cache["q"], cache["k"], cache["v"], cache["P"])
+    dqkv = np.concatenate([_merge_heads(dq), _merge_heads(dk), _merge_heads(dv)], axis=-1)
+    # qkv = x Wqkv + bqkv
+    gv["Wqkv"][...] = flat2(cache["x"]).T @ flat2(dqkv)
+    gv["bqkv"][...] = flat2(dqkv).sum(axis=0)
+    dx = dqkv @ p["Wqkv"].T + ds1
     return dx, grads
 
 

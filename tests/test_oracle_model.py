@@ -122,13 +122,66 @@ def test_layer_matches_torch_autograd_fp64(causal, d, heads, s, b):
             assert err < 1e-10, (k, err)
 
 
+def _torch_layer_post(x, flat, d, heads, causal, eps=om.LN_EPS):
+    """The original (post-LN) transformer encoder layer, built from torch's own ops (reading A-16)."""
+    p = {k: torch.from_numpy(v.copy()).requires_grad_(True) for k, v in om.unpack(flat, d).items()}
+    xt = torch.from_numpy(x.copy()).requires_grad_(True)
+    b, s, _ = x.shape
+    q, k, v = (xt @ p["Wqkv"] + p["bqkv"]).split(d, dim=-1)
+    sh = lambda t: t.reshape(b, s, heads, d // heads).transpose(1, 2)
+    o = F.scaled_dot_product_attention(sh(q), sh(k), sh(v), is_causal=causal).transpose(1, 2).reshape(b, s, d)
+    h1 = F.layer_norm(xt + o @ p["Wo"] + p["bo"], (d,), p["ln1_w"], p["ln1_b"], eps)
+    ffn = F.gelu(h1 @ p["W1"] + p["b1"], approximate="none") @ p["W2"] + p["b2"]
+    y = F.layer_norm(h1 + ffn, (d,), p["ln2_w"], p["ln2_b"], eps)
+    return xt, p, y
+
+
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("d,heads,s,b", [(16, 2, 7, 2), (32, 4, 12, 1)])
+def test_post_ln_layer_matches_torch_autograd_fp64(causal, d, heads, s, b):
+    rng = _rng(11)
+    flat = _params(d, 1, rng)[0]
+    x = rng.standard_normal((b, s, d))
+    dy = rng.standard_normal((b, s, d))
+    cfg = om.LayerCfg(d=d, heads=heads, causal=causal, post_ln=True)
+    y, cache = om.layer_forward(x, flat, cfg)
+    dx, g = om.layer_backward(dy, cache, flat, cfg)
+    xt, p, yt = _torch_layer_post(x, flat, d, heads, causal)
+    yt.backward(torch.from_numpy(dy))
+    np.testing.assert_allclose(y, yt.detach().numpy(), rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(dx, xt.grad.numpy(), rtol=1e-10, atol=1e-11)
+    gv = om.unpack(g, d)
+    for k in gv:
+        ref = p[k].grad.numpy()
+        if k == "bqkv":
+            assert np.max(np.abs(gv[k] - ref)) < 1e-11
+        else:
+            err = np.linalg.norm(gv[k] - ref) / max(np.linalg.norm(ref), 1e-30)
+            assert err < 1e-10, (k, err)
+    # every output row is normalised by LN2: mean b2, and (y - b2)/g2 has unit biased variance
+    yn = (y - p["ln2_b"].detach().numpy()) / p["ln2_w"].detach().numpy()
+    np.testing.assert_allclose(yn.mean(-1), 0.0, atol=1e-12)
+    np.testing.assert_allclose(yn.var(-1), 1.0, rtol=1e-3)
+
+
+def test_post_ln_differs_from_pre_ln():
+    rng = _rng(12)
+    d = 16
+    flat = _params(d, 1, rng)[0]
+    x = rng.standard_normal((1, 5, d))
+    y0, _ = om.layer_forward(x, flat, om.LayerCfg(d=d, heads=2))
+    y1, _ = om.layer_forward(x, flat, om.LayerCfg(d=d, heads=2, post_ln=True))
+    assert np.linalg.norm(y0 - y1) > 0.1 * np.linalg.norm(y0)
+
+
 # ------------------------------------------------------------------ P2: finite differences
 
-def test_step_gradient_matches_central_differences():
+@pytest.mark.parametrize("post_ln", [False, True])
+def test_step_gradient_matches_central_differences(post_ln):
     """Brute force on tiny inputs: every parameter of the whole 2-layer, 2x2-micro-batch step."""
     rng = _rng(2)
     d, heads, s, b, L, D, N = 8, 2, 5, 2, 2, 2, 2
-    cfg = om.LayerCfg(d=d, heads=heads, causal=True)
+    cfg = om.LayerCfg(d=d, heads=heads, causal=True, post_ln=post_ln)
     params = _params(d, L, rng, scale=0.3)
     X = rng.standard_normal((D, N, b, s, d))
     T = rng.standard_normal((D, N, b, s, d))

@@ -10,21 +10,21 @@ from oracle import model as om
 from oracle import schedule as osch
 
 
-def _setup(L=2, d=16, heads=2, s=6, b=2, N=3, D=2, seed=0, causal=True):
+def _setup(L=2, d=16, heads=2, s=6, b=2, N=3, D=2, seed=0, causal=True, post_ln=False):
     sh = synth.Shape(layers=L, d=d, heads=heads, seq=s, micro_batch=b, n_micro=N, dp=D)
     flat = synth.init_params(sh, seed=seed)
     params = [p.astype(np.float64) for p in synth.split_layers(flat, L)]
     X, T = synth.batch(sh, step=0, seed=seed + 10)
-    return om.LayerCfg(d=d, heads=heads, causal=causal), params, X, T
+    return om.LayerCfg(d=d, heads=heads, causal=causal, post_ln=post_ln), params, X, T
 
 
 def _rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
-@pytest.mark.parametrize("causal", [True, False])
-def test_layered_equals_standard_equals_fullbatch(causal):
-    cfg, params, X, T = _setup(causal=causal)
+@pytest.mark.parametrize("causal,post_ln", [(True, False), (False, False), (False, True)])
+def test_layered_equals_standard_equals_fullbatch(causal, post_ln):
+    cfg, params, X, T = _setup(causal=causal, post_ln=post_ln)
     ls, gs = osch.grads_standard(params, X, T, cfg)
     ll, gl = osch.grads_layered(params, X, T, cfg)
     lf, gf = osch.grads_fullbatch(params, X, T, cfg)
