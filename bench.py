@@ -117,6 +117,9 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) arm
+POST_LN = [False]   # --post-ln: the oracle sample runs the same layer variant as the timed path
+
+
 def oracle_sample_seconds(shape: dict, repeats: int = 1):
     """Time the fp64 oracle, as it stands, on one layer x one micro-batch forward + backward of the
     workload's shape (the bounded sample); returns (seconds per sample, threads used)."""
@@ -128,7 +131,7 @@ def oracle_sample_seconds(shape: dict, repeats: int = 1):
                      micro_batch=shape["micro_batch"], n_micro=1)
     flat = synth.init_params(sh, style="train").astype(np.float64)
     X, T = synth.batch(sh, step=0)
-    cfg = om.LayerCfg(d=sh.d, heads=sh.heads, causal=bool(shape.get("causal", 1)))
+    cfg = om.LayerCfg(d=sh.d, heads=sh.heads, causal=bool(shape.get("causal", 1)), post_ln=POST_LN[0])
     try:
         from threadpoolctl import threadpool_info
         threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
@@ -197,10 +200,12 @@ def main():
     ap.add_argument("--no-recompute", action="store_true", help="N2c: keep intermediates, no forward recompute")
     ap.add_argument("--pipeline", default="modular", choices=["modular", "contiguous"], help="N3: stage map")
     ap.add_argument("--nccl-dp", action="store_true", help="N1 baseline: NCCL all-gather / reduce-scatter")
+    ap.add_argument("--post-ln", action="store_true", help="N4: post-LN layer (original encoder, reading A-16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    POST_LN[0] = args.post_ln
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -229,11 +234,11 @@ def main():
     flags = _abi.LGA_FLAG_PROFILE | (_abi.LGA_FLAG_NO_COMM if args.no_comm else 0)
     variant = [n for n, on in (("keep_params", args.keep_params), ("unpartitioned", args.unpartitioned),
                                ("no_recompute", args.no_recompute), ("contiguous_pp", args.pipeline == "contiguous"),
-                               ("nccl_dp", args.nccl_dp)) if on]
+                               ("nccl_dp", args.nccl_dp), ("post_ln", args.post_ln)) if on]
     flags |= ((_abi.LGA_FLAG_KEEP_PARAMS if args.keep_params else 0) | (_abi.LGA_FLAG_UNPARTITIONED if args.unpartitioned else 0)
               | (_abi.LGA_FLAG_NO_RECOMPUTE if args.no_recompute else 0)
               | (_abi.LGA_FLAG_CONTIGUOUS_PP if args.pipeline == "contiguous" else 0)
-              | (_abi.LGA_FLAG_NCCL_DP if args.nccl_dp else 0))
+              | (_abi.LGA_FLAG_NCCL_DP if args.nccl_dp else 0) | (_abi.LGA_FLAG_POST_LN if args.post_ln else 0))
     cfg = Config(dp=dp, pp=pp, precision=precision, chunk=args.chunk,
                  schedule=LGA_LAYERED if args.schedule == "layered" else LGA_STANDARD, flags=flags, **shape)
     tr = Trainer(cfg, rank=rank, world=world, device=local, init_params=None, seed=1234)

@@ -101,6 +101,9 @@ typedef enum { LGA_LAYERED = 0, LGA_STANDARD = 1 } lga_schedule;
 #define LGA_FLAG_CONTIGUOUS_PP 0x40u  /* N3: contiguous pipeline map, layer i on stage i / (L/P) (the
                                          standard layout of P:71) instead of the modular i mod P;
                                          activations cross stages only at block boundaries */
+#define LGA_FLAG_POST_LN       0x100u /* N4: post-LN layer of the original encoder (reading A-16),
+                                         h1 = LN1(x + Attn(x)), y = LN2(h1 + FFN(h1)); same parameters and
+                                         layout.  Default: pre-LN (reading A-1).  Any schedule / variant */
 
 typedef struct {
   uint32_t abi_version;    /* must be LGA_ABI_VERSION */

@@ -26,6 +26,7 @@ LGA_FLAG_NO_RECOMPUTE = 0x10     # N2c: keep intermediates, no forward recompute
 LGA_FLAG_UNPARTITIONED = 0x20    # N2b: full state per replica, one all-reduce per layer
 LGA_FLAG_CONTIGUOUS_PP = 0x40    # N3: layer i on stage i // (L/P)
 LGA_FLAG_NCCL_DP = 0x80          # N1 baseline: NCCL all-gather / reduce-scatter instead of peer memory
+LGA_FLAG_POST_LN = 0x100         # N4: post-LN layer (original encoder; reading A-16)
 
 STATUS = {0: "LGA_OK", 1: "LGA_ERR_INVALID_ARG", 2: "LGA_ERR_UNSUPPORTED", 3: "LGA_ERR_OUT_OF_MEMORY",
           4: "LGA_ERR_CUDA", 5: "LGA_ERR_NCCL", 6: "LGA_ERR_SIZE_MISMATCH", 7: "LGA_ERR_BAD_STATE"}

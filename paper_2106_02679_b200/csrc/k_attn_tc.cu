@@ -320,7 +320,12 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
         mbar_arrive(&p_full[b * 2 + hf]);
       }
       // epilogue: combine the halves, o = (2^(m0-m) O_0 + 2^(m1-m) O_1) / (2^(m0-m) l_0 + 2^(m1-m) l_1)
-      mbar_wait(&o_done[0], (gt - 1) & 1);   // every PV of the item done: O final, P buffer free for `red`
+      // every PV of the item done: O final.  s_full(gt-1) only implies PV(gt-3), so o_done may be anywhere
+      // from PV(gt-3) to PV(gt-1) -- three states a parity wait cannot tell apart (a wait for (gt-1) would
+      // pass at once two completions short).  First PV(gt-2) through its buffer's p_free, which is either
+      // at PV(gt-4) or PV(gt-2) (PV(gt) needs this thread's o_free), then o_done is one phase from PV(gt-1).
+      if (gt >= 2) mbar_wait(&p_free[gt & 1], ((gt - 2) >> 1) & 1);
+      mbar_wait(&o_done[0], (gt - 1) & 1);
       mbar_wait(&o_done[1], (gt - 1) & 1);
       fence_after();
       red[hf * 128 + r] = m_used;

@@ -73,6 +73,7 @@ struct Cfg {
   bool keep, norecomp, unpart, contig;   // LGA_FLAG_KEEP_PARAMS / NO_RECOMPUTE / UNPARTITIONED / CONTIGUOUS_PP
   bool graph_off;                        // LGA_FLAG_NO_GRAPH
   bool dp_ipc;                           // DP all-gather / reduce-scatter over NVLink peer memory (not NCCL)
+  bool post_ln;                          // LGA_FLAG_POST_LN (reading A-16)
   // canonical offsets
   int64_t o_ln1w, o_ln1b, o_wqkv, o_bqkv, o_wo, o_bo, o_ln2w, o_ln2b, o_w1, o_b1, o_w2, o_b2;
 };
@@ -122,10 +123,11 @@ static lga_status validate(const lga_config* c, int world, Cfg* out) {
   g.norecomp = (c->flags & LGA_FLAG_NO_RECOMPUTE) != 0;
   g.contig = (c->flags & LGA_FLAG_CONTIGUOUS_PP) != 0;
   g.graph_off = (c->flags & LGA_FLAG_NO_GRAPH) != 0;
-  // N1: partitioned LAYERED data parallelism over peer memory unless LGA_FLAG_NCCL_DP asks for NCCL
-  g.dp_ipc = g.D > 1 && g.layered && !g.unpart && !(c->flags & LGA_FLAG_NCCL_DP);
   g.bf16 = c->precision == LGA_BF16;
   g.layered = c->schedule == LGA_LAYERED;
+  // N1: partitioned LAYERED data parallelism over peer memory unless LGA_FLAG_NCCL_DP asks for NCCL
+  g.dp_ipc = g.D > 1 && g.layered && !g.unpart && !(c->flags & LGA_FLAG_NCCL_DP);
+  g.post_ln = (c->flags & LGA_FLAG_POST_LN) != 0;
   g.causal = c->causal != 0;
   g.E = g.bf16 ? DT::BF16 : DT::F32;
   g.G = (g.bf16 && g.D > 1) ? DT::BF16 : DT::F32;   // 16-bit reduction only when there is a reduction (A-7)
@@ -170,6 +172,8 @@ struct Ws {
   void *a = nullptr, *qkv = nullptr, *o = nullptr, *cn = nullptr, *u = nullptr, *g = nullptr;
   float *h1 = nullptr, *lse = nullptr;
   float2 *st1 = nullptr, *st2 = nullptr;
+  // post-LN only: hn = LN1(s1) in fp32 (FFN2 residual; bf16 mode, else cn), s2 = h1 + FFN(h1) (LN2 input)
+  float *hn = nullptr, *s2 = nullptr;
 };
 
 }  // namespace lga
@@ -308,6 +312,10 @@ static void plan_arena(lga_handle* h) {
     w.lse = A.take<float>(Tw / c.s * c.H * c.s);
     w.st1 = A.take<float2>(Tw);
     w.st2 = A.take<float2>(Tw);
+    if (c.post_ln) {
+      w.hn = c.bf16 ? A.take<float>(Tw * d) : nullptr;
+      w.s2 = A.take<float>(Tw * d);
+    }
   }
   h->dYe = A.take_bytes(T * d * e);
   h->dh1e = A.take_bytes(T * d * e);
@@ -422,10 +430,13 @@ static void trace(lga_handle* h, const char* what, int64_t layer) {
 // Forward of local layer j over micro-batches [m0, m0+c) (module docstring of kernels.cuh).
 // x_in: [c][M][d] fp32; y_out: fp32 destination or nullptr (recompute: FFN2 not needed).
 // cc: micro-batches in this launch (default the configured chunk c)
+static void layer_fwd_post(lga_handle* h, const Ws& w, const void* W, const float* x_in, float* y_out, cudaStream_t st,
+                           int cc);
 static void layer_fwd(lga_handle* h, const Ws& w, const void* W, const float* x_in, float* y_out, cudaStream_t st,
                       int cc = -1) {
   const Cfg& c = h->c;
   if (cc < 0) cc = c.c;
+  if (c.post_ln) return layer_fwd_post(h, w, W, x_in, y_out, st, cc);
   const int T = cc * c.M;
   const int d = c.d;
   const DT E = c.E;
@@ -489,6 +500,82 @@ static void layer_fwd(lga_handle* h, const Ws& w, const void* W, const float* x_
   }
 }
 
+// Post-LN forward (reading A-16): a = x (cast to E for the QKV GEMM), s1 = x + Attn(a) Wo + bo (w.h1),
+// h1 = LN1(s1) (E copy in cn, fp32 copy in hn), s2 = h1 + GELU(h1 W1 + b1) W2 + b2, y = LN2(s2).  The
+// recompute (y_out == nullptr) still runs FFN2 and LN2: the LN2 backward reads s2 and its statistics.
+static void layer_fwd_post(lga_handle* h, const Ws& w, const void* W, const float* x_in, float* y_out, cudaStream_t st,
+                           int cc) {
+  const Cfg& c = h->c;
+  const int T = cc * c.M;
+  const int d = c.d;
+  const DT E = c.E;
+  cast_f32(x_in, w.a, E, (int64_t)T * d, st);
+  KCHECK();
+  {  // qkv = x Wqkv + bqkv
+    GemmArgs g;
+    g.M = T; g.N = 3 * d; g.K = d;
+    g.A = w.a; g.lda = d; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_wqkv); g.ldb = 3 * d; g.b_kmajor = false;
+    g.epi.kind = EPI_STORE; g.epi.bias = eoff((void*)W, E, c.o_bqkv); g.epi.bias_dt = E;
+    g.epi.out = w.qkv; g.epi.ldo = 3 * d; g.epi.out_dt = E;
+    gemm(h, g, st);
+  }
+  {  // o = attention(q, k, v)
+    AttnArgs a;
+    a.nseq = cc * c.b; a.seq = c.s; a.heads = c.H; a.dh = c.dh; a.d = d; a.causal = c.causal;
+    a.scale = 1.0f / sqrtf((float)c.dh);
+    a.qkv = w.qkv; a.o = w.o; a.lse = w.lse;
+    const int p = prof_begin(h, st);
+    if (c.bf16) CK(attn_fwd_bf16(a, st)); else attn_fwd_f32(a, st);
+    KCHECK();
+    prof_end(h, p, st, FAM_ATTN, attn_flops_fwd(c, a.nseq));
+  }
+  {  // s1 = x + o Wo + bo
+    GemmArgs g;
+    g.M = T; g.N = d; g.K = d;
+    g.A = w.o; g.lda = d; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_wo); g.ldb = d; g.b_kmajor = false;
+    g.epi.kind = EPI_STORE; g.epi.bias = eoff((void*)W, E, c.o_bo); g.epi.bias_dt = E;
+    g.epi.res = x_in; g.epi.ldr = d;
+    g.epi.out = w.h1; g.epi.ldo = d; g.epi.out_dt = DT::F32;
+    gemm(h, g, st);
+  }
+  // h1 = LN1(s1): the E copy feeds FFN1; bf16 mode also keeps an fp32 copy for the FFN2 residual (the same
+  // kernel on the same input: identical statistics)
+  ln_fwd(w.h1, eoff((void*)W, E, c.o_ln1w), eoff((void*)W, E, c.o_ln1b), E, w.cn, E, w.st1, T, d, c.ln_eps, st);
+  KCHECK();
+  const float* hn = static_cast<const float*>(w.cn);
+  if (c.bf16) {
+    ln_fwd(w.h1, eoff((void*)W, E, c.o_ln1w), eoff((void*)W, E, c.o_ln1b), E, w.hn, DT::F32, w.st1, T, d, c.ln_eps, st);
+    KCHECK();
+    hn = w.hn;
+  }
+  {  // u = h1 W1 + b1 ; g = GELU(u)
+    GemmArgs g;
+    g.M = T; g.N = c.f; g.K = d;
+    g.A = w.cn; g.lda = d; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_w1); g.ldb = c.f; g.b_kmajor = false;
+    g.epi.kind = EPI_GELU_FWD; g.epi.bias = eoff((void*)W, E, c.o_b1); g.epi.bias_dt = E;
+    g.epi.aux = w.u; g.epi.ldaux = c.f; g.epi.aux_dt = E;
+    g.epi.out = w.g; g.epi.ldo = c.f; g.epi.out_dt = E;
+    gemm(h, g, st);
+  }
+  {  // s2 = h1 + g W2 + b2
+    GemmArgs g;
+    g.M = T; g.N = d; g.K = c.f;
+    g.A = w.g; g.lda = c.f; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_w2); g.ldb = d; g.b_kmajor = false;
+    g.epi.kind = EPI_STORE; g.epi.bias = eoff((void*)W, E, c.o_b2); g.epi.bias_dt = E;
+    g.epi.res = hn; g.epi.ldr = d;
+    g.epi.out = w.s2; g.epi.ldo = d; g.epi.out_dt = DT::F32;
+    gemm(h, g, st);
+  }
+  // y = LN2(s2) (recompute: statistics only, y into the backward's dC scratch)
+  ln_fwd(w.s2, eoff((void*)W, E, c.o_ln2w), eoff((void*)W, E, c.o_ln2b), E, y_out ? y_out : h->dC, DT::F32, w.st2, T,
+         d, c.ln_eps, st);
+  KCHECK();
+}
+
 // wgrad: dW[i][j] (+)= sum_t X[t][i] dYm[t][j]  -> region at `off` with leading dim n
 static void wgrad(lga_handle* h, const void* X, int64_t ldx, const void* Dy, int64_t ldy, int m, int n, int T,
                   const GradDst& dst, int64_t /*off*/, cudaStream_t st) {
@@ -514,10 +601,13 @@ static void bias_grad(lga_handle* h, const void* X, DT xdt, int64_t ldx, int n, 
 // dx_out: where dX goes (in place over dY, the previous stage's buffer, or a scratch sink).
 // bf16: the GEMMs read dY as bf16 from h->dYe -- cast here unless dYe_ready (the previous layer's LN1
 // backward already wrote it next to its fp32 dX); dx_e_out: also write dX as bf16 there (or nullptr).
+static void layer_bwd_post(lga_handle* h, const Ws& w, const void* W, const float* dY, float* dx_out, int chunk_idx,
+                           int nchunks, int jl, cudaStream_t st);
 static void layer_bwd(lga_handle* h, const Ws& w, const void* W, const float* x_in, const float* dY, float* dx_out,
                       int chunk_idx, int nchunks, int jl, cudaStream_t st, bool dYe_ready = false,
                       void* dx_e_out = nullptr) {
   const Cfg& c = h->c;
+  if (c.post_ln) return layer_bwd_post(h, w, W, dY, dx_out, chunk_idx, nchunks, jl, st);
   const int T = c.c * c.M;
   const int d = c.d, f = c.f;
   const DT E = c.E;
@@ -606,6 +696,91 @@ static void layer_bwd(lga_handle* h, const Ws& w, const void* W, const float* x_
     colsum_finish(h->partial, nblk, 2LL * d, d, gw.acc_in, gw.out, gw.out_dt, st);
     colsum_finish(h->partial + d, nblk, 2LL * d, d, gbias.acc_in, gbias.out, gbias.out_dt, st);
     KCHECK();
+  }
+}
+
+// Post-LN backward (reading A-16; oracle.model.layer_backward_post): ds2 = LN2'(dY); FFN2 / FFN1 grads;
+// dh1 = dU W1^T + ds2 (GEMM epilogue residual); ds1 = LN1'(dh1); O-projection and attention grads;
+// dX = dqkv Wqkv^T + ds1.  dY is read only by the first kernel, so dx_out may alias it.
+static void layer_bwd_post(lga_handle* h, const Ws& w, const void* W, const float* dY, float* dx_out, int chunk_idx,
+                           int nchunks, int jl, cudaStream_t st) {
+  const Cfg& c = h->c;
+  const int T = c.c * c.M;
+  const int d = c.d, f = c.f;
+  const DT E = c.E;
+  auto dst = [&](int64_t off) { return grad_dst(h, chunk_idx, nchunks, jl, off); };
+  auto ln_back = [&](const float* dout, const float* xin, const float2* stats, int64_t ow, int64_t ob) {
+    // -> h->dh1 (fp32) and, bf16 mode, h->dh1e; gamma / beta gradients from the column partials
+    const int nblk = ln_bwd(dout, xin, stats, eoff((void*)W, E, ow), E, nullptr, h->dh1, c.bf16 ? h->dh1e : nullptr, E,
+                            h->partial, T, d, st);
+    KCHECK();
+    GradDst gw = dst(ow), gbias = dst(ob);
+    colsum_finish(h->partial, nblk, 2LL * d, d, gw.acc_in, gw.out, gw.out_dt, st);
+    colsum_finish(h->partial + d, nblk, 2LL * d, d, gbias.acc_in, gbias.out, gbias.out_dt, st);
+    KCHECK();
+  };
+  const void* dse = c.bf16 ? (const void*)h->dh1e : (const void*)h->dh1;   // ds2, then ds1, as GEMM operand
+  // ---- LN2: y = LN2(s2)
+  ln_back(dY, w.s2, w.st2, c.o_ln2w, c.o_ln2b);
+  // ---- FFN2: s2 = h1 + g W2 + b2
+  wgrad(h, w.g, f, dse, d, f, d, T, dst(c.o_w2), c.o_w2, st);
+  bias_grad(h, h->dh1, DT::F32, d, d, T, dst(c.o_b2), st);
+  {  // dU = (ds2 W2^T) * GELU'(u), written over u
+    GemmArgs g;
+    g.M = T; g.N = f; g.K = d;
+    g.A = dse; g.lda = d; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_w2); g.ldb = d; g.b_kmajor = true;
+    g.epi.kind = EPI_GELU_BWD; g.epi.aux = w.u; g.epi.ldaux = f; g.epi.aux_dt = E;
+    g.epi.out = w.u; g.epi.ldo = f; g.epi.out_dt = E;
+    gemm(h, g, st);
+  }
+  void* dU = w.u;
+  // ---- FFN1: u = h1 W1 + b1
+  wgrad(h, w.cn, d, dU, f, d, f, T, dst(c.o_w1), c.o_w1, st);
+  bias_grad(h, dU, E, f, f, T, dst(c.o_b1), st);
+  {  // dh1 = dU W1^T + ds2
+    GemmArgs g;
+    g.M = T; g.N = d; g.K = f;
+    g.A = dU; g.lda = f; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_w1); g.ldb = f; g.b_kmajor = true;
+    g.epi.res = h->dh1; g.epi.ldr = d;
+    g.epi.out = h->dC; g.epi.ldo = d; g.epi.out_dt = DT::F32;
+    gemm(h, g, st);
+  }
+  // ---- LN1: h1 = LN1(s1)
+  ln_back(h->dC, w.h1, w.st1, c.o_ln1w, c.o_ln1b);
+  // ---- O projection: s1 = x + o Wo + bo
+  wgrad(h, w.o, d, dse, d, d, d, T, dst(c.o_wo), c.o_wo, st);
+  bias_grad(h, h->dh1, DT::F32, d, d, T, dst(c.o_bo), st);
+  {  // dO = ds1 Wo^T
+    GemmArgs g;
+    g.M = T; g.N = d; g.K = d;
+    g.A = dse; g.lda = d; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_wo); g.ldb = d; g.b_kmajor = true;
+    g.epi.out = h->dO; g.epi.ldo = d; g.epi.out_dt = E;
+    gemm(h, g, st);
+  }
+  {  // attention backward -> dqkv
+    AttnArgs a;
+    a.nseq = c.c * c.b; a.seq = c.s; a.heads = c.H; a.dh = c.dh; a.d = d; a.causal = c.causal;
+    a.scale = 1.0f / sqrtf((float)c.dh);
+    a.qkv = w.qkv; a.o = w.o; a.lse = w.lse; a.dO = h->dO; a.dsum = h->dsum; a.dqkv = h->dqkv;
+    const int p = prof_begin(h, st);
+    if (c.bf16) CK(attn_bwd_bf16(a, st)); else attn_bwd_f32(a, st);
+    KCHECK();
+    prof_end(h, p, st, FAM_ATTN, 2.0 * attn_flops_fwd(c, a.nseq));
+  }
+  // ---- QKV: qkv = x Wqkv + bqkv
+  wgrad(h, w.a, d, h->dqkv, 3 * d, d, 3 * d, T, dst(c.o_wqkv), c.o_wqkv, st);
+  bias_grad(h, h->dqkv, E, 3 * d, 3 * d, T, dst(c.o_bqkv), st);
+  {  // dX = dqkv Wqkv^T + ds1
+    GemmArgs g;
+    g.M = T; g.N = d; g.K = 3 * d;
+    g.A = h->dqkv; g.lda = 3 * d; g.a_kmajor = true;
+    g.B = eoff((void*)W, E, c.o_wqkv); g.ldb = 3 * d; g.b_kmajor = true;
+    g.epi.res = h->dh1; g.epi.ldr = d;
+    g.epi.out = dx_out; g.epi.ldo = d; g.epi.out_dt = DT::F32;
+    gemm(h, g, st);
   }
 }
 
@@ -759,6 +934,8 @@ static Ws chunk_ws(lga_handle* h, int j, int m0) {
   w.lse = b.lse + (int64_t)m0 * c.b * c.H * c.s;
   w.st1 = b.st1 + t;
   w.st2 = b.st2 + t;
+  w.hn = b.hn ? b.hn + t * d : nullptr;
+  w.s2 = b.s2 ? b.s2 + t * d : nullptr;
   return w;
 }
 

@@ -16,8 +16,9 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / nb) if nb > 0 else float(np.linalg.norm(a - b))
 
 
-def oracle_run(sh: synth.Shape, init: np.ndarray, batches, causal=True, lr=1e-3, wd=0.0, schedule="standard"):
-    cfg = om.LayerCfg(d=sh.d, heads=sh.heads, causal=bool(causal))
+def oracle_run(sh: synth.Shape, init: np.ndarray, batches, causal=True, lr=1e-3, wd=0.0, schedule="standard",
+               post_ln=False):
+    cfg = om.LayerCfg(d=sh.d, heads=sh.heads, causal=bool(causal), post_ln=bool(post_ln))
     params = [p.astype(np.float64) for p in synth.split_layers(init, sh.layers)]
     opt = osch.AdamW(lr=lr, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=wd)
     new, losses, grads = osch.train_steps(params, batches, cfg, opt, schedule)

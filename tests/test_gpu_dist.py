@@ -38,7 +38,7 @@ def _launch(tmp_path, sh, precision=0, schedule=0, chunk=0, steps=1, flags=0):
 
 
 # LGA_FLAG_* variant bits (include/lga.h) -> oracle.counters keyword arguments
-KEEP, NORECOMP, UNPART, CONTIG, NCCL_DP = 0x8, 0x10, 0x20, 0x40, 0x80
+KEEP, NORECOMP, UNPART, CONTIG, NCCL_DP, POST_LN = 0x8, 0x10, 0x20, 0x40, 0x80, 0x100
 
 
 def _variant(flags):
@@ -49,7 +49,7 @@ def _variant(flags):
 def _check(outs, sh, tol, steps=1, schedule="layered", elem=4, flags=0):
     batches = [synth.batch(sh, step=k) for k in range(steps)]
     init = synth.init_params(sh, style="parity")
-    rp, rl, rg = oracle_run(sh, init, batches, lr=1e-3)
+    rp, rl, rg = oracle_run(sh, init, batches, lr=1e-3, post_ln=bool(flags & POST_LN))
     pl = sh.d * sh.d * 12 + 13 * sh.d
     for o in outs:
         stage = int(o["stage"])
@@ -152,3 +152,32 @@ def test_dp4_bf16_peer_memory_three_steps(tmp_path):
     """Peer-memory DP over 3 steps (graph replay from step 2): flags and epochs across steps."""
     sh = synth.Shape(layers=4, d=256, heads=2, seq=128, micro_batch=1, n_micro=4, dp=4)
     _check(_launch(tmp_path, sh, precision=1, steps=3), sh, 2e-2, steps=3, elem=2)
+
+
+@pytest.mark.parametrize("flags,R", [(0, 2), (KEEP, 1)])
+def test_dp2_peer_memory_path_is_the_one_that_runs(tmp_path, flags, R):
+    """The default D > 1 LAYERED path really is peer memory: per step it launches exactly 4 more kernels per
+    layer (two flag waits and two signals around the fused reduce-scatter + AdamW) and 2 more per
+    all-gather (flag wait + read signal; the copies are copy-engine memcpys) than the NCCL baseline."""
+    sh = synth.Shape(layers=4, d=64, heads=4, seq=32, micro_batch=2, n_micro=4, dp=2)
+    (tmp_path / "peer").mkdir()
+    (tmp_path / "nccl").mkdir()
+    peer = _launch(tmp_path / "peer", sh, flags=flags)
+    nccl = _launch(tmp_path / "nccl", sh, flags=flags | NCCL_DP)
+    lloc = sh.layers
+    for a, b in zip(peer, nccl):
+        ka = json.loads(str(a["timing"]))["kernel_launches"]
+        kb = json.loads(str(b["timing"]))["kernel_launches"]
+        assert ka - kb == 4 * lloc + 2 * R * lloc, (ka, kb)
+        np.testing.assert_allclose(a["params"], b["params"], rtol=1e-6, atol=1e-8)
+
+
+# ---- N4: post-LN layer (reading A-16) under peer-memory DP and the modular pipeline
+def test_dp2_bf16_post_ln(tmp_path):
+    sh = synth.Shape(layers=2, d=256, heads=2, seq=128, micro_batch=1, n_micro=4, dp=2)
+    _check(_launch(tmp_path, sh, precision=1, steps=2, flags=POST_LN), sh, 2e-2, steps=2, elem=2, flags=POST_LN)
+
+
+def test_pp2_dp2_fp32_post_ln(tmp_path):
+    sh = synth.Shape(layers=4, d=64, heads=4, seq=32, micro_batch=2, n_micro=4, dp=2, pp=2)
+    _check(_launch(tmp_path, sh, flags=POST_LN), sh, 1e-5, flags=POST_LN)
