@@ -50,16 +50,18 @@ def test_gloo_data_parallel_decomposition(tmp_path):
     assert outs[0]["shard"][1] == outs[1]["shard"][1] and outs[1]["shard"][0] == outs[0]["shard"][1]
 
 
-def test_gloo_modular_pipeline_decomposition(tmp_path):
+@pytest.mark.parametrize("pp,dp", [(2, 1), (2, 2)])
+def test_gloo_modular_pipeline_decomposition(tmp_path, pp, dp):
     from oracle import counters as oc
     from oracle import model as om
     from oracle import schedule as osch
-    sh = synth.Shape(layers=4, d=32, heads=2, seq=8, micro_batch=2, n_micro=3, pp=2)
+    sh = synth.Shape(layers=4, d=32, heads=2, seq=8, micro_batch=2, n_micro=3, pp=pp, dp=dp)
     shape = json.dumps(dict(layers=sh.layers, d=sh.d, heads=sh.heads, seq=sh.seq, micro_batch=sh.micro_batch,
-                            n_micro=sh.n_micro, pp=sh.pp))
-    r = _torchrun([os.path.join(HERE, "pipe_cpu_worker.py"), "--out", str(tmp_path), "--shape", shape])
+                            n_micro=sh.n_micro, pp=sh.pp, dp=sh.dp))
+    r = _torchrun([os.path.join(HERE, "pipe_cpu_worker.py"), "--out", str(tmp_path), "--shape", shape],
+                  nproc=pp * dp)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-    outs = [dict(np.load(os.path.join(tmp_path, f"rank{k}.npz"))) for k in range(2)]
+    outs = [dict(np.load(os.path.join(tmp_path, f"rank{k}.npz"))) for k in range(pp * dp)]
     init = synth.init_params(sh, style="parity")
     params = [p.astype(np.float64) for p in synth.split_layers(init, sh.layers)]
     X, T = synth.batch(sh, step=0)
@@ -68,10 +70,10 @@ def test_gloo_modular_pipeline_decomposition(tmp_path):
         assert rel(o["grads"], np.concatenate(ref_g)) < 1e-12
         assert abs(float(o["loss"][0]) - ref_loss) < 1e-12 * abs(ref_loss)
         c = oc.comm_counters(oc.StepShape(layers=sh.layers, d=sh.d, seq=sh.seq, micro_batch=sh.micro_batch,
-                                          n_micro=sh.n_micro, pp=sh.pp), stage=k)
+                                          n_micro=sh.n_micro, pp=sh.pp), stage=k % pp)
         assert int(o["sends"]) == c["p2p_send_calls"] and int(o["recvs"]) == c["p2p_recv_calls"]
-    # 2 N (L - 1) crossings per step in total (P10)
-    assert sum(int(o["sends"]) for o in outs) == 2 * sh.n_micro * (sh.layers - 1)
+    # 2 N (L - 1) crossings per replica per step (P10)
+    assert sum(int(o["sends"]) for o in outs) == dp * 2 * sh.n_micro * (sh.layers - 1)
 
 
 def test_reference_arm_under_torchrun_rank0_only():
