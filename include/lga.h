@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define LGA_ABI_VERSION 2u
+#define LGA_ABI_VERSION 3u
 #define LGA_NCCL_ID_BYTES 128
 
 typedef enum {
@@ -168,27 +168,46 @@ lga_status lga_param_count(const lga_config* cfg, uint64_t* per_layer, uint64_t*
 
 /* Fill `out` (LGA_NCCL_ID_BYTES bytes, host) with a fresh NCCL unique id.  Rank 0 calls
  * it and the caller broadcasts the bytes to every rank (e.g. over torch.distributed)
- * before lga_init.  Not needed when world == 1. */
+ * before lga_init.  Needed only for the NCCL baseline (LGA_FLAG_NCCL_DP with dp > 1). */
 lga_status lga_nccl_unique_id(uint8_t* out);
+
+/* Host all-gather supplied by the caller for the bootstrap of a world > 1 (the CUDA IPC
+ * handles of every rank's arena and their offsets): copy `bytes`
+ * bytes from `send` into recv + r * bytes of EVERY rank r, in rank order, and return 0
+ * (non-zero = failure, lga_init then returns LGA_ERR_INVALID_ARG).  Called only from
+ * inside lga_init, on the calling thread; torch.distributed.all_gather_object over any
+ * backend (gloo included) is a valid implementation.  `ctx` is passed through. */
+typedef int32_t (*lga_allgather_fn)(void* ctx, const void* send, void* recv, uint64_t bytes);
 
 /* Create the per-rank state.  Collective over all `world` ranks.
  *   cfg          configuration (copied).
  *   rank, world  this process's rank and the world size; world must equal dp * pp.
  *   device       CUDA device ordinal this rank uses (the library calls cudaSetDevice).
- *   nccl_id      LGA_NCCL_ID_BYTES from lga_nccl_unique_id on rank 0; NULL iff world == 1.
+ *                Several ranks may share one device (CUDA IPC works between processes
+ *                on one GPU; the peer-memory paths then run time-sliced).
+ *   allgather,   host all-gather for the bootstrap; required when world > 1 unless
+ *   allgather_ctx  nccl_id is given (the exchange then runs over NCCL); ignored if world == 1.
+ *   nccl_id      LGA_NCCL_ID_BYTES from lga_nccl_unique_id on rank 0, or NULL.  Required
+ *                only by LGA_FLAG_NCCL_DP with dp > 1 (INVALID_ARG otherwise); every
+ *                other data path -- all-gathers, reduce-scatters, the unpartitioned
+ *                all-reduce, pipeline transfers, the loss all-reduce -- runs over CUDA IPC
+ *                peer memory, so one GPU can host several ranks.  (SURVEY 8(b) sketched a
+ *                borrowed NCCL communicator; DESIGN.md "Boundary" records the change.)
  *   cuda_stream  borrowed cudaStream_t (0 = legacy default stream) the caller orders its
  *                work on; lga_step consumes inputs and publishes results on it.
  *   init_params  host fp32, canonical layout of ALL L layers (L * P_l floats, layout in
  *                DESIGN.md "Canonical parameter layout"; each rank keeps only its stage's
  *                layers and its shard); NULL = on-device seeded init ("train" recipe,
  *                DESIGN.md "Inputs") from `seed`.
+ * On any error *out stays NULL and everything allocated so far is freed.
  * Errors: INVALID_ARG (d % heads, L % pp, world != dp*pp, N < pp, schedule/pp, chunk,
- *         a variant flag with LGA_STANDARD),
+ *         a variant flag with LGA_STANDARD, no bootstrap for world > 1, a failing
+ *         allgather, NCCL_DP without nccl_id),
  *         UNSUPPORTED (bf16 with d % 64 != 0 or head size not 64/128; ffn_mult != 4),
  *         OUT_OF_MEMORY, CUDA, NCCL. */
 lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t device,
-                    const uint8_t* nccl_id, uintptr_t cuda_stream, const float* init_params,
-                    uint64_t seed, lga_handle** out);
+                    lga_allgather_fn allgather, void* allgather_ctx, const uint8_t* nccl_id,
+                    uintptr_t cuda_stream, const float* init_params, uint64_t seed, lga_handle** out);
 
 /* One training step: forward + loss + recompute/backward + reduce-scatter + AdamW.
  *   x, target   DEVICE fp32 [N][b][s][d] (row-major, this replica's micro-batches).  x is
@@ -200,12 +219,15 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
 lga_status lga_step(lga_handle* h, const float* x, const float* target, double* loss_out);
 
 /* Same as lga_step with HOST inputs: x and target (host, same layout, pinned or pageable)
- * are copied to the device inside the call; the end-to-end path of bench.py's "e2e". */
+ * are copied to the device inside the call; the end-to-end path of bench.py's "e2e".  The
+ * call returns only after both copies have completed, so the caller may refill or free x
+ * and target as soon as it returns (loss_out NULL or not). */
 lga_status lga_step_host(lga_handle* h, const float* x, const float* target, double* loss_out);
 
 /* The last step's reduced gradient dL/dtheta (fp32, canonical layout), requires
  * retain_grads.  pp == 1: all L layers (n = L * P_l); pp > 1: this stage's layers in
- * ascending order (n = (L/pp) * P_l).  Collective over the rank's data-parallel group.
+ * ascending order (n = (L/pp) * P_l).  Collective over all world ranks: the shards of the
+ * replicas are read over peer memory between two device barriers.
  * out_on_device: 1 = `out` is a device pointer, 0 = host.  SIZE_MISMATCH if n differs. */
 lga_status lga_grads(lga_handle* h, float* out, uint64_t n, int32_t out_on_device);
 
@@ -222,7 +244,9 @@ lga_status lga_layer_stage(const lga_handle* h, int32_t* stage_of_layer, int32_t
 /* Device timing of the last step (synchronises the step's completion event). */
 lga_status lga_timing_last(lga_handle* h, lga_timing* out);
 
-/* Free everything the handle owns.  Not collective-safe to skip: call on every rank. */
+/* Free everything the handle owns.  Collective: waits for this rank's last step on the
+ * caller stream, then for every rank to arrive (device barrier over peer memory, 60 s
+ * timeout) before unmapping the peers' arenas and freeing its own, which peers write into. */
 void lga_destroy(lga_handle* h);
 
 #ifdef __cplusplus

@@ -13,7 +13,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liblga.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 NCCL_ID_BYTES = 128
 
 LGA_FP32, LGA_BF16 = 0, 1
@@ -68,6 +68,9 @@ class lga_timing(C.Structure):
         return {n: float(getattr(self, n)) for n, _ in self._fields_}
 
 
+# int32_t (*lga_allgather_fn)(void* ctx, const void* send, void* recv, uint64_t bytes)  (include/lga.h)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
+
 _lib = None
 
 
@@ -87,8 +90,8 @@ def lib():
         "lga_last_error": (C.c_char_p, []),
         "lga_param_count": (C.c_int, [C.POINTER(lga_config), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "lga_nccl_unique_id": (C.c_int, [C.c_char_p]),
-        "lga_init": (C.c_int, [C.POINTER(lga_config), C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_void_p,
-                               C.c_void_p, C.c_uint64, C.POINTER(H)]),
+        "lga_init": (C.c_int, [C.POINTER(lga_config), C.c_int32, C.c_int32, C.c_int32, ALLGATHER_FN, C.c_void_p,
+                               C.c_char_p, C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(H)]),
         "lga_step": (C.c_int, [H, C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]),
         "lga_step_host": (C.c_int, [H, C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]),
         "lga_grads": (C.c_int, [H, C.c_void_p, C.c_uint64, C.c_int32]),

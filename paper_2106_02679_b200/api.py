@@ -60,9 +60,32 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr())
 
 
+def torch_allgather(group=None):
+    """An ``lga_allgather_fn`` over torch.distributed (any backend; bytes travel as a Python object): the
+    bootstrap exchange of lga_init (include/lga.h).  Returns the ctypes callback; keep it alive during the call."""
+    import torch.distributed as dist
+
+    def fn(ctx, send, recv, nbytes):
+        try:
+            mine = C.string_at(send, nbytes)
+            out = [None] * dist.get_world_size(group)
+            dist.all_gather_object(out, mine, group=group)
+            blob = b"".join(out)
+            if len(blob) != nbytes * len(out):
+                return 1
+            C.memmove(recv, blob, len(blob))
+            return 0
+        except Exception:   # a Python exception must not cross the C ABI
+            return 1
+
+    return _abi.ALLGATHER_FN(fn)
+
+
 class Trainer:
-    """One rank of the LGA step.  For world > 1, torch.distributed must be initialised (any
-    backend); it is used only to broadcast the NCCL unique id."""
+    """One rank of the LGA step.  For world > 1, torch.distributed must be initialised (any backend): it
+    carries only the bootstrap exchange of lga_init (IPC handles), on a gloo group; every data path runs
+    inside liblga.so over CUDA IPC peer memory.  The NCCL baseline (LGA_FLAG_NCCL_DP) also broadcasts an
+    NCCL unique id.  Several ranks may share one GPU (device = LOCAL_RANK modulo the visible devices)."""
 
     def __init__(self, cfg: Config, rank: int | None = None, world: int | None = None, device: int | None = None,
                  init_params: np.ndarray | None = None, seed: int = 1234, stream=None):
@@ -73,18 +96,22 @@ class Trainer:
         if rank is None:
             rank = int(os.environ.get("RANK", "0"))
         if device is None:
-            device = int(os.environ.get("LOCAL_RANK", str(rank % max(1, torch.cuda.device_count()))))
+            device = int(os.environ.get("LOCAL_RANK", str(rank))) % max(1, torch.cuda.device_count())
         self.rank, self.world, self.device = rank, world, device
         torch.cuda.set_device(device)
         nid = None
+        cb = _abi.ALLGATHER_FN()   # NULL
         if world > 1:
             import torch.distributed as dist
-            buf = C.create_string_buffer(_abi.NCCL_ID_BYTES)
-            if rank == 0:
-                check(lib().lga_nccl_unique_id(buf))
-            obj = [bytes(buf.raw) if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            nid = C.create_string_buffer(obj[0], _abi.NCCL_ID_BYTES)
+            group = None if dist.get_backend() == "gloo" else dist.new_group(backend="gloo")
+            cb = torch_allgather(group)
+            if cfg.dp > 1 and (cfg.flags & _abi.LGA_FLAG_NCCL_DP):
+                buf = C.create_string_buffer(_abi.NCCL_ID_BYTES)
+                if rank == 0:
+                    check(lib().lga_nccl_unique_id(buf))
+                obj = [bytes(buf.raw) if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0, group=group)
+                nid = C.create_string_buffer(obj[0], _abi.NCCL_ID_BYTES)
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
@@ -96,8 +123,8 @@ class Trainer:
                 raise ValueError(f"init_params has {self._init_params.size} floats, expected {tot}")
             ip = self._init_params.ctypes.data_as(C.c_void_p)
         h = C.c_void_p()
-        check(lib().lga_init(C.byref(cfg.to_c()), rank, world, device, nid, C.c_void_p(stream.cuda_stream), ip,
-                             C.c_uint64(seed), C.byref(h)))
+        check(lib().lga_init(C.byref(cfg.to_c()), rank, world, device, cb, None, nid, C.c_void_p(stream.cuda_stream),
+                             ip, C.c_uint64(seed), C.byref(h)))
         self._h = h
         self.stage = rank % cfg.pp
         self.replica = rank // cfg.pp

@@ -263,6 +263,48 @@ void adamw_rs(const void* const* gbase, int64_t goff, int D, DT gdt, float gscal
 #undef AR
 }
 
+// Peer-memory reduction of one slice (fixed rank order p = 0..D-1, fp32 sum of the D peers' staging at
+// gbase[p] + goff, read uncached).  acc != nullptr (STANDARD): acc[i] = (first ? 0 : acc[i]) + sum, the
+// per-micro-batch reduced shard accumulated in fp32.  Otherwise (unpartitioned all-reduce, phase 1 = the
+// reduce-scatter): out[i] = sum in the staging dtype (out is this rank's own slice; it is read by no
+// peer during this phase, so the in-place write is race-free).  n % 4 == 0.
+template <typename GE>
+__global__ void __launch_bounds__(256) peer_reduce_kernel(const void* const* __restrict__ gbase, int64_t goff, int D,
+                                                          float* __restrict__ acc, bool first, GE* __restrict__ out,
+                                                          int64_t n) {
+  const int64_t n4 = n / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float g[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int p = 0; p < D; ++p) {
+      float q[4];
+      ld4_cv(static_cast<const GE*>(gbase[p]) + goff, i, q);
+      g[0] += q[0], g[1] += q[1], g[2] += q[2], g[3] += q[3];
+    }
+    if (acc) {
+      float4 a = first ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<float4*>(acc)[i];
+      a.x += g[0], a.y += g[1], a.z += g[2], a.w += g[3];
+      reinterpret_cast<float4*>(acc)[i] = a;
+    } else if (sizeof(GE) == 4) {
+      reinterpret_cast<float4*>(out)[i] = make_float4(g[0], g[1], g[2], g[3]);
+    } else {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(g[0], g[1]), hi = __floats2bfloat162_rn(g[2], g[3]);
+      reinterpret_cast<uint2*>(out)[i] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    }
+  }
+}
+
+void peer_reduce(const void* const* gbase, int64_t goff, int D, DT gdt, float* acc, bool first, void* out, int64_t n,
+                 cudaStream_t st) {
+  if (n <= 0) return;
+  const int grid = (int)std::min<int64_t>((n / 4 + 255) / 256 + 1, (int64_t)num_sms() * 8);
+  if (gdt == DT::F32)
+    note_launch(), peer_reduce_kernel<float><<<grid, 256, 0, st>>>(gbase, goff, D, acc, first, (float*)out, n);
+  else
+    note_launch(), peer_reduce_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(gbase, goff, D, acc, first,
+                                                                           (__nv_bfloat16*)out, n);
+}
+
 void adamw(const void* gin, DT gdt, float gscale, float* master, float* m, float* v,
            void* param_out, DT pdt, float* keep, int64_t n, float lr, float beta1, float beta2,
            float eps, float wd, const long long* tstep, cudaStream_t st) {
@@ -397,6 +439,74 @@ __global__ void dp_signal_kernel(unsigned long long* const* fbase, int D, int id
 }
 void dp_signal(unsigned long long* const* fbase, int D, int idx, cudaStream_t st) {
   note_launch(), dp_signal_kernel<<<1, 32, 0, st>>>(fbase, D, idx);
+}
+
+// World-wide loss all-reduce over peer memory (replaces a 1-element NCCL all-reduce): thread q stores this
+// rank's loss sum into rank q's ring slot [t mod 4][rank] and bumps q's arrival counter (system-scope
+// release); thread 0 then waits for all `world` arrivals of step t and sums the slots in rank order, so every
+// rank gets the same bits.  Four ring slots: a rank can run at most one step ahead of a peer (every world > 1
+// step has a cross-rank dependency: the data-parallel gathers or the pipeline receives).
+__global__ void loss_allreduce_kernel(double* loss, double* const* ring, unsigned long long* const* wflag, int rank,
+                                      int world, const long long* tstep, const volatile unsigned long long* myflag,
+                                      const volatile double* myring) {
+  const long long t = *tstep;
+  const int slot = (int)(t & 3);
+  const double mine = loss[0];
+  if ((int)threadIdx.x < world) {
+    const int q = threadIdx.x;
+    volatile double* dst = ring[q] + slot * world + rank;
+    *dst = mine;
+    __threadfence_system();
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(wflag[q] + 0), "l"(1ull) : "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long target = (unsigned long long)t * (unsigned long long)world;
+    unsigned long long v;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(myflag) : "memory");
+      if (v >= target) break;
+      __nanosleep(200);
+    }
+    double s = 0.0;
+    for (int r = 0; r < world; ++r) s += myring[slot * world + r];
+    loss[0] = s;
+  }
+}
+void loss_allreduce_peer(double* loss, double* const* ring, unsigned long long* const* wflag, int rank, int world,
+                         const long long* tstep, const unsigned long long* myflag, const double* myring,
+                         cudaStream_t st) {
+  note_launch(), loss_allreduce_kernel<<<1, 32, 0, st>>>(loss, ring, wflag, rank, world, tstep, myflag, myring);
+}
+
+// Device barrier over peer memory: bump every rank's counter wflag[q][1], wait until this rank's counter
+// reaches `target` (= world x barriers so far).  Gives up after timeout_ns (a peer that died must not hang
+// lga_destroy): *timed_out = 1.
+__global__ void world_barrier_kernel(unsigned long long* const* wflag, int world, unsigned long long target,
+                                     const volatile unsigned long long* myflag, int* timed_out, long long timeout_ns) {
+  if ((int)threadIdx.x < world) {
+    __threadfence_system();
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(wflag[threadIdx.x] + 1), "l"(1ull) : "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t0, now, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(myflag) : "memory");
+      if (v >= target) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if ((long long)(now - t0) > timeout_ns) {
+        *timed_out = 1;
+        break;
+      }
+      __nanosleep(1000);
+    }
+  }
+}
+void world_barrier(unsigned long long* const* wflag, int world, unsigned long long target,
+                   const unsigned long long* myflag, int* timed_out, long long timeout_ns, cudaStream_t st) {
+  note_launch(), world_barrier_kernel<<<1, 32, 0, st>>>(wflag, world, target, myflag, timed_out, timeout_ns);
 }
 
 // the step counter t (AdamW bias corrections, flag epochs): incremented first thing in every step

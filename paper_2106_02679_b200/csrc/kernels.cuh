@@ -132,5 +132,16 @@ void adamw_rs(const void* const* gbase, int64_t goff, int D, DT gdt, float gscal
               void* param_out, DT pdt, float* keep, int64_t n, float lr, float beta1, float beta2, float eps, float wd,
               const long long* tstep, cudaStream_t st);
 void dp_signal(unsigned long long* const* fbase, int D, int idx, cudaStream_t st);
+// fixed-order fp32 sum of one slice of the D peers' staging buffers: into acc (STANDARD: acc = (first ? 0 : acc)
+// + sum) or, acc == nullptr, into out in the staging dtype (unpartitioned all-reduce, reduce-scatter phase)
+void peer_reduce(const void* const* gbase, int64_t goff, int D, DT gdt, float* acc, bool first, void* out, int64_t n,
+                 cudaStream_t st);
+// loss[0] = sum over the world's ranks (rank order) of their loss[0], over peer memory (ring of 4 step slots)
+void loss_allreduce_peer(double* loss, double* const* ring, unsigned long long* const* wflag, int rank, int world,
+                         const long long* tstep, const unsigned long long* myflag, const double* myring,
+                         cudaStream_t st);
+// device barrier over peer memory (wflag[q][1] counters), bounded by timeout_ns (*timed_out = 1 on expiry)
+void world_barrier(unsigned long long* const* wflag, int world, unsigned long long target,
+                   const unsigned long long* myflag, int* timed_out, long long timeout_ns, cudaStream_t st);
 
 }  // namespace lga

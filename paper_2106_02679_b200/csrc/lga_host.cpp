@@ -72,7 +72,8 @@ struct Cfg {
   bool retain, no_comm, profile;
   bool keep, norecomp, unpart, contig;   // LGA_FLAG_KEEP_PARAMS / NO_RECOMPUTE / UNPARTITIONED / CONTIGUOUS_PP
   bool graph_off;                        // LGA_FLAG_NO_GRAPH
-  bool dp_ipc;                           // DP all-gather / reduce-scatter over NVLink peer memory (not NCCL)
+  bool dp_ipc;                           // D > 1: all-gather / reduce-scatter / all-reduce over peer memory
+  bool nccl_dp;                          // D > 1 with LGA_FLAG_NCCL_DP: the NCCL baseline
   bool post_ln;                          // LGA_FLAG_POST_LN (reading A-16)
   // canonical offsets
   int64_t o_ln1w, o_ln1b, o_wqkv, o_bqkv, o_wo, o_bo, o_ln2w, o_ln2b, o_w1, o_b1, o_w2, o_b2;
@@ -125,8 +126,9 @@ static lga_status validate(const lga_config* c, int world, Cfg* out) {
   g.graph_off = (c->flags & LGA_FLAG_NO_GRAPH) != 0;
   g.bf16 = c->precision == LGA_BF16;
   g.layered = c->schedule == LGA_LAYERED;
-  // N1: partitioned LAYERED data parallelism over peer memory unless LGA_FLAG_NCCL_DP asks for NCCL
-  g.dp_ipc = g.D > 1 && g.layered && !g.unpart && !(c->flags & LGA_FLAG_NCCL_DP);
+  // N1: data parallelism over peer memory (every schedule and variant) unless LGA_FLAG_NCCL_DP asks for NCCL
+  g.nccl_dp = g.D > 1 && (c->flags & LGA_FLAG_NCCL_DP) != 0;
+  g.dp_ipc = g.D > 1 && !g.nccl_dp;
   g.post_ln = (c->flags & LGA_FLAG_POST_LN) != 0;
   g.causal = c->causal != 0;
   g.E = g.bf16 ? DT::BF16 : DT::F32;
@@ -159,13 +161,24 @@ struct Arena {
   void* take_bytes(size_t bytes) { return take<char>(bytes); }
 };
 
+// What a rank publishes about its arena at the bootstrap (exchanged with the caller's all-gather)
 struct PeerInfo {
   cudaIpcMemHandle_t handle;
   uint64_t off_ckpt, off_dY, off_flags;   // pipeline
   uint64_t off_gst, off_psh, off_dpf;     // data parallelism over peer memory (N1)
-  uint64_t pad[2];
+  uint64_t off_master, off_gkeep;         // lga_params / lga_grads read the replicas' shards
+  uint64_t off_wflags, off_loss;          // world counters (loss all-reduce, barrier), loss ring
+  int32_t rank, world;                    // consistency check
+  uint64_t pad;
 };
 static_assert(sizeof(PeerInfo) % 16 == 0, "PeerInfo size");
+
+// Per-layer peer counters of the data-parallel group, dpf[kind * Lloc + j], each bumped by every replica:
+//   GRAD  "my gradient of layer j is staged"        PARAM "my shard j is updated"
+//   READ  "I read the shards of layer j" (gathers; unpartitioned: "I read the reduced slices")
+//   RED   "my reduced slice of layer j is ready"    (unpartitioned all-reduce, between its two phases)
+//   GREAD "I read my slice of your staging j"       (STANDARD: staging j is rewritten every micro-batch)
+enum { DPF_GRAD = 0, DPF_PARAM = 1, DPF_READ = 2, DPF_RED = 3, DPF_GREAD = 4, DPF_KINDS = 5 };
 
 // Forward intermediates of a chunk that the backward reads (pointers at the chunk's first token).
 struct Ws {
@@ -197,12 +210,25 @@ struct lga_handle {
   float* gacc = nullptr;
   void* gstage[2] = {nullptr, nullptr};   // staging of the reduced-precision layer gradient (alternating layers)
   void* gst_layers = nullptr;             // dp_ipc: one staging buffer per local layer [Lloc][plpad]
-  // dp_ipc: per-layer counters [3][Lloc] (gradient staged / shard updated / shard read), written by peers
+  // dp_ipc: per-layer counters [DPF_KINDS][Lloc] (gradient staged / shard updated / shard read / reduced slice
+  // ready / staging read), written by the peers
   unsigned long long* dpf = nullptr;
   void** dp_gst_dev = nullptr;                   // device [D]: every DP peer's staging base (replica order)
   unsigned long long** dp_flag_dev = nullptr;    // device [D]: every DP peer's dpf
   std::vector<char*> dp_base;                    // host: IPC-mapped arena base of every DP peer (self: own)
   std::vector<char*> dp_psh;                     // host: every DP peer's pshard
+  // world (bootstrap, loss all-reduce, barriers): every rank's arena mapped over CUDA IPC (self: own base)
+  std::vector<char*> wbase;
+  std::vector<PeerInfo> peers;
+  bool connected = false;                        // every rank's arena mapped (world > 1)
+  bool ready = false;                            // lga_init completed
+  bool stepped = false;                          // ev_t1 recorded at least once
+  unsigned long long* wflags = nullptr;          // [0] loss arrivals, [1] barrier arrivals (written by peers)
+  double* loss_ring = nullptr;                   // [4][world] loss slots (written by peers)
+  unsigned long long** w_flag_dev = nullptr;     // device [world]: every rank's wflags
+  double** w_loss_dev = nullptr;                 // device [world]: every rank's loss_ring
+  int* barrier_to = nullptr;                     // device: barrier timed out
+  unsigned long long n_barrier = 0;              // barriers so far (collective, the same on every rank)
   // activations
   float* ckpt = nullptr;  // [Lloc][N][M][d]
   float* yout = nullptr;  // [N][M][d] on the stage owning layer L-1
@@ -218,8 +244,6 @@ struct lga_handle {
   float *xin = nullptr, *tin = nullptr;  // device copies for lga_step_host
   unsigned long long* flags = nullptr;   // [0] fwd receive count, [1] bwd receive count
   // pipeline peers
-  char* peer_next_base = nullptr;  // stage (s+1) mod P of my replica
-  char* peer_prev_base = nullptr;  // stage (s-1) mod P
   float *next_ckpt = nullptr, *prev_dY = nullptr;
   unsigned long long *next_flags = nullptr, *prev_flags = nullptr;
   unsigned long long sent_fwd = 0, sent_bwd = 0, recv_fwd = 0, recv_bwd = 0;   // this step's transfers so far
@@ -286,7 +310,7 @@ static void plan_arena(lga_handle* h) {
   h->gacc = A.take<float>(c.plpad);
   if (c.dp_ipc) {   // a layer's staged gradient stays readable by the peers until the next step
     h->gst_layers = A.take_bytes(Ll * c.plpad * dt_size(c.G));
-    h->dpf = A.take<unsigned long long>(3 * Ll);
+    h->dpf = A.take<unsigned long long>(DPF_KINDS * Ll);
     h->dp_gst_dev = A.take<void*>(c.D);
     h->dp_flag_dev = A.take<unsigned long long*>(c.D);
   } else {
@@ -334,6 +358,13 @@ static void plan_arena(lga_handle* h) {
   h->tin = A.take<float>(act);
   h->flags = A.take<unsigned long long>(8);
   h->tstep = A.take<long long>(1);
+  if (h->world > 1) {
+    h->wflags = A.take<unsigned long long>(16);
+    h->loss_ring = A.take<double>(4 * (int64_t)h->world);
+    h->w_flag_dev = A.take<unsigned long long*>(h->world);
+    h->w_loss_dev = A.take<double*>(h->world);
+    h->barrier_to = A.take<int>(4);
+  }
 }
 
 // timing events: plain records, or event-record nodes (cudaEventRecordExternal) inside a step capture
@@ -810,7 +841,6 @@ static const void* layer_weights(lga_handle* h, int j, int slot) {
   return eoff(h->pshard, h->c.E, (int64_t)j * h->c.S);   // D == 1 or unpartitioned: the local full layer
 }
 
-enum { DPF_GRAD = 0, DPF_PARAM = 1, DPF_READ = 2 };   // dpf[kind * Lloc + j]
 
 static void all_gather(lga_handle* h, int j, int slot) {
   const Cfg& c = h->c;
@@ -906,6 +936,82 @@ static void rs_adam_peer(lga_handle* h, int j) {
   if (!c.no_comm) {
     dp_signal(h->dp_flag_dev, c.D, DPF_PARAM * c.Lloc + j, h->s_comm);
     KCHECK();
+  }
+}
+
+// N2b over peer memory: the all-reduce of layer j's gradient as a reduce-scatter then an all-gather (the
+// bandwidth-optimal 2 (D-1)/D of the layer per rank), then AdamW on the whole layer (every replica holds
+// the full state).  (1) announce the staged gradient, wait for all D; (2) sum slice r of the D staging buffers in
+// fixed rank order into this rank's own slice r (no peer reads slice r of this rank in this phase); (3) announce
+// the reduced slice, wait for all D; (4) copy the D-1 other reduced slices from their owners (copy engines) and
+// announce the reads, which the next step's backward of layer j waits for before it rewrites the staging.
+static void allreduce_adam_peer(lga_handle* h, int j) {
+  const Cfg& c = h->c;
+  const int64_t Sr = c.plpad / c.D;   // slice of the reduce-scatter phase
+  const size_t eg = dt_size(c.G);
+  h->last.allreduce_calls++;
+  h->last.allreduce_bytes += 2ull * (c.D - 1) * (uint64_t)Sr * eg;
+  void* gs = stage_buf(h, j);
+  if (!c.no_comm) {
+    const unsigned long long D = (unsigned long long)c.D;
+    dp_signal(h->dp_flag_dev, c.D, DPF_GRAD * c.Lloc + j, h->s_comm);
+    KCHECK();
+    wait_flag(h->dpf + DPF_GRAD * c.Lloc + j, h->tstep, D, D, h->s_comm);
+    KCHECK();
+    const int64_t goff = (int64_t)j * c.plpad + (int64_t)h->replica * Sr;
+    peer_reduce(h->dp_gst_dev, goff, c.D, c.G, nullptr, false, eoff(gs, c.G, (int64_t)h->replica * Sr), Sr, h->s_comm);
+    KCHECK();
+    dp_signal(h->dp_flag_dev, c.D, DPF_RED * c.Lloc + j, h->s_comm);
+    KCHECK();
+    wait_flag(h->dpf + DPF_RED * c.Lloc + j, h->tstep, D, D, h->s_comm);
+    KCHECK();
+    for (int p = 0; p < c.D; ++p) {
+      if (p == h->replica) continue;
+      const int64_t o = (int64_t)p * Sr;
+      const char* src = h->dp_base[p] + h->peers[p * c.P + h->stage].off_gst + ((int64_t)j * c.plpad + o) * eg;
+      CK(cudaMemcpyAsync(eoff(gs, c.G, o), src, (size_t)Sr * eg, cudaMemcpyDeviceToDevice, h->s_comm));
+    }
+    dp_signal(h->dp_flag_dev, c.D, DPF_READ * c.Lloc + j, h->s_comm);
+    KCHECK();
+  }
+  adam_layer(h, j, gs, c.G);
+}
+
+// STANDARD over peer memory: micro-batch m's gradient of layer j is reduce-scattered into this
+// rank's fp32 shard accumulator (fixed rank order, (re)started at m = 0); the peers then announce that they read
+// their slice of this rank's staging j (the next micro-batch's backward waits for that before rewriting it).
+// After the last micro-batch: wait until every replica has done all of this step's 2 N gathers of shard j, then
+// AdamW and announce the updated shard.
+static void rs_acc_peer(lga_handle* h, int j, int m) {
+  const Cfg& c = h->c;
+  h->last.rs_calls++;
+  h->last.rs_bytes += (uint64_t)(c.D - 1) * c.S * dt_size(c.G);
+  const unsigned long long D = (unsigned long long)c.D, N = (unsigned long long)c.N;
+  float* acc = h->gshard_acc + (int64_t)j * c.S;
+  if (!c.no_comm) {
+    dp_signal(h->dp_flag_dev, c.D, DPF_GRAD * c.Lloc + j, h->s_comm);
+    KCHECK();
+    wait_flag(h->dpf + DPF_GRAD * c.Lloc + j, h->tstep, D * N, D * (unsigned long long)(m + 1), h->s_comm);
+    KCHECK();
+    peer_reduce(h->dp_gst_dev, (int64_t)j * c.plpad + (int64_t)h->replica * c.S, c.D, c.G, acc, m == 0, nullptr, c.S,
+                h->s_comm);
+    KCHECK();
+    dp_signal(h->dp_flag_dev, c.D, DPF_GREAD * c.Lloc + j, h->s_comm);
+    KCHECK();
+  } else {
+    shard_accumulate(eoff(stage_buf(h, j), c.G, (int64_t)h->replica * c.S), c.G, acc, c.S, m == 0, h->s_comm);
+    KCHECK();
+  }
+  if (m == c.N - 1) {
+    if (!c.no_comm) {
+      wait_flag(h->dpf + DPF_READ * c.Lloc + j, h->tstep, 2 * N * D, 2 * N * D, h->s_comm);
+      KCHECK();
+    }
+    adam_layer(h, j, acc, DT::F32);
+    if (!c.no_comm) {
+      dp_signal(h->dp_flag_dev, c.D, DPF_PARAM * c.Lloc + j, h->s_comm);
+      KCHECK();
+    }
   }
 }
 
@@ -1055,6 +1161,12 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
       count_wait_end(h);
     }
     if (!c.dp_ipc && h->rec_adam[gb]) CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));   // staging gb free again
+    if (c.dp_ipc && c.unpart && !c.no_comm) {   // every replica read last step's reduced slices of staging j
+      count_wait(h, nullptr, 0);
+      wait_flag(h->dpf + DPF_READ * c.Lloc + j, h->tstep, (unsigned long long)c.D, 0ull, h->s_comp);
+      KCHECK();
+      count_wait_end(h);
+    }
     const void* W = layer_weights(h, j, sl);
     const bool recv = c.P > 1 && i < c.L - 1 && stage_of(c, i + 1) != h->stage;   // dY_i from another stage
     const bool send = c.P > 1 && i > 0 && stage_of(c, i - 1) != h->stage;         // dX_i to another stage
@@ -1103,7 +1215,8 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
     CK(cudaEventRecord(h->ev_grad[gb], h->s_comp));
     CK(cudaStreamWaitEvent(h->s_comm, h->ev_grad[gb], 0));
     if (c.dp_ipc) {
-      rs_adam_peer(h, j);
+      if (c.unpart) allreduce_adam_peer(h, j);
+      else rs_adam_peer(h, j);
     } else {
       void* shard_g = reduce_scatter(h, j);
       adam_layer(h, j, shard_g, c.G);
@@ -1163,7 +1276,14 @@ static void step_standard(lga_handle* h, const float* x, const float* T) {
         count_wait(h, h->ev_ag[sl], 0);
         count_wait_end(h);
       }
-      if (h->rec_adam[gb]) CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));
+      if (!c.dp_ipc && h->rec_adam[gb]) CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));
+      if (c.dp_ipc && !c.no_comm) {   // every replica read its slice of the previous micro-batch's staging j
+        count_wait(h, nullptr, 0);
+        wait_flag(h->dpf + DPF_GREAD * c.Lloc + j, h->tstep, (unsigned long long)c.D * c.N, (unsigned long long)c.D * m,
+                  h->s_comp);
+        KCHECK();
+        count_wait_end(h);
+      }
       const void* W = layer_weights(h, j, sl);
       const float* xin = j == 0 ? x + m * mb : ckpt_ptr(h, j, m);
       float* dYc = act_ptr(h->dY, c, m);
@@ -1174,12 +1294,15 @@ static void step_standard(lga_handle* h, const float* x, const float* T) {
       { CK(cudaEventRecord(h->ev_slot_free[sl], h->s_comp)); h->rec_slot[sl] = 1; }
       CK(cudaEventRecord(h->ev_grad[gb], h->s_comp));
       CK(cudaStreamWaitEvent(h->s_comm, h->ev_grad[gb], 0));
-      // reduce-scatter this micro-batch's gradient, accumulate it on the shard (fixed order over m)
-      void* shard_g = reduce_scatter(h, j);
-      float* acc = h->gshard_acc + (int64_t)j * c.S;
-      shard_accumulate(shard_g, c.G, acc, c.S, m == 0, h->s_comm);
-      KCHECK();
-      if (m == c.N - 1) adam_layer(h, j, acc, DT::F32);
+      if (c.dp_ipc) {
+        rs_acc_peer(h, j, m);
+      } else {   // reduce-scatter this micro-batch's gradient, accumulate it on the shard (fixed order over m)
+        void* shard_g = reduce_scatter(h, j);
+        float* acc = h->gshard_acc + (int64_t)j * c.S;
+        shard_accumulate(shard_g, c.G, acc, c.S, m == 0, h->s_comm);
+        KCHECK();
+        if (m == c.N - 1) adam_layer(h, j, acc, DT::F32);
+      }
       { CK(cudaEventRecord(h->ev_adam[gb], h->s_comm)); h->rec_adam[gb] = true; }
     }
   }
@@ -1242,48 +1365,69 @@ lga_status lga_nccl_unique_id(uint8_t* out) {
   return LGA_OK;
 }
 
+// Device barrier of all world ranks over peer memory (collective; every rank calls it in the same order).
+// Returns false if it timed out (a peer never arrived).
+static bool world_sync(lga_handle* h, double timeout_s) {
+  if (h->world <= 1 || !h->connected) return true;
+  h->n_barrier += 1;
+  CK(cudaMemsetAsync(h->barrier_to, 0, sizeof(int), h->s_comp));
+  world_barrier(h->w_flag_dev, h->world, h->n_barrier * (unsigned long long)h->world, h->wflags + 1, h->barrier_to,
+                (long long)(timeout_s * 1e9), h->s_comp);
+  KCHECK();
+  int to = 0;
+  CK(cudaMemcpyAsync(&to, h->barrier_to, sizeof(int), cudaMemcpyDeviceToHost, h->s_comp));
+  CK(cudaStreamSynchronize(h->s_comp));
+  return to == 0;
+}
+
 static void free_handle(lga_handle* h) {
   if (!h) return;
   cudaSetDevice(h->dev);
+  if (h->stepped && h->ev_t1) cudaEventSynchronize(h->ev_t1);   // the last step (graph replays run on the caller stream)
   if (h->s_comp) cudaStreamSynchronize(h->s_comp);
   if (h->s_comm) cudaStreamSynchronize(h->s_comm);
   if (h->s_copy) cudaStreamSynchronize(h->s_copy);
+  // peers write into this arena (pipeline transfers, counters, loss slots): free it only after every rank is done
+  if (h->ready && h->connected && !h->bad) {
+    try {
+      world_sync(h, 60.0);
+    } catch (...) {
+    }
+  }
+  cudaGetLastError();
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
-  if (h->peer_next_base) cudaIpcCloseMemHandle(h->peer_next_base);
-  if (h->peer_prev_base && h->peer_prev_base != h->peer_next_base) cudaIpcCloseMemHandle(h->peer_prev_base);
-  for (char* b : h->dp_base)
-    if (b && b != h->arena.base) cudaIpcCloseMemHandle(b);
+  for (size_t q = 0; q < h->wbase.size(); ++q)
+    if (h->wbase[q] && h->wbase[q] != h->arena.base) cudaIpcCloseMemHandle(h->wbase[q]);
   if (h->dp_comm) ncclCommDestroy(h->dp_comm);
   if (h->world_comm) ncclCommDestroy(h->world_comm);
   cudaEvent_t evs[] = {h->ev_in, h->ev_tin, h->ev_grad[0], h->ev_grad[1], h->ev_adam[0], h->ev_adam[1], h->ev_comm_end,
                        h->ev_comp_end, h->ev_t0, h->ev_t1, h->ev_fwd_end};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
-  for (auto e : h->ev_ag)
-    if (e) cudaEventDestroy(e);
-  for (auto e : h->ev_x)
-    if (e) cudaEventDestroy(e);
-  for (auto e : h->ev_slot_free)
-    if (e) cudaEventDestroy(e);
-  for (auto e : h->ev_wait0) cudaEventDestroy(e);
-  for (auto e : h->ev_wait1) cudaEventDestroy(e);
+  for (auto* v : {&h->ev_ag, &h->ev_x, &h->ev_slot_free, &h->ev_wait0, &h->ev_wait1, &h->prof0, &h->prof1})
+    for (auto e : *v)
+      if (e) cudaEventDestroy(e);
   if (h->s_comp) cudaStreamDestroy(h->s_comp);
   if (h->s_comm) cudaStreamDestroy(h->s_comm);
   if (h->s_copy) cudaStreamDestroy(h->s_copy);
   if (h->arena.base) cudaFree(h->arena.base);
   if (h->loss_host) cudaFreeHost(h->loss_host);
+  cudaGetLastError();
   delete h;
 }
 
-lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t device, const uint8_t* nccl_id,
-                    uintptr_t cuda_stream, const float* init_params, uint64_t seed, lga_handle** out) {
+lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t device, lga_allgather_fn allgather,
+                    void* allgather_ctx, const uint8_t* nccl_id, uintptr_t cuda_stream, const float* init_params,
+                    uint64_t seed, lga_handle** out) {
   if (!out) return ERR(LGA_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   Cfg c;
   lga_status s = validate(cfg, world, &c);
   if (s != LGA_OK) return s;
   if (rank < 0 || rank >= world) return ERR(LGA_ERR_INVALID_ARG, "rank %d out of [0, %d)", rank, world);
-  if (world > 1 && !nccl_id) return ERR(LGA_ERR_INVALID_ARG, "nccl_id is NULL with world %d", world);
+  if (world > 1 && !allgather && !nccl_id)
+    return ERR(LGA_ERR_INVALID_ARG, "world %d needs a bootstrap: an allgather callback or an nccl_id", world);
+  if (c.nccl_dp && !nccl_id) return ERR(LGA_ERR_INVALID_ARG, "LGA_FLAG_NCCL_DP with dp > 1 needs nccl_id");
   lga_handle* h = new lga_handle();
   h->c = c;
   h->rank = rank;
@@ -1336,14 +1480,12 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
   plan_arena(h);
   CK(cudaMemsetAsync(h->arena.base, 0, need, h->s_comp));
   CK(cudaMallocHost(&h->loss_host, 8 * sizeof(double)));
-  // communicators: world (loss all-reduce, handle exchange) and the stage's DP group
-  if (world > 1) {
+  // NCCL only for the baseline (LGA_FLAG_NCCL_DP) or, without an allgather callback, for the bootstrap exchange
+  if (world > 1 && nccl_id) {
     ncclUniqueId id;
     memcpy(&id, nccl_id, sizeof(id));
     NK(ncclCommInitRank(&h->world_comm, world, id, rank));
-    if (c.D > 1) {
-      NK(ncclCommSplit(h->world_comm, h->stage, h->replica, &h->dp_comm, nullptr));
-    }
+    if (c.nccl_dp) NK(ncclCommSplit(h->world_comm, h->stage, h->replica, &h->dp_comm, nullptr));
   }
   // parameters: fp32 master shard of each local layer (A-10: contiguous 1/D slice of the padded layer)
   const int64_t Ll = c.Lloc;
@@ -1371,64 +1513,89 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
     cast_f32(h->master, h->pshard, c.E, Ll * c.S, h->s_comp);
     KCHECK();
   }
-  // pipeline / data-parallel peers: exchange IPC handles over the world communicator
-  if (c.P > 1 || c.dp_ipc) {
+  // bootstrap (world > 1): exchange every rank's arena IPC handle and offsets, map all of them.  The arena is
+  // zeroed and synchronised above, so once a rank holds every handle, every peer's counters are initialised.
+  if (world > 1) {
+    CK(cudaStreamSynchronize(h->s_comp));
     PeerInfo me{};
     CK(cudaIpcGetMemHandle(&me.handle, h->arena.base));
-    me.off_ckpt = (uint64_t)((char*)h->ckpt - h->arena.base);
-    me.off_dY = (uint64_t)((char*)h->dY - h->arena.base);
-    me.off_flags = (uint64_t)((char*)h->flags - h->arena.base);
-    if (c.dp_ipc) {
-      me.off_gst = (uint64_t)((char*)h->gst_layers - h->arena.base);
-      me.off_psh = (uint64_t)((char*)h->pshard - h->arena.base);
-      me.off_dpf = (uint64_t)((char*)h->dpf - h->arena.base);
+    auto off = [&](const void* p) { return p ? (uint64_t)((const char*)p - h->arena.base) : 0ull; };
+    me.off_ckpt = off(h->ckpt);
+    me.off_dY = off(h->dY);
+    me.off_flags = off(h->flags);
+    me.off_gst = off(h->gst_layers);
+    me.off_psh = off(h->pshard);
+    me.off_dpf = off(h->dpf);
+    me.off_master = off(h->master);
+    me.off_gkeep = off(h->gkeep);
+    me.off_wflags = off(h->wflags);
+    me.off_loss = off(h->loss_ring);
+    me.rank = rank;
+    me.world = world;
+    std::vector<PeerInfo>& all = h->peers;
+    all.assign(world, PeerInfo{});
+    if (allgather) {
+      if (allgather(allgather_ctx, &me, all.data(), sizeof(PeerInfo)) != 0) {
+        ERR(LGA_ERR_INVALID_ARG, "the allgather callback failed");
+        throw StatusError{LGA_ERR_INVALID_ARG};
+      }
+    } else {
+      PeerInfo* dev_info = nullptr;
+      CK(cudaMalloc(&dev_info, sizeof(PeerInfo) * (world + 1)));
+      CK(cudaMemcpy(dev_info + world, &me, sizeof(me), cudaMemcpyHostToDevice));
+      NK(ncclAllGather(dev_info + world, dev_info, sizeof(PeerInfo), ncclUint8, h->world_comm, h->s_comp));
+      CK(cudaMemcpyAsync(all.data(), dev_info, sizeof(PeerInfo) * world, cudaMemcpyDeviceToHost, h->s_comp));
+      CK(cudaStreamSynchronize(h->s_comp));
+      CK(cudaFree(dev_info));
     }
-    PeerInfo* dev_info = nullptr;
-    CK(cudaMalloc(&dev_info, sizeof(PeerInfo) * (world + 1)));
-    CK(cudaMemcpy(dev_info + world, &me, sizeof(me), cudaMemcpyHostToDevice));
-    NK(ncclAllGather(dev_info + world, dev_info, sizeof(PeerInfo), ncclUint8, h->world_comm, h->s_comp));
-    std::vector<PeerInfo> all(world);
-    CK(cudaMemcpyAsync(all.data(), dev_info, sizeof(PeerInfo) * world, cudaMemcpyDeviceToHost, h->s_comp));
-    CK(cudaStreamSynchronize(h->s_comp));
-    CK(cudaFree(dev_info));
+    for (int q = 0; q < world; ++q)
+      if (all[q].rank != q || all[q].world != world) {
+        ERR(LGA_ERR_INVALID_ARG, "bootstrap: slot %d holds rank %d of world %d", q, all[q].rank, all[q].world);
+        throw StatusError{LGA_ERR_INVALID_ARG};
+      }
+    h->wbase.assign(world, nullptr);
+    for (int q = 0; q < world; ++q) {
+      if (q == rank) {
+        h->wbase[q] = h->arena.base;
+        continue;
+      }
+      void* pb = nullptr;
+      CK(cudaIpcOpenMemHandle(&pb, all[q].handle, cudaIpcMemLazyEnablePeerAccess));
+      h->wbase[q] = (char*)pb;
+    }
+    h->connected = true;
+    std::vector<unsigned long long*> wf(world);
+    std::vector<double*> wl(world);
+    for (int q = 0; q < world; ++q) {
+      wf[q] = (unsigned long long*)(h->wbase[q] + all[q].off_wflags);
+      wl[q] = (double*)(h->wbase[q] + all[q].off_loss);
+    }
+    CK(cudaMemcpy(h->w_flag_dev, wf.data(), world * sizeof(void*), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->w_loss_dev, wl.data(), world * sizeof(void*), cudaMemcpyHostToDevice));
     if (c.P > 1) {
       const int next = h->replica * c.P + (h->stage + 1) % c.P;
       const int prev = h->replica * c.P + (h->stage + c.P - 1) % c.P;
-      void* pn = nullptr;
-      CK(cudaIpcOpenMemHandle(&pn, all[next].handle, cudaIpcMemLazyEnablePeerAccess));
-      h->peer_next_base = (char*)pn;
-      if (prev == next) {
-        h->peer_prev_base = h->peer_next_base;
-      } else {
-        void* pp = nullptr;
-        CK(cudaIpcOpenMemHandle(&pp, all[prev].handle, cudaIpcMemLazyEnablePeerAccess));
-        h->peer_prev_base = (char*)pp;
-      }
-      h->next_ckpt = (float*)(h->peer_next_base + all[next].off_ckpt);
-      h->next_flags = (unsigned long long*)(h->peer_next_base + all[next].off_flags);
-      h->prev_dY = (float*)(h->peer_prev_base + all[prev].off_dY);
-      h->prev_flags = (unsigned long long*)(h->peer_prev_base + all[prev].off_flags);
+      h->next_ckpt = (float*)(h->wbase[next] + all[next].off_ckpt);
+      h->next_flags = (unsigned long long*)(h->wbase[next] + all[next].off_flags);
+      h->prev_dY = (float*)(h->wbase[prev] + all[prev].off_dY);
+      h->prev_flags = (unsigned long long*)(h->wbase[prev] + all[prev].off_flags);
     }
-    if (c.dp_ipc) {  // the replicas of this stage, in replica order (self: own arena)
+    if (c.D > 1) {  // the replicas of this stage, in replica order (self: own arena)
       h->dp_base.assign(c.D, nullptr);
       h->dp_psh.assign(c.D, nullptr);
       std::vector<void*> gst(c.D);
       std::vector<unsigned long long*> fl(c.D);
       for (int r = 0; r < c.D; ++r) {
         const int q = r * c.P + h->stage;
-        char* base = h->arena.base;
-        if (q != rank) {
-          void* pb = nullptr;
-          CK(cudaIpcOpenMemHandle(&pb, all[q].handle, cudaIpcMemLazyEnablePeerAccess));
-          base = (char*)pb;
-        }
-        h->dp_base[r] = base;
-        h->dp_psh[r] = base + all[q].off_psh;
-        gst[r] = base + all[q].off_gst;
-        fl[r] = (unsigned long long*)(base + all[q].off_dpf);
+        h->dp_base[r] = h->wbase[q];
+        h->dp_psh[r] = h->wbase[q] + all[q].off_psh;
+        gst[r] = h->wbase[q] + all[q].off_gst;
+        fl[r] = (unsigned long long*)(h->wbase[q] + all[q].off_dpf);
       }
-      CK(cudaMemcpy(h->dp_gst_dev, gst.data(), c.D * sizeof(void*), cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(h->dp_flag_dev, fl.data(), c.D * sizeof(unsigned long long*), cudaMemcpyHostToDevice));
+      if (c.dp_ipc) {
+        CK(cudaMemcpy(h->dp_gst_dev, gst.data(), c.D * sizeof(void*), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->dp_flag_dev, fl.data(), c.D * sizeof(unsigned long long*), cudaMemcpyHostToDevice));
+      }
     }
   }
   CK(cudaStreamSynchronize(h->s_comp));
@@ -1436,14 +1603,16 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
   CK(cudaEventRecord(h->ev_adam[0], h->s_comm));
   CK(cudaEventRecord(h->ev_adam[1], h->s_comm));
   for (auto e : h->ev_slot_free) CK(cudaEventRecord(e, h->s_comp));
-  if (world > 1) {  // all ranks' arenas are initialised before anyone writes into a peer
-    double* tmp = h->loss_dev;
-    NK(ncclAllReduce(tmp, tmp, 1, ncclFloat64, ncclSum, h->world_comm, h->s_comp));
-    CK(cudaStreamSynchronize(h->s_comp));
-  }
+  h->ready = true;
   *out = h;
   return LGA_OK;
-  ABI_CATCH
+  } catch (const StatusError& e) {   // free everything allocated so far; *out stays NULL
+    free_handle(h);
+    return e.s;
+  } catch (...) {
+    free_handle(h);
+    return ERR(LGA_ERR_CUDA, "unexpected exception in lga_init");
+  }
 }
 
 // Issue one step on s_comp / s_comm / s_copy: from "s_comp, s_comm start after ev_in" to "s_comp has joined
@@ -1473,11 +1642,14 @@ static void issue_step(lga_handle* h, const float* x, const float* T, bool host_
         CK(cudaEventRecord(h->ev_x[m], h->s_copy));
       }
       h->x_split = true;
-    } else if (need_x) {
-      CK(cudaMemcpyAsync(h->xin, x, act * sizeof(float), cudaMemcpyHostToDevice, h->s_comp));
+    } else if (need_x) {   // on s_copy too, so that the end-of-call sync of s_copy covers every host read
+      CK(cudaStreamWaitEvent(h->s_copy, h->ev_in, 0));
+      CK(cudaMemcpyAsync(h->xin, x, act * sizeof(float), cudaMemcpyHostToDevice, h->s_copy));
+      CK(cudaEventRecord(h->ev_x[0], h->s_copy));
+      CK(cudaStreamWaitEvent(h->s_comp, h->ev_x[0], 0));
     }
     if (need_t) {  // needed only at the loss: copy on s_copy, overlapped with the forward
-      if (!h->x_split) CK(cudaStreamWaitEvent(h->s_copy, h->ev_in, 0));
+      if (!need_x) CK(cudaStreamWaitEvent(h->s_copy, h->ev_in, 0));
       CK(cudaMemcpyAsync(h->tin, T, act * sizeof(float), cudaMemcpyHostToDevice, h->s_copy));
       CK(cudaEventRecord(h->ev_tin, h->s_copy));
       h->tin_pending = true;
@@ -1494,7 +1666,11 @@ static void issue_step(lga_handle* h, const float* x, const float* T, bool host_
   mse_finish(h->loss_dev + 1, c.N, 1.0, h->loss_dev, h->s_comp);
   KCHECK();
   h->last.allreduce_calls += 1;   // the loss (plus, unpartitioned, the per-layer gradient all-reduces)
-  if (h->world > 1 && !c.no_comm) NK(ncclAllReduce(h->loss_dev, h->loss_dev, 1, ncclFloat64, ncclSum, h->world_comm, h->s_comp));
+  if (h->world > 1 && !c.no_comm) {   // over peer memory (every rank gets the same rank-order sum)
+    loss_allreduce_peer(h->loss_dev, h->w_loss_dev, h->w_flag_dev, h->rank, h->world, h->tstep, h->wflags + 0,
+                        h->loss_ring, h->s_comp);
+    KCHECK();
+  }
   CK(cudaMemcpyAsync(h->loss_host, h->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, h->s_comp));
   CK(cudaEventRecord(h->ev_comm_end, h->s_comm));
   CK(cudaStreamWaitEvent(h->s_comp, h->ev_comm_end, 0));
@@ -1578,6 +1754,8 @@ static lga_status run_step(lga_handle* h, const float* x, const float* T, double
     h->eager_steps += 1;
   }
   CK(cudaEventRecord(h->ev_t1, h->user));
+  h->stepped = true;
+  if (host_inputs) CK(cudaStreamSynchronize(h->s_copy));   // the caller may reuse x / target on return
   h->last.steps = 1;
   lga_comm_stats& tt = h->total;
   tt.steps += 1;
@@ -1602,7 +1780,11 @@ lga_status lga_step_host(lga_handle* h, const float* x, const float* target, dou
   return run_step(h, x, target, loss_out, true);
 }
 
-static lga_status gather_state(lga_handle* h, const float* src_shards, float* out, uint64_t n, int32_t on_device) {
+// lga_grads / lga_params: this rank's stage layers in canonical layout.  The D replicas' shards are read over
+// peer memory between two world barriers (every peer finished its last step before the reads; nobody starts
+// the next step, which rewrites master / m / v, before every rank has read).
+static lga_status gather_state(lga_handle* h, const float* src_shards, uint64_t peer_off, float* out, uint64_t n,
+                               int32_t on_device) {
   if (!h) return ERR(LGA_ERR_INVALID_ARG, "handle is NULL");
   if (h->bad) return ERR(LGA_ERR_BAD_STATE, "handle latched");
   const Cfg& c = h->c;
@@ -1611,19 +1793,32 @@ static lga_status gather_state(lga_handle* h, const float* src_shards, float* ou
   if (!out) return ERR(LGA_ERR_INVALID_ARG, "out is NULL");
   ABI_TRY
   CK(cudaSetDevice(h->dev));
-  CK(cudaEventSynchronize(h->ev_t1));   // the last step (a replayed graph runs on the caller's stream)
+  if (h->stepped) CK(cudaEventSynchronize(h->ev_t1));   // the last step (a replayed graph runs on the caller's stream)
   CK(cudaStreamSynchronize(h->s_comp));
   CK(cudaStreamSynchronize(h->s_comm));
+  const bool sharded = c.D > 1 && !c.unpart;
+  if (sharded && !world_sync(h, 600.0)) {
+    ERR(LGA_ERR_CUDA, "world barrier timed out (a peer did not call lga_grads / lga_params)");
+    throw StatusError{LGA_ERR_CUDA};
+  }
   float* full = nullptr;
   CK(cudaMalloc(&full, (size_t)c.Lloc * c.plpad * sizeof(float)));
   for (int j = 0; j < c.Lloc; ++j) {
-    const float* shard = src_shards + (int64_t)j * c.S;
     float* dst = full + (int64_t)j * c.plpad;
-    if (c.D > 1 && !c.unpart) {
-      NK(ncclAllGather(shard, dst, (size_t)c.S, ncclFloat32, h->dp_comm, h->s_comp));
+    if (sharded) {
+      for (int r = 0; r < c.D; ++r) {
+        const char* src = h->dp_base[r] + peer_off + (size_t)j * c.S * sizeof(float);
+        CK(cudaMemcpyAsync(dst + (int64_t)r * c.S, src, (size_t)c.S * sizeof(float), cudaMemcpyDeviceToDevice, h->s_comp));
+      }
     } else {
-      CK(cudaMemcpyAsync(dst, shard, (size_t)c.S * sizeof(float), cudaMemcpyDeviceToDevice, h->s_comp));
+      CK(cudaMemcpyAsync(dst, src_shards + (int64_t)j * c.S, (size_t)c.S * sizeof(float), cudaMemcpyDeviceToDevice,
+                         h->s_comp));
     }
+  }
+  CK(cudaStreamSynchronize(h->s_comp));
+  if (sharded && !world_sync(h, 600.0)) {
+    ERR(LGA_ERR_CUDA, "world barrier timed out");
+    throw StatusError{LGA_ERR_CUDA};
   }
   for (int j = 0; j < c.Lloc; ++j) {
     CK(cudaMemcpyAsync(out + (int64_t)j * c.pl, full + (int64_t)j * c.plpad, (size_t)c.pl * sizeof(float),
@@ -1637,11 +1832,13 @@ static lga_status gather_state(lga_handle* h, const float* src_shards, float* ou
 
 lga_status lga_grads(lga_handle* h, float* out, uint64_t n, int32_t out_on_device) {
   if (h && !h->c.retain) return ERR(LGA_ERR_INVALID_ARG, "retain_grads was 0 at lga_init");
-  return gather_state(h, h ? h->gkeep : nullptr, out, n, out_on_device);
+  return gather_state(h, h ? h->gkeep : nullptr, h && h->connected ? h->peers[h->rank].off_gkeep : 0, out, n,
+                      out_on_device);
 }
 
 lga_status lga_params(lga_handle* h, float* out, uint64_t n, int32_t out_on_device) {
-  return gather_state(h, h ? h->master : nullptr, out, n, out_on_device);
+  return gather_state(h, h ? h->master : nullptr, h && h->connected ? h->peers[h->rank].off_master : 0, out, n,
+                      out_on_device);
 }
 
 lga_status lga_comm_bytes(const lga_handle* h, lga_comm_stats* last_step, lga_comm_stats* total) {

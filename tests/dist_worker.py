@@ -29,6 +29,7 @@ def main():
     import torch.distributed as dist
     from paper_2106_02679_b200 import Config, Trainer
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    local = local % torch.cuda.device_count()   # fewer GPUs than ranks: ranks share devices (peer memory over IPC)
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     sh = synth.Shape(**json.loads(a.shape))

@@ -57,14 +57,26 @@ def test_invalid_configs_rejected_without_side_effects():
         h = C.c_void_p()
         world = cfg.dp * cfg.pp
         nid = C.create_string_buffer(128) if world > 1 else None
-        st = L.lga_init(C.byref(cfg.to_c()), 0, world, 0, nid, None, None, 0, C.byref(h))
+        st = L.lga_init(C.byref(cfg.to_c()), 0, world, 0, _abi.ALLGATHER_FN(), None, nid, None, None, 0, C.byref(h))
         assert st == status, (kw, st, L.lga_last_error())
         assert not h.value
     # world mismatch
-    cfg = Config(layers=2, d_model=64, heads=4, seq_len=32, micro_batch=2, n_micro=4, dp=2)
+    cfg = Config(layers=2, d_model=64, heads=4, seq_len=32, micro_batch=2, n_micro=4, dp=2, precision=0)
     h = C.c_void_p()
-    assert L.lga_init(C.byref(cfg.to_c()), 0, 3, 0, C.create_string_buffer(128), None, None, 0, C.byref(h)) == 1
+    assert L.lga_init(C.byref(cfg.to_c()), 0, 3, 0, _abi.ALLGATHER_FN(), None, C.create_string_buffer(128), None, None,
+                      0, C.byref(h)) == 1
     assert b"world" in L.lga_last_error()
+    # world > 1 without any bootstrap (no allgather callback, no NCCL id)
+    assert L.lga_init(C.byref(cfg.to_c()), 0, 2, 0, _abi.ALLGATHER_FN(), None, None, None, None, 0, C.byref(h)) == 1
+    assert b"bootstrap" in L.lga_last_error()
+    assert not h.value
+    # the NCCL baseline needs an NCCL id
+    cfg = Config(layers=2, d_model=64, heads=4, seq_len=32, micro_batch=2, n_micro=4, dp=2, precision=0,
+                 flags=_abi.LGA_FLAG_NCCL_DP)
+    cb = _abi.ALLGATHER_FN(lambda ctx, a, b, n: 0)
+    assert L.lga_init(C.byref(cfg.to_c()), 0, 2, 0, cb, None, None, None, None, 0, C.byref(h)) == 1
+    assert b"nccl_id" in L.lga_last_error()
+    assert not h.value
 
 
 def test_status_strings():
