@@ -29,6 +29,38 @@ int lgatest_attn_fwd(int path, int nseq, int seq, int heads, int dh, int causal,
 int lgatest_attn_bwd(int path, int nseq, int seq, int heads, int dh, int causal, const void* qkv, const void* o,
                      const float* lse, const void* dO, float* dsum, void* dqkv, uintptr_t stream);
 
+/* LayerNorm forward (reading A-1): y = (x - mu) rstd gamma + beta over rows of d; x fp32, gamma / beta in
+ * p_dt, y in y_dt, stats[r] = (mu, rstd) as float2. */
+int lgatest_ln_fwd(const float* x, const void* gamma, const void* beta, int p_dt, void* y, int y_dt, float* stats,
+                   int rows, int d, float eps, uintptr_t stream);
+/* LayerNorm backward (O5) as the step runs it: the row kernel(s) write dx (+ resid) (fp32) and optionally dx_e
+ * (e_dt), plus deterministic column partials; the fixed-order finisher then writes dgamma = sum dout * xhat and
+ * dbeta = sum dout (fp32, d each).  `partial` is scratch of lgatest_ln_bwd_partial_floats(rows, d) floats. */
+int lgatest_ln_bwd(const float* dout, const float* x, const float* stats, const void* gamma, int p_dt,
+                   const float* resid, float* dx, void* dx_e, int e_dt, float* dgamma, float* dbeta, float* partial,
+                   int rows, int d, uintptr_t stream);
+int64_t lgatest_ln_bwd_partial_floats(int rows, int d);
+/* Bias gradient as the step computes it: out[n] = (acc_in ? acc_in[n] : 0) + sum_r X[r][n] (fixed row
+ * blocks, fixed order); X in x_dt with leading dimension ldx; out in out_dt.  `partial` is scratch of
+ * lgatest_colsum_partial_floats(rows, n) floats. */
+int lgatest_colsum(const void* X, int x_dt, int64_t ldx, int rows, int n, const float* acc_in, void* out, int out_dt,
+                   float* partial, uintptr_t stream);
+int64_t lgatest_colsum_partial_floats(int rows, int n);
+/* Sharded AdamW (torch semantics, reading A-4) on n elements: g = gin * gscale; master / m / v fp32 updated in
+ * place; param_out (p_dt) = theta; keep (fp32, optional) = g.  tstep: DEVICE long long, the step t (from 1). */
+int lgatest_adamw(const void* gin, int g_dt, float gscale, float* master, float* m, float* v, void* param_out,
+                  int p_dt, float* keep, int64_t n, float lr, float beta1, float beta2, float eps, float wd,
+                  const long long* tstep, uintptr_t stream);
+/* The reduce-scatter fused into AdamW: g = gscale * sum_{p<D} gbase[p][goff + i] in fixed order p = 0..D-1
+ * (gbase: DEVICE array of D pointers, g_dt elements), then AdamW as above.  n % 4 == 0. */
+int lgatest_adamw_rs(const void* const* gbase, int64_t goff, int D, int g_dt, float gscale, float* master, float* m,
+                     float* v, void* param_out, int p_dt, float* keep, int64_t n, float lr, float beta1, float beta2,
+                     float eps, float wd, const long long* tstep, uintptr_t stream);
+/* Peer-slice reduction: s = sum_{p<D} gbase[p][goff + i] (fixed order); acc != NULL: acc = (first ? 0 : acc) + s
+ * (fp32); else out (g_dt) = s.  n % 4 == 0. */
+int lgatest_peer_reduce(const void* const* gbase, int64_t goff, int D, int g_dt, float* acc, int first, void* out,
+                        int64_t n, uintptr_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,13 @@ its gradient; the paper's claim is that they are the same computation reordered:
 * ``grads_fullbatch`` -- no accumulation: one pass over all D*N*b sequences.
 
 AdamW follows torch.optim.AdamW (reading A-4): "The Adam optimizer is assumed".
+
+Mixed precision ("the bulk of the computation is done in half-precision, while the weights
+are stored and updated in single-precision"; bfloat16 named there): ``train_steps(...,
+param_round="bf16")`` evaluates each step's gradient at the 16-bit copy of the weights,
+round-to-nearest-even of the stored weights (reading A-9), and applies it to the stored weights.
+This is the gradient the mixed-precision method defines; the default (None) is the plain
+definition at the stored weights.
 """
 
 from __future__ import annotations
@@ -30,6 +37,14 @@ from dataclasses import dataclass
 import numpy as np
 
 from .model import LayerCfg, layer_backward, layer_forward, mse_loss
+
+
+def round_bf16(a) -> np.ndarray:
+    """Round-to-nearest-even of float32(a) to bfloat16, returned as float64 (reading A-9): keep the top 16
+    bits of the fp32 pattern after adding 0x7FFF plus the lowest kept bit (ties to even)."""
+    u = np.ascontiguousarray(np.asarray(a, dtype=np.float32)).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
 def _as64(a):
@@ -152,16 +167,18 @@ class AdamW:
 SCHEDULES = {"standard": grads_standard, "layered": grads_layered, "fullbatch": grads_fullbatch}
 
 
-def train_steps(params, batches, cfg: LayerCfg, opt: AdamW, schedule="standard"):
+def train_steps(params, batches, cfg: LayerCfg, opt: AdamW, schedule="standard", param_round=None):
     """Run len(batches) optimizer steps.  batches: list of (X, T).  Returns
     (params, losses, last_grads).  Parameters are fp64 copies; the caller passes the fp32
-    initial values the GPU side received (O1)."""
+    initial values the GPU side received (O1).  param_round="bf16": each gradient is taken at
+    round_bf16 of the stored weights (mixed precision; module docstring)."""
     params = [_as64(p).copy() for p in params]
     states = [opt.init_state(p) for p in params]
     losses, grads = [], None
     fn = SCHEDULES[schedule]
     for X, T in batches:
-        loss, grads = fn(params, X, T, cfg)
+        at = params if param_round is None else [round_bf16(p) for p in params]
+        loss, grads = fn(at, X, T, cfg)
         losses.append(loss)
         params = [opt.update(p, g, s) for p, g, s in zip(params, grads, states)]
     return params, losses, grads

@@ -67,3 +67,56 @@ extern "C" int lgatest_attn_bwd(int path, int nseq, int seq, int heads, int dh, 
   }
   return (int)cudaGetLastError();
 }
+
+extern "C" int lgatest_ln_fwd(const float* x, const void* gamma, const void* beta, int p_dt, void* y, int y_dt,
+                              float* stats, int rows, int d, float eps, uintptr_t stream) {
+  ln_fwd(x, gamma, beta, (DT)p_dt, y, (DT)y_dt, reinterpret_cast<float2*>(stats), rows, d, eps,
+         reinterpret_cast<cudaStream_t>(stream));
+  return (int)cudaGetLastError();
+}
+
+extern "C" int64_t lgatest_ln_bwd_partial_floats(int rows, int d) { return (int64_t)ln_bwd_blocks(rows, d) * 2 * d; }
+
+extern "C" int lgatest_ln_bwd(const float* dout, const float* x, const float* stats, const void* gamma, int p_dt,
+                              const float* resid, float* dx, void* dx_e, int e_dt, float* dgamma, float* dbeta,
+                              float* partial, int rows, int d, uintptr_t stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int nblk = ln_bwd(dout, x, reinterpret_cast<const float2*>(stats), gamma, (DT)p_dt, resid, dx, dx_e, (DT)e_dt,
+                          partial, rows, d, st);
+  colsum_finish(partial, nblk, 2LL * d, d, nullptr, dgamma, DT::F32, st);
+  colsum_finish(partial + d, nblk, 2LL * d, d, nullptr, dbeta, DT::F32, st);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int64_t lgatest_colsum_partial_floats(int rows, int n) { return (int64_t)colsum_blocks(rows) * n; }
+
+extern "C" int lgatest_colsum(const void* X, int x_dt, int64_t ldx, int rows, int n, const float* acc_in, void* out,
+                              int out_dt, float* partial, uintptr_t stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int nblk = colsum_partial(X, (DT)x_dt, ldx, rows, n, partial, st);
+  colsum_finish(partial, nblk, n, n, acc_in, out, (DT)out_dt, st);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int lgatest_adamw(const void* gin, int g_dt, float gscale, float* master, float* m, float* v,
+                             void* param_out, int p_dt, float* keep, int64_t n, float lr, float beta1, float beta2,
+                             float eps, float wd, const long long* tstep, uintptr_t stream) {
+  adamw(gin, (DT)g_dt, gscale, master, m, v, param_out, (DT)p_dt, keep, n, lr, beta1, beta2, eps, wd, tstep,
+        reinterpret_cast<cudaStream_t>(stream));
+  return (int)cudaGetLastError();
+}
+
+extern "C" int lgatest_adamw_rs(const void* const* gbase, int64_t goff, int D, int g_dt, float gscale, float* master,
+                                float* m, float* v, void* param_out, int p_dt, float* keep, int64_t n, float lr,
+                                float beta1, float beta2, float eps, float wd, const long long* tstep,
+                                uintptr_t stream) {
+  adamw_rs(gbase, goff, D, (DT)g_dt, gscale, master, m, v, param_out, (DT)p_dt, keep, n, lr, beta1, beta2, eps, wd,
+           tstep, reinterpret_cast<cudaStream_t>(stream));
+  return (int)cudaGetLastError();
+}
+
+extern "C" int lgatest_peer_reduce(const void* const* gbase, int64_t goff, int D, int g_dt, float* acc, int first,
+                                   void* out, int64_t n, uintptr_t stream) {
+  peer_reduce(gbase, goff, D, (DT)g_dt, acc, first != 0, out, n, reinterpret_cast<cudaStream_t>(stream));
+  return (int)cudaGetLastError();
+}

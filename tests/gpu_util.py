@@ -17,14 +17,78 @@ def rel(a, b):
 
 
 def oracle_run(sh: synth.Shape, init: np.ndarray, batches, causal=True, lr=1e-3, wd=0.0, schedule="standard",
-               post_ln=False):
+               post_ln=False, param_round=None):
+    """The fp64 oracle's train_steps on the same seeded inputs.  param_round="bf16": gradients at the 16-bit
+    weight copy (mixed precision) -- the reference of the bf16 per-tensor checks, which thereby measure
+    the kernels' arithmetic apart from the method's weight quantisation."""
     cfg = om.LayerCfg(d=sh.d, heads=sh.heads, causal=bool(causal), post_ln=bool(post_ln))
     params = [p.astype(np.float64) for p in synth.split_layers(init, sh.layers)]
     opt = osch.AdamW(lr=lr, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=wd)
-    new, losses, grads = osch.train_steps(params, batches, cfg, opt, schedule)
+    new, losses, grads = osch.train_steps(params, batches, cfg, opt, schedule, param_round=param_round)
     return np.concatenate(new), losses, np.concatenate(grads)
 
 
 def per_layer_rel(a, b, layers):
     pl = a.size // layers
     return [rel(a[l * pl:(l + 1) * pl], b[l * pl:(l + 1) * pl]) for l in range(layers)]
+
+
+# Per-tensor comparison (reading A-15 refined): every tensor of every layer is held to the bar by its own
+# relative Frobenius error, so that a small tensor (LayerNorm gamma / beta, a bias) cannot hide inside the
+# per-layer norm.  The key bias is the exception: dL/db_K == 0 in exact arithmetic (pin P4, softmax shift
+# invariance), so its relative error is undefined; it is held ABSOLUTELY, against the query bias gradient.
+TENSORS = ["ln1_w", "ln1_b", "Wq", "Wk", "Wv", "bq", "bv", "Wo", "bo", "ln2_w", "ln2_b", "W1", "b1", "W2", "b2"]
+
+
+def _split(flat, d):
+    from oracle import model as om
+    u = om.unpack(np.asarray(flat, dtype=np.float64), d)
+    out = {k: u[k] for k in ("ln1_w", "ln1_b", "Wo", "bo", "ln2_w", "ln2_b", "W1", "b1", "W2", "b2")}
+    out["Wq"], out["Wk"], out["Wv"] = u["Wqkv"][:, :d], u["Wqkv"][:, d:2 * d], u["Wqkv"][:, 2 * d:]
+    out["bq"], out["bk"], out["bv"] = u["bqkv"][:d], u["bqkv"][d:2 * d], u["bqkv"][2 * d:]
+    return out
+
+
+def per_tensor_rel(a, b, d, layers, grads=True, init=None):
+    """[{tensor: rel err}] per layer.
+    Gradients: the key bias as 'bk_abs' = ||a_bK|| / ||b_bQ|| (b_bK is zero up to rounding, pin P4).
+    Parameters after AdamW steps: the key bias is left out -- its gradient is rounding noise on the GPU and
+    ~1e-22 in the oracle, and AdamW normalises each element (at t = 1 the update is lr g / (|g| + eps)), so
+    the GPU moves b_K by up to lr per element while the oracle leaves it in place; that is the optimizer's
+    normalisation of a zero gradient, not an arithmetic error.  For the same reason a tensor whose initial
+    value is identically 0 (biases and LayerNorm beta of the "train" init; pass `init`) is left out: its value
+    after one step IS the normalised update of every element, including the near-zero gradients."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    pl = a.size // layers
+    res = []
+    for l in range(layers):
+        ta, tb = _split(a[l * pl:(l + 1) * pl], d), _split(b[l * pl:(l + 1) * pl], d)
+        t0 = _split(np.asarray(init[l * pl:(l + 1) * pl], dtype=np.float64), d) if init is not None else None
+        r = {k: rel(ta[k], tb[k]) for k in TENSORS if t0 is None or np.any(t0[k] != 0)}
+        if grads:
+            r["bk_abs"] = float(np.linalg.norm(ta["bk"]) / max(np.linalg.norm(tb["bq"]), 1e-300))
+        res.append(r)
+    return res
+
+
+def assert_per_tensor(a, b, d, layers, tol, grads=True, init=None):
+    """Every tensor within `tol` relative Frobenius (gradients: the key bias within `tol` of ||dL/db_Q||;
+    parameters: see per_tensor_rel for the tensors left out)."""
+    worst = per_tensor_rel(a, b, d, layers, grads=grads, init=init)
+    for l, r in enumerate(worst):
+        bad = {k: v for k, v in r.items() if v >= tol}
+        assert not bad, (l, bad)
+    return worst
+
+
+# Per-tensor tolerances: bf16 mode = the north-star bar itself; fp32 mode = 10x the per-layer bar.  fp32 per
+# tensor is an added guard (the per-layer / global 1e-5 stays): a tensor that is a column sum of cancelling
+# terms (e.g. the LayerNorm beta gradient of the post-LN layer, the sum of y - T over rows) carries a relative
+# rounding error set by its condition number, measured up to 1.2e-5, while a wrong kernel gives O(1).
+TENSOR_TOL = {"fp32": 1e-4, "bf16": 2e-2}
+
+
+def max_per_tensor(rows):
+    keys = rows[0].keys()
+    return {k: max(r[k] for r in rows) for k in keys}

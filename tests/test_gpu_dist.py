@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 import synth
-from gpu_util import oracle_run, per_layer_rel, rel
+from gpu_util import TENSOR_TOL, assert_per_tensor, oracle_run, per_layer_rel, rel
 from oracle import counters as oc
 
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
@@ -55,6 +55,9 @@ def _check(outs, sh, tol, steps=1, schedule="layered", elem=4, flags=0):
     batches = [synth.batch(sh, step=k) for k in range(steps)]
     init = synth.init_params(sh, style="parity")
     rp, rl, rg = oracle_run(sh, init, batches, lr=1e-3, post_ln=bool(flags & POST_LN))
+    mp, mg = rp, rg   # bf16: the per-tensor checks use gradients at the 16-bit weight copy
+    if elem == 2:
+        mp, _, mg = oracle_run(sh, init, batches, lr=1e-3, post_ln=bool(flags & POST_LN), param_round="bf16")
     pl = sh.d * sh.d * 12 + 13 * sh.d
     for o in outs:
         stage = int(o["stage"])
@@ -64,6 +67,9 @@ def _check(outs, sh, tol, steps=1, schedule="layered", elem=4, flags=0):
         g, p = o["grads"], o["params"]
         assert rel(g, rg[sel]) < tol, (stage, per_layer_rel(g, rg[sel], len(layers)))
         assert rel(p, rp[sel]) < tol
+        assert_per_tensor(g, mg[sel], sh.d, len(layers), TENSOR_TOL["fp32" if tol <= 1e-5 else "bf16"])
+        assert_per_tensor(p, mp[sel], sh.d, len(layers), TENSOR_TOL["fp32" if tol <= 1e-5 else "bf16"], grads=False,
+                          init=init[sel])
         np.testing.assert_allclose(o["losses"], rl, rtol=max(tol, 1e-6))
         assert list(o["stages"]) == [oc.stage_of_layer(i, sh.pp, sh.layers, var["pipeline"]) for i in range(sh.layers)]
         last = json.loads(str(o["last"]))

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import synth
-from gpu_util import oracle_run, per_layer_rel, rel
+from gpu_util import TENSOR_TOL, assert_per_tensor, oracle_run, per_layer_rel, rel
 from oracle import counters as oc
 
 pytestmark = pytest.mark.gpu
@@ -30,6 +30,9 @@ def _run(sh, precision=LGA_FP32, schedule=LGA_LAYERED, chunk=0, causal=0, steps=
     out = dict(params=tr.params(), grads=tr.grads(), losses=losses, stats=tr.comm_stats()[0])
     tr.close()
     ref = oracle_run(sh, init, batches, causal=causal, post_ln=True)
+    if precision == LGA_BF16:   # reference of the per-tensor checks: gradients at the bf16 weight copy
+        out["mp_params"], _, out["mp_grads"] = oracle_run(sh, init, batches, causal=causal, post_ln=True,
+                                                          param_round="bf16")
     return out, ref, init
 
 
@@ -37,7 +40,13 @@ def _check(sh, out, ref, init, tol, elem, no_recompute=False):
     rp, rl, rg = ref
     assert max(per_layer_rel(out["grads"], rg, sh.layers)) < tol, per_layer_rel(out["grads"], rg, sh.layers)
     assert rel(out["params"], rp) < tol
-    assert rel(out["params"] - init, rp - init) < 10 * tol
+    mg, mp = out.get("mp_grads", rg), out.get("mp_params", rp)   # bf16: against the 16-bit-weight oracle
+    assert_per_tensor(out["grads"], mg, sh.d, sh.layers, TENSOR_TOL["fp32" if tol <= 1e-5 else "bf16"])
+    assert_per_tensor(out["params"], mp, sh.d, sh.layers, TENSOR_TOL["fp32" if tol <= 1e-5 else "bf16"], grads=False,
+                      init=init)
+    # the update itself (AdamW at t = 1 is lr sign(g) where |g| >> eps: elements with a rounding-level gradient
+    # flip sign, so the update's relative error is set by how many gradients sit near 0, not by the arithmetic)
+    assert rel(out["params"] - init, rp - init) < (1e-4 if tol <= 1e-5 else 1e-1)
     np.testing.assert_allclose(out["losses"], rl, rtol=max(tol, 1e-6))
     c = oc.comm_counters(oc.StepShape(layers=sh.layers, d=sh.d, seq=sh.seq, micro_batch=sh.micro_batch,
                                       n_micro=sh.n_micro), param_bytes=elem, grad_bytes=elem, no_recompute=no_recompute)

@@ -1,12 +1,14 @@
 """Parity of the CUDA step (through the C ABI) with the fp64 oracle, single GPU.
 
-fp32 mode: gradients and updated parameters within 1e-5 relative Frobenius (BASELINE.json
-north star), per layer and globally; counters exact."""
+Gradients and updated parameters within relative Frobenius 1e-5 (fp32 mode) / 2e-2 (bf16 mode)
+(BASELINE.json north star) globally, per layer, and PER TENSOR of every layer (the key bias, whose
+exact gradient is 0 by pin P4, is held absolutely against the query bias gradient); counters exact
+(SURVEY.md 8(c) O8)."""
 import numpy as np
 import pytest
 
 import synth
-from gpu_util import oracle_run, per_layer_rel, rel
+from gpu_util import TENSOR_TOL, assert_per_tensor, oracle_run, per_layer_rel, rel
 from oracle import counters as oc
 
 pytestmark = pytest.mark.gpu
@@ -35,6 +37,9 @@ def _run(sh, precision=LGA_FP32, schedule=LGA_LAYERED, chunk=0, causal=1, steps=
                timing=tr.timing())
     tr.close()
     ref_params, ref_losses, ref_grads = oracle_run(sh, init, batches, causal=causal, lr=lr, wd=wd)
+    if precision == LGA_BF16:   # reference of the per-tensor checks: gradients at the bf16 weight copy
+        out["mp_params"], _, out["mp_grads"] = oracle_run(sh, init, batches, causal=causal, lr=lr, wd=wd,
+                                                          param_round="bf16")
     return out, (ref_params, ref_losses, ref_grads, init)
 
 
@@ -45,6 +50,8 @@ C1 = synth.Shape(layers=2, d=64, heads=4, seq=32, micro_batch=2, n_micro=4)
 def test_fp32_c1_layered_parity(chunk):
     out, (rp, rl, rg, init) = _run(C1, chunk=chunk)
     assert rel(out["grads"], rg) < 1e-5, per_layer_rel(out["grads"], rg, C1.layers)
+    assert_per_tensor(out["grads"], rg, C1.d, C1.layers, TENSOR_TOL["fp32"])
+    assert_per_tensor(out["params"], rp, C1.d, C1.layers, TENSOR_TOL["fp32"], grads=False, init=init)
     assert max(per_layer_rel(out["grads"], rg, C1.layers)) < 1e-5
     assert rel(out["params"], rp) < 1e-5
     # the update itself, not just the parameters
@@ -88,6 +95,8 @@ def test_bf16_layered_parity(sh, chunk):
     per = per_layer_rel(out["grads"], rg, sh.layers)
     assert rel(out["grads"], rg) < 2e-2 and max(per) < 2e-2, per
     assert rel(out["params"], rp) < 2e-2
+    assert_per_tensor(out["grads"], out["mp_grads"], sh.d, sh.layers, TENSOR_TOL["bf16"])
+    assert_per_tensor(out["params"], out["mp_params"], sh.d, sh.layers, TENSOR_TOL["bf16"], grads=False, init=init)
     assert abs(out["losses"][0] - rl[0]) < 1e-2 * abs(rl[0])
 
 
@@ -95,17 +104,34 @@ def test_bf16_layered_parity(sh, chunk):
 # The bench configs' per-layer shapes exactly (d, heads, s, b; chunk = N so one launch covers all
 # micro-batches, as bench.py times it) with L and N small enough for the fp64 oracle (seconds).
 FULL = [synth.Shape(layers=2, d=2048, heads=16, seq=2048, micro_batch=1, n_micro=2),     # 1.3B layer (C3)
-        synth.Shape(layers=1, d=768, heads=12, seq=1024, micro_batch=4, n_micro=2)]       # GPT-2-small layer (C2)
+        synth.Shape(layers=1, d=768, heads=12, seq=1024, micro_batch=4, n_micro=2),       # GPT-2-small layer (C2)
+        synth.Shape(layers=1, d=4096, heads=32, seq=2048, micro_batch=1, n_micro=2)]      # ~10B layer (C4)
 
 
-@pytest.mark.parametrize("sh", FULL, ids=["c3_layer", "c2_layer"])
+@pytest.mark.parametrize("sh", FULL, ids=["c3_layer", "c2_layer", "c4_layer"])
 def test_bf16_full_width_parity(sh):
     out, (rp, rl, rg, init) = _run(sh, precision=LGA_BF16, style="train")
     per = per_layer_rel(out["grads"], rg, sh.layers)
     assert max(per) < 2e-2 and rel(out["grads"], rg) < 2e-2, per
-    assert rel(out["params"] - init, rp - init) < 5e-2      # the update itself (sign flips of tiny g count)
+    # the update itself: AdamW at t = 1 is lr sign(g) where |g| >> eps, so elements whose gradient is at the
+    # rounding level flip sign and the update is ill-conditioned; the parameters are the quantity the bar binds
+    assert rel(out["params"] - init, rp - init) < 1e-1
     assert rel(out["params"], rp) < 2e-2
     assert abs(out["losses"][0] - rl[0]) < 1e-3 * abs(rl[0])
+    assert_per_tensor(out["grads"], out["mp_grads"], sh.d, sh.layers, TENSOR_TOL["bf16"])
+    assert_per_tensor(out["params"], out["mp_params"], sh.d, sh.layers, TENSOR_TOL["bf16"], grads=False, init=init)
+
+
+@pytest.mark.parametrize("d,heads,seq", [(1024, 8, 96), (2048, 16, 80), (4096, 32, 64)], ids=["d1024", "d2048", "d4096"])
+def test_fp32_wide_parity_per_tensor(d, heads, seq):
+    """fp32 mode at the configs' widths: the fused LayerNorm backward (d = 1024, 2048: 4 / 8 columns per lane),
+    the warp-per-row LayerNorm kernels up to 32 column groups (d = 4096) and the wide bias column sums are
+    held to 1e-5 per tensor -- the bf16 tolerance alone cannot see a wrong LayerNorm gamma / beta gradient."""
+    sh = synth.Shape(layers=1, d=d, heads=heads, seq=seq, micro_batch=1, n_micro=2)
+    out, (rp, rl, rg, init) = _run(sh)
+    assert_per_tensor(out["grads"], rg, sh.d, sh.layers, TENSOR_TOL["fp32"])
+    assert_per_tensor(out["params"], rp, sh.d, sh.layers, TENSOR_TOL["fp32"], grads=False, init=init)
+    assert abs(out["losses"][0] - rl[0]) < 1e-6 * abs(rl[0])
 
 
 def test_bf16_single_position_degenerate():
@@ -156,6 +182,7 @@ def test_bf16_no_recompute_parity_and_flags_without_dp():
     sh = synth.Shape(layers=2, d=256, heads=2, seq=128, micro_batch=1, n_micro=4)
     out, (rp, rl, rg, _) = _run(sh, precision=LGA_BF16, flags=NO_RECOMPUTE | KEEP_PARAMS)
     assert rel(out["grads"], rg) < 2e-2 and rel(out["params"], rp) < 2e-2
+    assert_per_tensor(out["grads"], out["mp_grads"], sh.d, sh.layers, TENSOR_TOL["bf16"])
     assert out["stats"]["ag_calls"] == 0 and out["stats"]["recompute_units"] == 0
 
 
@@ -200,6 +227,7 @@ def test_bf16_d1024_parity():
     sh = synth.Shape(layers=2, d=1024, heads=8, seq=130, micro_batch=1, n_micro=2)
     out, (rp, rl, rg, _) = _run(sh, precision=LGA_BF16)
     assert rel(out["grads"], rg) < 2e-2 and rel(out["params"], rp) < 2e-2
+    assert_per_tensor(out["grads"], out["mp_grads"], sh.d, sh.layers, TENSOR_TOL["bf16"])
 
 
 @pytest.mark.parametrize("precision", [LGA_FP32, LGA_BF16])

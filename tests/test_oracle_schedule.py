@@ -96,3 +96,42 @@ def test_train_steps_schedules_agree():
     for a, b_ in zip(ps, pl):
         np.testing.assert_allclose(b_, a, rtol=1e-10, atol=1e-14)
     assert ls[2] < ls[0]   # the optimiser descends on a fixed-target regression
+
+
+def test_round_bf16_is_round_to_nearest_even():
+    """Mixed precision (reading A-9): the 16-bit weight copy is round-to-nearest-even of fp32.  Closed
+    forms at the halfway points of [1, 2) (bf16 ulp 2^-7) and a library routine (torch's bfloat16 cast) on
+    values across the exponent range."""
+    h = 2.0 ** -8   # half an ulp in [1, 2)
+    cases = {1.0: 1.0, 1.0 + h: 1.0, 1.0 + 3 * h: 1.0 + 4 * h, 1.0 + 0.9 * h: 1.0, 1.0 + 1.1 * h: 1.0 + 2 * h,
+             -(1.0 + h): -1.0, 2.0 ** -130: 2.0 ** -130, 0.0: 0.0}
+    for x, want in cases.items():
+        assert osch.round_bf16(np.array([x]))[0] == want, x
+    rng = np.random.default_rng(0)
+    v = (rng.standard_normal(100_000) * np.exp2(rng.integers(-60, 60, 100_000))).astype(np.float32)
+    b = osch.round_bf16(v[:1000])                       # bf16 values; exactly halfway to the next one up:
+    ties = (b + np.sign(b) * np.exp2(np.frexp(b)[1] - 9.0)).astype(np.float32)   # ulp = 2^(e-8), frexp e = exp+1
+    for a in (v, ties):
+        ref = torch.from_numpy(a).bfloat16().double().numpy()
+        np.testing.assert_array_equal(osch.round_bf16(a), ref)
+
+
+def test_train_steps_mixed_precision_is_gradient_at_rounded_weights():
+    """param_round="bf16" evaluates the gradient at the rounded weights and updates the stored ones: with weights
+    already representable in bf16 it changes nothing; otherwise its first gradient is the plain gradient at
+    round_bf16(theta) while the update is applied to theta itself."""
+    cfg, params, X, T = _setup(L=2, d=8, heads=2, s=4, b=1, N=2, D=1)
+    opt = osch.AdamW(lr=1e-2)
+    rp = [osch.round_bf16(p) for p in params]
+    a = osch.train_steps(rp, [(X, T)], cfg, opt, param_round="bf16")
+    b = osch.train_steps(rp, [(X, T)], cfg, opt)
+    for x, y in zip(a[0], b[0]):
+        np.testing.assert_array_equal(x, y)
+    new, losses, grads = osch.train_steps(params, [(X, T)], cfg, opt, param_round="bf16")
+    l_ref, g_ref = osch.grads_standard(rp, X, T, cfg)
+    assert losses[0] == l_ref
+    for g, gr, p, n in zip(grads, g_ref, params, new):
+        np.testing.assert_array_equal(g, gr)
+        # first AdamW step moves theta (not its rounded copy) by lr g / (|g| + eps)
+        np.testing.assert_allclose(n, p - 1e-2 * gr / (np.abs(gr) + 1e-8), rtol=1e-12, atol=1e-15)
+    assert any(np.any(p != q) for p, q in zip(params, rp))   # the parity init is not bf16-representable
