@@ -116,6 +116,37 @@ class ClockSampler:
                 "samples": len(rows), "samples_under_load": len(load), "reasons": sorted(reasons)}
 
 
+class NvlinkCounters:
+    """NVLink payload byte counters of this rank's GPU (NVML field values, all links summed), read around the
+    timed region: the transfers the peer-memory data path really put on NVLink, per step."""
+    TX, RX = 138, 139   # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX (KiB, cumulative)
+
+    def __init__(self, device=0):
+        self.ok = False
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[device]) if vis else device
+            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(idx)
+            self.ok = self.read() is not None
+        except Exception:
+            self.ok = False
+
+    def read(self):
+        try:
+            nv = self.nv
+            vals = nv.nvmlDeviceGetFieldValues(self.h, [(self.TX, 0xFFFFFFFF), (self.RX, 0xFFFFFFFF)])
+            out = []
+            for v in vals:
+                if v.nvmlReturn != 0:
+                    return None
+                out.append(int(v.value.ullVal) * 1024)
+            return out
+        except Exception:
+            return None
+
+
 # ----------------------------------------------------------------------------- oracle (CPU) arm
 POST_LN = [False]   # --post-ln: the oracle sample runs the same layer variant as the timed path
 
@@ -202,6 +233,7 @@ def main():
     ap.add_argument("--nccl-dp", action="store_true", help="N1 baseline: NCCL all-gather / reduce-scatter")
     ap.add_argument("--post-ln", action="store_true", help="N4: post-LN layer (original encoder, reading A-16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ab", action="store_true", help="skip the no-comm A/B run (second exposed-comm measure)")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -270,6 +302,8 @@ def main():
         clocks = ClockSampler(local) if rank == 0 else None
         if clocks:
             clocks.start()
+        nvl = NvlinkCounters(local) if world > 1 else None
+        nvl0 = nvl.read() if nvl and nvl.ok else None
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         step_ms = []   # per-step device time (library events on the caller stream), for median / p90
@@ -286,11 +320,18 @@ def main():
             step_ms.append(float(t["step_ms"]))
         e1.record(stream)
         torch.cuda.synchronize()
+        nvl1 = nvl.read() if nvl0 is not None else None
         barrier()
         torch.cuda.synchronize()
         clk = clocks.stop() if clocks else None
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     stats_last, _ = tr.comm_stats()
+    nvlink = None
+    if nvl1 is not None:
+        nvlink = {"tx_bytes_per_step": (nvl1[0] - nvl0[0]) / args.steps, "rx_bytes_per_step": (nvl1[1] - nvl0[1]) / args.steps,
+                  "counted_bytes_per_step": stats_last["ag_bytes"] + stats_last["rs_bytes"] + stats_last["p2p_send_bytes"]
+                  + stats_last["allreduce_bytes"],
+                  "source": "NVML NVLink data throughput counters (rank 0's GPU, all links), timed region"}
     tokens_per_step = dp * N * b * s
     value = tokens_per_step / (ms / 1000.0)
 
@@ -321,6 +362,34 @@ def main():
         e2e = {"value": tokens_per_step / (e2e_ms / 1000.0), "unit": "tokens/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "loss": loss.value}
 
+    # ---- second exposed-comm measure: the same step with every transfer skipped after the
+    # first (LGA_FLAG_NO_COMM), on the same GPUs right after; exposed = T(step) - T(step without comm)
+    ab = None
+    if world > 1 and not args.no_comm and not args.no_ab:
+        tr.close()
+        cfg_ab = Config(dp=dp, pp=pp, precision=precision, chunk=args.chunk,
+                        schedule=LGA_LAYERED if args.schedule == "layered" else LGA_STANDARD,
+                        flags=(flags | _abi.LGA_FLAG_NO_COMM) & ~_abi.LGA_FLAG_PROFILE, **shape)
+        tr_ab = Trainer(cfg_ab, rank=rank, world=world, device=local, init_params=None, seed=1234)
+        with torch.cuda.stream(tr_ab.stream):
+            for _ in range(args.warmup):
+                tr_ab.step(x, tgt, sync=False)
+            torch.cuda.synchronize()
+            barrier()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(tr_ab.stream)
+            for _ in range(args.steps):
+                tr_ab.step(x, tgt, sync=False)
+            a1.record(tr_ab.stream)
+            torch.cuda.synchronize()
+            barrier()
+        ab_ms = max_over_ranks(a0.elapsed_time(a1) / args.steps)
+        tr_ab.close()
+        tr = None
+        ab = {"no_comm_ms_per_step": ab_ms, "exposed_comm_ms_per_step": ms - ab_ms,
+              "frac_of_step": (ms - ab_ms) / ms}
+
     peaks, peak_src = measured_peaks()
     gemm_tflops = prof["gemm_flop"] / (prof["gemm_ms"] / 1000.0) / 1e12 if prof["gemm_ms"] > 0 else 0.0
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
@@ -344,7 +413,8 @@ def main():
               "adamw": {"achieved_gbs": prof["adam_bytes"] / (prof["adam_ms"] / 1e3) / 1e9 if prof["adam_ms"] else 0,
                         "peak_gbs": peaks.get("hbm_gbs"), "share_of_step": prof["adam_ms"] / (ms * args.steps)}}
     if rank != 0:
-        tr.close()
+        if tr is not None:
+            tr.close()
         if dist is not None:
             dist.destroy_process_group()
         return 0
@@ -366,6 +436,8 @@ def main():
         "step_ms_median": statistics.median(step_ms) if step_ms else None,
         "step_ms_p90": sorted(step_ms)[min(len(step_ms) - 1, int(0.9 * len(step_ms)))] if step_ms else None,
         "exposed_comm_ms_per_step": prof["comm_wait_ms"] / args.steps,
+        "exposed_comm_ab": ab,
+        "nvlink": nvlink,
         "p2p_wait_ms_per_step": prof["p2p_wait_ms"] / args.steps,
         "model_tflops_per_gpu": value * fpt / world / 1e12,
         "mfu_vs_measured_peak": value * fpt / world / 1e12 / peaks.get("bf16_tflops", 1620.5),
@@ -379,7 +451,8 @@ def main():
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
-    tr.close()
+    if tr is not None:
+        tr.close()
     if dist is not None:
         dist.destroy_process_group()
     return 0

@@ -75,8 +75,11 @@ typedef enum { LGA_FP32 = 0, LGA_BF16 = 1 } lga_precision;
 typedef enum { LGA_LAYERED = 0, LGA_STANDARD = 1 } lga_schedule;
 
 /* flags */
-#define LGA_FLAG_NO_COMM   0x1u  /* debug A/B timing only: skip every collective and p2p
-                                    transfer (results are then wrong); counters still count */
+#define LGA_FLAG_NO_COMM   0x1u  /* A/B timing only (exposed communication = T(step) - T(step without
+                                    comm)): the first step communicates as usual, so the parameter slots
+                                    hold real gathered weights; every later step skips every all-gather,
+                                    reduce-scatter, all-reduce and pipeline transfer (the same kernels run,
+                                    the results are then wrong); counters still count */
 #define LGA_FLAG_NO_GRAPH  0x2u  /* run every step eagerly.  By default lga_step captures the whole step
                                     (all streams, NCCL calls included) into a CUDA graph at its second
                                     call and replays it while x / target keep their pointers; the first
@@ -143,7 +146,9 @@ typedef struct {
 /* Device-measured timing of the last step (CUDA events on the library's streams). */
 typedef struct {
   float step_ms;          /* caller-stream start to step completion */
-  float comm_wait_ms;     /* sum of compute-stream stalls waiting on DP collectives */
+  float comm_wait_ms;     /* exposed data-parallel communication: the sum of compute-stream stalls on
+                             all-gathers, staging-buffer reuse, the peer loss all-reduce, and the
+                             step-end join of the last reduce-scatter + AdamW (the tail) */
   float p2p_wait_ms;      /* sum of compute-stream stalls waiting on pipeline receives */
   float fwd_ms, bwd_ms;   /* compute-stream time of the forward / backward passes */
   /* Per kernel family, only with LGA_FLAG_PROFILE (else 0): summed device time of the

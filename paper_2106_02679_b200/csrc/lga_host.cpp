@@ -223,6 +223,9 @@ struct lga_handle {
   bool connected = false;                        // every rank's arena mapped (world > 1)
   bool ready = false;                            // lga_init completed
   bool stepped = false;                          // ev_t1 recorded at least once
+  // LGA_FLAG_NO_COMM A/B: the first step communicates (the parameter slots then hold real gathered weights,
+  // so the A/B runs the same kernels on the same kind of data), every later step skips all transfers
+  bool comm_off = false;
   unsigned long long* wflags = nullptr;          // [0] loss arrivals, [1] barrier arrivals (written by peers)
   double* loss_ring = nullptr;                   // [4][world] loss slots (written by peers)
   unsigned long long** w_flag_dev = nullptr;     // device [world]: every rank's wflags
@@ -847,7 +850,7 @@ static void all_gather(lga_handle* h, int j, int slot) {
   if (h->slot.empty()) return;
   h->last.ag_calls++;
   h->last.ag_bytes += (uint64_t)(c.D - 1) * c.S * dt_size(c.E);
-  if (c.no_comm) return;
+  if (h->comm_off) return;
   if (c.dp_ipc) {
     // every replica's AdamW of layer j of the previous step is done (D (t-1) signals), then pull the D
     // shards over NVLink on the copy engines and tell each owner that its shard j has been read
@@ -887,7 +890,7 @@ static void* reduce_scatter(lga_handle* h, int j) {
     if (c.D > 1) {
       h->last.allreduce_calls++;
       h->last.allreduce_bytes += 2ull * (c.D - 1) * (uint64_t)(c.plpad / c.D) * dt_size(c.G);
-      if (!c.no_comm) NK(ncclAllReduce(gs, gs, (size_t)c.plpad, nccl_dt(c.G), ncclSum, h->dp_comm, h->s_comm));
+      if (!h->comm_off) NK(ncclAllReduce(gs, gs, (size_t)c.plpad, nccl_dt(c.G), ncclSum, h->dp_comm, h->s_comm));
     }
     return gs;
   }
@@ -895,7 +898,7 @@ static void* reduce_scatter(lga_handle* h, int j) {
   if (c.D > 1) {
     h->last.rs_calls++;
     h->last.rs_bytes += (uint64_t)(c.D - 1) * c.S * dt_size(c.G);
-    if (!c.no_comm)
+    if (!h->comm_off)
       NK(ncclReduceScatter(gs, shard_g, (size_t)c.S, nccl_dt(c.G), ncclSum, h->dp_comm, h->s_comm));
   }
   return shard_g;
@@ -910,7 +913,7 @@ static void rs_adam_peer(lga_handle* h, int j) {
   h->last.rs_calls++;
   h->last.rs_bytes += (uint64_t)(c.D - 1) * c.S * dt_size(c.G);
   const unsigned long long D = (unsigned long long)c.D, R = c.keep ? 1ull : 2ull;
-  if (!c.no_comm) {
+  if (!h->comm_off) {
     dp_signal(h->dp_flag_dev, c.D, DPF_GRAD * c.Lloc + j, h->s_comm);
     KCHECK();
     wait_flag(h->dpf + DPF_GRAD * c.Lloc + j, h->tstep, D, D, h->s_comm);
@@ -922,7 +925,7 @@ static void rs_adam_peer(lga_handle* h, int j) {
   const int64_t off = (int64_t)j * c.S;
   const int64_t goff = (int64_t)j * c.plpad + (int64_t)h->replica * c.S;
   const int p = prof_begin(h, h->s_comm);
-  if (c.no_comm)
+  if (h->comm_off)
     adamw(eoff(stage_buf(h, j), c.G, (int64_t)h->replica * c.S), c.G, gscale, h->master + off, h->mom + off,
           h->var + off, eoff(h->pshard, c.E, off), c.E, c.retain ? h->gkeep + off : nullptr, c.S, c.lr, c.b1, c.b2,
           c.eps, c.wd, h->tstep, h->s_comm);
@@ -933,7 +936,7 @@ static void rs_adam_peer(lga_handle* h, int j) {
   KCHECK();
   const double per = (double)c.D * dt_size(c.G) + 24.0 + (double)dt_size(c.E) + (c.retain ? 4.0 : 0.0);
   prof_end(h, p, h->s_comm, FAM_ADAM, per * (double)c.S);
-  if (!c.no_comm) {
+  if (!h->comm_off) {
     dp_signal(h->dp_flag_dev, c.D, DPF_PARAM * c.Lloc + j, h->s_comm);
     KCHECK();
   }
@@ -952,7 +955,7 @@ static void allreduce_adam_peer(lga_handle* h, int j) {
   h->last.allreduce_calls++;
   h->last.allreduce_bytes += 2ull * (c.D - 1) * (uint64_t)Sr * eg;
   void* gs = stage_buf(h, j);
-  if (!c.no_comm) {
+  if (!h->comm_off) {
     const unsigned long long D = (unsigned long long)c.D;
     dp_signal(h->dp_flag_dev, c.D, DPF_GRAD * c.Lloc + j, h->s_comm);
     KCHECK();
@@ -988,7 +991,7 @@ static void rs_acc_peer(lga_handle* h, int j, int m) {
   h->last.rs_bytes += (uint64_t)(c.D - 1) * c.S * dt_size(c.G);
   const unsigned long long D = (unsigned long long)c.D, N = (unsigned long long)c.N;
   float* acc = h->gshard_acc + (int64_t)j * c.S;
-  if (!c.no_comm) {
+  if (!h->comm_off) {
     dp_signal(h->dp_flag_dev, c.D, DPF_GRAD * c.Lloc + j, h->s_comm);
     KCHECK();
     wait_flag(h->dpf + DPF_GRAD * c.Lloc + j, h->tstep, D * N, D * (unsigned long long)(m + 1), h->s_comm);
@@ -1003,12 +1006,12 @@ static void rs_acc_peer(lga_handle* h, int j, int m) {
     KCHECK();
   }
   if (m == c.N - 1) {
-    if (!c.no_comm) {
+    if (!h->comm_off) {
       wait_flag(h->dpf + DPF_READ * c.Lloc + j, h->tstep, 2 * N * D, 2 * N * D, h->s_comm);
       KCHECK();
     }
     adam_layer(h, j, acc, DT::F32);
-    if (!c.no_comm) {
+    if (!h->comm_off) {
       dp_signal(h->dp_flag_dev, c.D, DPF_PARAM * c.Lloc + j, h->s_comm);
       KCHECK();
     }
@@ -1098,7 +1101,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
           h->recv_fwd += cw;
           h->last.p2p_recv_calls += cw;
           h->last.p2p_recv_bytes += (uint64_t)cw * mb * 4;
-          if (!c.no_comm) {
+          if (!h->comm_off) {
             count_wait(h, nullptr, 1);
             wait_flag(h->flags + 0, h->tstep, h->k_recv_fwd, h->recv_fwd, h->s_comp);
             KCHECK();
@@ -1113,7 +1116,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
         yo = ckpt_ptr(h, j + 1, m0);
       } else {  // write x_{i+1} straight into the next stage's checkpoint buffer (fused p2p)
         const int jn = local_index(c, i + 1);
-        yo = c.no_comm ? h->dscratch : h->next_ckpt + ((int64_t)jn * c.N + m0) * mb;
+        yo = h->comm_off ? h->dscratch : h->next_ckpt + ((int64_t)jn * c.N + m0) * mb;
       }
       layer_fwd(h, chunk_ws(h, j, m0), W, xin, yo, h->s_comp, cw);
       h->last.fwd_units += cw;
@@ -1121,7 +1124,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
         h->sent_fwd += cw;
         h->last.p2p_send_calls += cw;
         h->last.p2p_send_bytes += (uint64_t)cw * mb * 4;
-        if (!c.no_comm) {
+        if (!h->comm_off) {
           set_flag(h->next_flags + 0, h->tstep, h->k_send_fwd, h->sent_fwd, h->s_comp);
           KCHECK();
         }
@@ -1160,8 +1163,11 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
       count_wait(h, h->ev_ag[sl], 0);
       count_wait_end(h);
     }
-    if (!c.dp_ipc && h->rec_adam[gb]) CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));   // staging gb free again
-    if (c.dp_ipc && c.unpart && !c.no_comm) {   // every replica read last step's reduced slices of staging j
+    if (!c.dp_ipc && h->rec_adam[gb]) {   // staging gb free again (NCCL path: RS + AdamW of layer j + 2 done)
+      count_wait(h, h->ev_adam[gb], 0);
+      count_wait_end(h);
+    }
+    if (c.dp_ipc && c.unpart && !h->comm_off) {   // every replica read last step's reduced slices of staging j
       count_wait(h, nullptr, 0);
       wait_flag(h->dpf + DPF_READ * c.Lloc + j, h->tstep, (unsigned long long)c.D, 0ull, h->s_comp);
       KCHECK();
@@ -1182,7 +1188,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
         h->recv_bwd += c.c;
         h->last.p2p_recv_calls += c.c;
         h->last.p2p_recv_bytes += (uint64_t)c.c * mb * 4;
-        if (!c.no_comm) {
+        if (!h->comm_off) {
           count_wait(h, nullptr, 1);
           wait_flag(h->flags + 1, h->tstep, h->k_recv_bwd, h->recv_bwd, h->s_comp);
           KCHECK();
@@ -1197,14 +1203,14 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
       float* dx;
       if (i == 0) dx = h->dscratch;
       else if (!send) dx = dYc;
-      else dx = c.no_comm ? h->dscratch : h->prev_dY + m0 * mb;
+      else dx = h->comm_off ? h->dscratch : h->prev_dY + m0 * mb;
       layer_bwd(h, w, W, xin, dYc, dx, k, nchunks, j, h->s_comp, dye_ready, dx_e);
       h->last.bwd_units += c.c;
       if (send) {
         h->sent_bwd += c.c;
         h->last.p2p_send_calls += c.c;
         h->last.p2p_send_bytes += (uint64_t)c.c * mb * 4;
-        if (!c.no_comm) {
+        if (!h->comm_off) {
           set_flag(h->prev_flags + 1, h->tstep, h->k_send_bwd, h->sent_bwd, h->s_comp);
           KCHECK();
         }
@@ -1276,8 +1282,11 @@ static void step_standard(lga_handle* h, const float* x, const float* T) {
         count_wait(h, h->ev_ag[sl], 0);
         count_wait_end(h);
       }
-      if (!c.dp_ipc && h->rec_adam[gb]) CK(cudaStreamWaitEvent(h->s_comp, h->ev_adam[gb], 0));
-      if (c.dp_ipc && !c.no_comm) {   // every replica read its slice of the previous micro-batch's staging j
+      if (!c.dp_ipc && h->rec_adam[gb]) {   // staging gb free again (NCCL path)
+        count_wait(h, h->ev_adam[gb], 0);
+        count_wait_end(h);
+      }
+      if (c.dp_ipc && !h->comm_off) {   // every replica read its slice of the previous micro-batch's staging j
         count_wait(h, nullptr, 0);
         wait_flag(h->dpf + DPF_GREAD * c.Lloc + j, h->tstep, (unsigned long long)c.D * c.N, (unsigned long long)c.D * m,
                   h->s_comp);
@@ -1666,14 +1675,18 @@ static void issue_step(lga_handle* h, const float* x, const float* T, bool host_
   mse_finish(h->loss_dev + 1, c.N, 1.0, h->loss_dev, h->s_comp);
   KCHECK();
   h->last.allreduce_calls += 1;   // the loss (plus, unpartitioned, the per-layer gradient all-reduces)
-  if (h->world > 1 && !c.no_comm) {   // over peer memory (every rank gets the same rank-order sum)
+  if (h->world > 1 && !h->comm_off) {   // over peer memory (every rank gets the same rank-order sum)
+    count_wait(h, nullptr, 0);          // the kernel waits for the peers' losses: an exposed wait
     loss_allreduce_peer(h->loss_dev, h->w_loss_dev, h->w_flag_dev, h->rank, h->world, h->tstep, h->wflags + 0,
                         h->loss_ring, h->s_comp);
     KCHECK();
+    count_wait_end(h);
   }
   CK(cudaMemcpyAsync(h->loss_host, h->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, h->s_comp));
+  // the step ends when the last reduce-scatter + AdamW (layer 0's, the exposed tail) has finished
   CK(cudaEventRecord(h->ev_comm_end, h->s_comm));
-  CK(cudaStreamWaitEvent(h->s_comp, h->ev_comm_end, 0));
+  count_wait(h, h->ev_comm_end, 0);
+  count_wait_end(h);
 }
 
 // Capture issue_step into a graph (LGA_FLAG_NO_GRAPH off, device inputs).  False on any capture failure
@@ -1724,6 +1737,7 @@ static lga_status run_step(lga_handle* h, const float* x, const float* T, double
   ABI_TRY
   CK(cudaSetDevice(h->dev));
   h->t += 1;
+  h->comm_off = c.no_comm && h->t > 1;
   CK(cudaEventRecord(h->ev_t0, h->user));
   // CUDA graph of the whole step: captured at the second device-input call, replayed while the input
   // pointers stay the same; the first call (lazy initialisation) and host-input calls run eagerly
