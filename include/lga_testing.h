@@ -23,7 +23,7 @@ int lgatest_gemm(int path, int M, int N, int K, const void* A, int64_t lda, int 
                  const float* acc_in, void* aux, int aux_dt, void* out, int64_t ldo, int out_dt, uintptr_t stream);
 
 /* Attention forward / backward on packed qkv [nseq*seq][3d] (head h at column h*dh of q, k, v);
- * path 0 = fp32 SIMT, 1 = bf16 tensor cores.  o, dO: [nseq*seq][d]; lse, dsum: [nseq][heads][seq]. */
+ * path 0 = fp32 SIMT, 1 = bf16 tensor cores (tcgen05).  o, dO: [nseq*seq][d]; lse, dsum: [nseq][heads][seq]. */
 int lgatest_attn_fwd(int path, int nseq, int seq, int heads, int dh, int causal, const void* qkv, void* o, float* lse,
                      uintptr_t stream);
 int lgatest_attn_bwd(int path, int nseq, int seq, int heads, int dh, int causal, const void* qkv, const void* o,

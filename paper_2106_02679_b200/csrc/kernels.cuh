@@ -66,9 +66,6 @@ void attn_fwd_f32(const AttnArgs& a, cudaStream_t st);
 void attn_bwd_f32(const AttnArgs& a, cudaStream_t st);
 cudaError_t attn_fwd_bf16(const AttnArgs& a, cudaStream_t st);  // tcgen05 + TMA + TMEM (k_attn_tc.cu)
 cudaError_t attn_bwd_bf16(const AttnArgs& a, cudaStream_t st);  // tcgen05 (k_attn_tc_bwd.cu)
-// warp-level mma.sync variants (k_attn_bf16.cu), kept as the comparison baseline of the tcgen05 kernels
-void attn_fwd_bf16_mma(const AttnArgs& a, cudaStream_t st);
-void attn_bwd_bf16_mma(const AttnArgs& a, cudaStream_t st);
 
 // ------------------------------------------------------------------ LayerNorm
 // y = (x - mu) * rstd * gamma + beta, biased variance (reading A-1).  x fp32 [rows][d];

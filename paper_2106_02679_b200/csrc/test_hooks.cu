@@ -46,7 +46,7 @@ extern "C" int lgatest_attn_fwd(int path, int nseq, int seq, int heads, int dh, 
     const cudaError_t e = attn_fwd_bf16(a, st);
     if (e != cudaSuccess) return (int)e;
   } else {
-    attn_fwd_bf16_mma(a, st);
+    return (int)cudaErrorInvalidValue;
   }
   return (int)cudaGetLastError();
 }
@@ -63,7 +63,7 @@ extern "C" int lgatest_attn_bwd(int path, int nseq, int seq, int heads, int dh, 
     const cudaError_t e = attn_bwd_bf16(a, st);
     if (e != cudaSuccess) return (int)e;
   } else {
-    attn_bwd_bf16_mma(a, st);
+    return (int)cudaErrorInvalidValue;
   }
   return (int)cudaGetLastError();
 }

@@ -128,8 +128,8 @@ def _attn_ref(qkv, nseq, s, H, dh, causal):
 
 
 @pytest.mark.parametrize("path,dh,s,causal,mag", [(0, 16, 37, 1, 1), (0, 64, 128, 0, 1), (1, 64, 256, 1, 1),
-                                                  (1, 128, 200, 1, 1), (2, 128, 200, 1, 1), (2, 64, 300, 0, 1),
-                                                  (1, 64, 300, 0, 1), (1, 128, 512, 0, 1), (1, 64, 1024, 1, 1),
+                                                  (1, 128, 200, 1, 1), (1, 64, 300, 0, 1), (1, 128, 512, 0, 1),
+                                                  (1, 64, 1024, 1, 1),
                                                   (1, 128, 1024, 1, 6), (1, 64, 700, 0, 6), (0, 32, 300, 1, 6)])
 def test_attention_fwd_bwd(path, dh, s, causal, mag, nseq=2, H=3):
     d = H * dh

@@ -1,3 +1,5 @@
+// NOT BUILT: the round-1 warp-level mma.sync flash attention (the comparison baseline the tcgen05 kernels
+// replaced); kept for reference only, outside the product library.
 // k_attn_bf16.cu -- bf16 causal multi-head attention forward / backward on the tensor cores
 // (warp-level mma.sync m16n8k16, fp32 accumulate), flash-style (O3 / O5 of DESIGN.md):
 //   forward : online softmax over 64-key tiles, o and the per-row log-sum-exp written once;

@@ -54,7 +54,7 @@ def attn(args):
     dsum = torch.empty(nseq, H, s, device="cuda")
     dqkv = torch.empty_like(qkv)
     flops = 4.0 * dh * (s * (s + 1) / 2) * H * nseq
-    for path, name in ((1, "fwd tcgen05"), (2, "fwd mma.sync")):
+    for path, name in ((1, "fwd tcgen05"),):
         ms = timeit(lambda: L.lgatest_attn_fwd(path, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), st))
         print(f"attn {name:14s} nseq={nseq} s={s} H={H} dh={dh}: {ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s")
     L.lgatest_attn_fwd(1, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), st)
