@@ -22,6 +22,13 @@ int lgatest_gemm(int path, int M, int N, int K, const void* A, int64_t lda, int 
                  int64_t ldb, int b_kmajor, int kind, const void* bias, int bias_dt, const float* res,
                  const float* acc_in, void* aux, int aux_dt, void* out, int64_t ldo, int out_dt, uintptr_t stream);
 
+/* lgatest_gemm with a split-K workspace of ws_floats fp32 (device): tile-starved shapes (fewer 128 x 128 tiles
+ * than SMs, M % 128 == 0, plain-store epilogue) then run split over K with a fixed-order reduce.  Returns the
+ * split count used through *split_used (host int, may be NULL) or a negative cudaError_t. */
+int lgatest_gemm_ws(int M, int N, int K, const void* A, int64_t lda, int a_kmajor, const void* B, int64_t ldb,
+                    int b_kmajor, const void* bias, int bias_dt, const float* acc_in, void* out, int64_t ldo,
+                    int out_dt, float* ws, int64_t ws_floats, int* split_used, uintptr_t stream);
+
 /* Attention forward / backward on packed qkv [nseq*seq][3d] (head h at column h*dh of q, k, v);
  * path 0 = fp32 SIMT, 1 = bf16 tensor cores (tcgen05).  o, dO: [nseq*seq][d]; lse, dsum: [nseq][heads][seq]. */
 int lgatest_attn_fwd(int path, int nseq, int seq, int heads, int dh, int causal, const void* qkv, void* o, float* lse,

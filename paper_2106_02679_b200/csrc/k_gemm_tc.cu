@@ -355,10 +355,13 @@ __device__ __forceinline__ void epilogue_loop(const GemmArgs& g, const EpiMaps& 
   if (TMA_EPI && lane == 0) bulk_wait0();
 }
 
+// Split-K (g.split_k = S > 1): the tile space is S stacked copies of the M x N tiles; copy ks covers k-blocks
+// [ks * nkper, (ks + 1) * nkper) and its epilogue `ge` (built on the host: M' = S M rows of fp32 workspace, plain
+// store) writes the partial sum at rows ks M .. ks M + M - 1.  splitk_reduce_kernel then applies g.epi.
 template <int BN, bool A_MN, bool B_MN, bool TMA_EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ EpiMaps em, const GemmArgs g) {
+                   const __grid_constant__ EpiMaps em, const GemmArgs g, const GemmArgs ge) {
   using SM = Smem<BN>;
   constexpr int STAGES = SM::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -371,9 +374,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 2 * EPI_WARPS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int num_m = (g.M + BM - 1) / BM, num_n = (g.N + BN - 1) / BN;
+  const int S = g.split_k;
+  const int num_m1 = (g.M + BM - 1) / BM;
+  const int num_m = num_m1 * S, num_n = (g.N + BN - 1) / BN;   // stacked m-blocks: split ks owns [ks num_m1, ..)
   const int num_tiles = num_m * num_n;
-  const int nk = (g.K + BK - 1) / BK;
+  const int nk_all = (g.K + BK - 1) / BK;
+  const int nkper = (nk_all + S - 1) / S;
+  // k-block range of a (stacked) m-block
+  auto krange = [&](int mb, int& kb0, int& kb1) {
+    const int ks = mb / num_m1;
+    kb0 = ks * nkper;
+    kb1 = min(nk_all, kb0 + nkper);
+  };
   constexpr int GM = 8;   // tile raster: groups of GM m-blocks sweep all n-blocks (L2 reuse of B)
 
   if (warp == 0 && lane == 0) {
@@ -405,10 +417,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        int mb, nb;
+        int mb, nb, kb0, kb1;
         tile_coords(t, mb, nb);
-        const int m0 = mb * BM, n0 = nb * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        krange(mb, kb0, kb1);
+        const int m0 = (mb % num_m1) * BM, n0 = nb * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * SM::STAGE_BYTES;
           uint8_t* sb = sa + SM::A_BYTES;
@@ -445,17 +458,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
         const int as = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
+        int mb, nb, kb0, kb1;
+        tile_coords(t, mb, nb);
+        krange(mb, kb0, kb1);
         mbar_wait(&tempty[as], aphase ^ 1);
         fence_after();
         const uint32_t dtm = tmem_base + as * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           fence_after();
           const uint64_t ad = desc_add(ad0, stage * SM::STAGE_BYTES), bd = desc_add(bd0, stage * SM::STAGE_BYTES);
           if (leader) {
 #pragma unroll
             for (int k = 0; k < BK / UMMA_K; ++k)
-              umma_f16(dtm, desc_add(ad, k * KSTEP_A), desc_add(bd, k * KSTEP_B), idesc, (kb | k) != 0 ? 1u : 0u);
+              umma_f16(dtm, desc_add(ad, k * KSTEP_A), desc_add(bd, k * KSTEP_B), idesc,
+                       (kb != kb0 || k != 0) ? 1u : 0u);
             umma_commit(&empty[stage]);   // frees the smem slot when these MMAs complete
           }
           __syncwarp();
@@ -466,7 +483,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp >= EPI_WARP0) {  // ===== epilogue: TMEM -> registers -> fused epilogue -> global
-    epilogue_loop<BN, TMA_EPI>(g, em, smem + SM::EPI_OFF, ebar, tfull, tmem_base, num_tiles, blockIdx.x, gridDim.x,
+    epilogue_loop<BN, TMA_EPI>(ge, em, smem + SM::EPI_OFF, ebar, tfull, tmem_base, num_tiles, blockIdx.x, gridDim.x,
                                0, BM,
                                [&](int t, int& mb, int& nb) { tile_coords(t, mb, nb); },
                                [&](int as) { mbar_arrive(&tempty[as]); });
@@ -669,7 +686,7 @@ static bool epi_maps(const GemmArgs& g, EpiMaps* em) {
 
 template <int BN, bool A_MN, bool B_MN, bool TMA_EPI>
 static cudaError_t launch_k(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const GemmArgs& g,
-                            cudaStream_t st) {
+                            const GemmArgs& ge, cudaStream_t st) {
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, TMA_EPI>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -677,14 +694,82 @@ static cudaError_t launch_k(const CUtensorMap& ta, const CUtensorMap& tb, const 
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * g.split_k;
   const int grid = std::min(tiles, num_sms());
-  note_launch(), kern<<<grid, NUM_THREADS, Smem<BN>::TOTAL, st>>>(ta, tb, em, g);
+  note_launch(), kern<<<grid, NUM_THREADS, Smem<BN>::TOTAL, st>>>(ta, tb, em, g, ge);
   return cudaGetLastError();
 }
 
+// split-K finish: out = epi(sum_{ks < S} ws[ks]) in split order (deterministic); 4 columns per thread
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int S, int M, int N,
+                                                            const Epi e) {
+  const int64_t MN = (int64_t)M * N, n4 = MN / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = reinterpret_cast<const float4*>(ws)[i];
+    for (int ks = 1; ks < S; ++ks) {
+      const float4 b = reinterpret_cast<const float4*>(ws + ks * MN)[i];
+      a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
+    }
+    const int64_t m = (i * 4) / N, n = (i * 4) % N;
+    float v[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (e.bias) v[j] += ld_elem(e.bias, n + j, e.bias_dt);
+      if (e.res) v[j] += e.res[m * e.ldr + n + j];
+      if (e.acc_in) v[j] += e.acc_in[m * e.ldacc + n + j];
+      st_elem(e.out, m * e.ldo + n + j, e.out_dt, v[j]);
+    }
+  }
+}
+
+// Split count for a tile-starved GEMM: S minimising waves(tiles * S) / S (each split does 1/S of K), at least
+// 8 k-blocks per split, workspace S M N floats within capacity; 1 = no split.
+int choose_split(const GemmArgs& g, int tiles, int ns) {
+  if (!g.splitk_ws || g.M % BM || g.N % 4 || g.epi.kind != EPI_STORE || tiles >= ns) return 1;
+  const int nk = (g.K + BK - 1) / BK;
+  int best = 1;
+  double best_cost = 1.0;
+  for (int S = 2; S <= 16; ++S) {
+    if (nk / S < 8 || (int64_t)S * g.M * g.N > g.splitk_ws_floats) break;
+    const double cost = (double)((tiles * S + ns - 1) / ns) / S + 0.02 * S;   // + the reduce pass
+    if (cost < best_cost - 1e-9) best_cost = cost, best = S;
+  }
+  if (best > 1) {   // every split non-empty
+    const int nkper = (nk + best - 1) / best;
+    best = (nk + nkper - 1) / nkper;
+  }
+  return best;
+}
+
 template <int BN, bool A_MN, bool B_MN>
-static cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
+static cudaError_t launch(const GemmArgs& g0, cudaStream_t st) {
+  GemmArgs g = g0;
+  g.split_k = BN == 128 ? choose_split(g, ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN), num_sms()) : 1;
+  if (g.split_k > 1) {   // partial sums into the workspace (plain fp32 stores), then the fixed-order reduce
+    GemmArgs ge = g;
+    ge.M = g.split_k * g.M;
+    ge.epi = Epi{};
+    ge.epi.out = g.splitk_ws;
+    ge.epi.ldo = g.N;
+    ge.epi.out_dt = DT::F32;
+    CUtensorMap ta, tb;
+    cudaError_t e;
+    if (!A_MN) e = make_map(&ta, g.A, DT::BF16, g.K, g.M, g.lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+    else e = make_map(&ta, g.A, DT::BF16, g.M, g.K, g.lda, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (e != cudaSuccess) return e;
+    if (!B_MN) e = make_map(&tb, g.B, DT::BF16, g.K, g.N, g.ldb, BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    else e = make_map(&tb, g.B, DT::BF16, g.N, g.K, g.ldb, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (e != cudaSuccess) return e;
+    EpiMaps em;
+    if (epi_maps(ge, &em)) e = launch_k<BN, A_MN, B_MN, true>(ta, tb, em, g, ge, st);
+    else memset(&em, 0, sizeof(em)), e = launch_k<BN, A_MN, B_MN, false>(ta, tb, em, g, ge, st);
+    if (e != cudaSuccess) return e;
+    const int64_t n4 = (int64_t)g.M * g.N / 4;
+    const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)num_sms() * 4);
+    note_launch(), splitk_reduce_kernel<<<grid, 256, 0, st>>>(g.splitk_ws, g.split_k, g.M, g.N, g.epi);
+    return cudaGetLastError();
+  }
+  g.split_k = 1;
   CUtensorMap ta, tb;
   cudaError_t e;
   if (!A_MN) e = make_map(&ta, g.A, DT::BF16, g.K, g.M, g.lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -694,9 +779,9 @@ static cudaError_t launch(const GemmArgs& g, cudaStream_t st) {
   else e = make_map(&tb, g.B, DT::BF16, g.N, g.K, g.ldb, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B);
   if (e != cudaSuccess) return e;
   EpiMaps em;
-  if (epi_maps(g, &em)) return launch_k<BN, A_MN, B_MN, true>(ta, tb, em, g, st);
+  if (epi_maps(g, &em)) return launch_k<BN, A_MN, B_MN, true>(ta, tb, em, g, g, st);
   memset(&em, 0, sizeof(em));
-  return launch_k<BN, A_MN, B_MN, false>(ta, tb, em, g, st);
+  return launch_k<BN, A_MN, B_MN, false>(ta, tb, em, g, g, st);
 }
 
 template <bool A_MN, bool B_MN, bool TMA_EPI>
@@ -756,7 +841,9 @@ cudaError_t gemm_bf16_tc(const GemmArgs& g, cudaStream_t st) {
   const int pair_tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256);
   const double c_pair = (double)((pair_tiles + ns / 2 - 1) / (ns / 2)) * 2.0 / 1.0;
   const double c_256 = (double)((tiles256 + ns - 1) / ns) * 2.0 / 0.85;
-  const double c_128 = (double)((tiles128 + ns - 1) / ns) * 1.0 / 0.70;
+  double c_128 = (double)((tiles128 + ns - 1) / ns) * 1.0 / 0.70;
+  const int split = tc::choose_split(g, tiles128, ns);   // tile-starved: 128 x 128 tiles split over K
+  if (split > 1) c_128 = ((double)((tiles128 * split + ns - 1) / ns) / split + 0.02 * split) / 0.70;
   const bool wide = g.N > 128 && c_256 < c_128;
   if (gemm_mode() == 1 && g.N > 128 && c_pair <= std::min(c_256, c_128))
     return amn ? (bmn ? tc::launch2<true, true>(g, st) : tc::launch2<true, false>(g, st))

@@ -38,8 +38,12 @@ struct GemmArgs {
   const void* A = nullptr; int64_t lda = 0; bool a_kmajor = true;
   const void* B = nullptr; int64_t ldb = 0; bool b_kmajor = true;
   Epi epi;
-  int split_k = 1;            // tensor-core path: >1 = deterministic split over K (needs workspace)
-  float* splitk_ws = nullptr; // [split_k][M][N] fp32
+  // tensor-core path, deterministic split over K (chosen by gemm_bf16_tc when the tile count would leave SMs
+  // idle and M % 128 == 0): partial sums go to the workspace [split][M][N] fp32, then one reduce pass adds them
+  // in split order and runs the epilogue.  splitk_ws = nullptr disables it.
+  int split_k = 1;
+  float* splitk_ws = nullptr;
+  int64_t splitk_ws_floats = 0;   // workspace capacity
 };
 
 void gemm_f32_simt(const GemmArgs& g, cudaStream_t st);       // fp32 operands, CUDA cores

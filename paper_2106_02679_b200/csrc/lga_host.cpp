@@ -243,6 +243,8 @@ struct lga_handle {
   // backward temporaries (chunk-sized)
   void *dYe = nullptr, *dh1e = nullptr, *dO = nullptr, *dqkv = nullptr;
   float *dC = nullptr, *dh1 = nullptr, *dsum = nullptr, *partial = nullptr;
+  float* splitk_ws = nullptr;   // split-K partial sums of tile-starved GEMMs (small-d weight gradients)
+  int64_t splitk_floats = 0;
   double *mse_partial = nullptr, *loss_dev = nullptr, *loss_host = nullptr;
   float *xin = nullptr, *tin = nullptr;  // device copies for lga_step_host
   unsigned long long* flags = nullptr;   // [0] fwd receive count, [1] bwd receive count
@@ -355,6 +357,8 @@ static void plan_arena(lga_handle* h) {
   const int64_t pln = (int64_t)ln_bwd_blocks((int)T, (int)d) * 2 * d;
   h->partial_floats = std::max(pcol, pln);
   h->partial = A.take<float>(h->partial_floats);
+  h->splitk_floats = c.bf16 ? std::min<int64_t>(16LL * 4 * d * d, (int64_t)1 << 25) : 0;
+  h->splitk_ws = c.bf16 ? A.take<float>(h->splitk_floats) : nullptr;
   h->mse_partial = A.take<double>(mse_blocks(act) + 64);
   h->loss_dev = A.take<double>(c.N + 8);
   h->xin = A.take<float>(act);
@@ -404,6 +408,8 @@ static void gemm(lga_handle* h, GemmArgs g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
   const int p = prof_begin(h, st);
   if (h->c.bf16) {
+    g.splitk_ws = h->splitk_ws;
+    g.splitk_ws_floats = h->splitk_floats;
     CK(gemm_bf16_tc(g, st));
   } else {
     gemm_f32_simt(g, st);

@@ -28,6 +28,25 @@ extern "C" int lgatest_gemm(int path, int M, int N, int K, const void* A, int64_
   return (int)gemm_bf16_tc(g, st);
 }
 
+namespace lga { namespace tc { int choose_split(const GemmArgs& g, int tiles, int ns); } }
+
+extern "C" int lgatest_gemm_ws(int M, int N, int K, const void* A, int64_t lda, int a_kmajor, const void* B,
+                               int64_t ldb, int b_kmajor, const void* bias, int bias_dt, const float* acc_in, void* out,
+                               int64_t ldo, int out_dt, float* ws, int64_t ws_floats, int* split_used,
+                               uintptr_t stream) {
+  GemmArgs g;
+  g.M = M; g.N = N; g.K = K;
+  g.A = A; g.lda = lda; g.a_kmajor = a_kmajor != 0;
+  g.B = B; g.ldb = ldb; g.b_kmajor = b_kmajor != 0;
+  g.epi.bias = bias; g.epi.bias_dt = (DT)bias_dt;
+  g.epi.acc_in = acc_in; g.epi.ldacc = ldo;
+  g.epi.out = out; g.epi.ldo = ldo; g.epi.out_dt = (DT)out_dt;
+  g.splitk_ws = ws;
+  g.splitk_ws_floats = ws_floats;
+  if (split_used) *split_used = tc::choose_split(g, ((M + 127) / 128) * ((N + 127) / 128), num_sms());
+  return (int)gemm_bf16_tc(g, reinterpret_cast<cudaStream_t>(stream));
+}
+
 static AttnArgs mk(int nseq, int seq, int heads, int dh, int causal) {
   AttnArgs a;
   a.nseq = nseq; a.seq = seq; a.heads = heads; a.dh = dh; a.d = heads * dh; a.causal = causal != 0;

@@ -107,6 +107,39 @@ def test_tc_gemm_epilogues(kind, M, N, K):
         assert relerr(out.float(), acc * gl) < 5e-3
 
 
+L.lgatest_gemm_ws.restype = C.c_int
+L.lgatest_gemm_ws.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_int,
+                              C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64,
+                              C.POINTER(C.c_int), C.c_void_p]
+
+
+@pytest.mark.parametrize("M,N,K,obf,acc,split", [(768, 768, 32768, False, True, True), (768, 2304, 32768, True, False, True),
+                                                 (3072, 768, 32768, False, True, False),   # 144 tiles: one full wave
+                                                 (256, 384, 4096, False, False, True), (768, 768, 1000, False, False, True)])
+def test_tc_gemm_split_k_weight_gradient(M, N, K, obf, acc, split):
+    """Tile-starved weight gradients (d = 768: 36 tiles of 128 x 128 on 148 SMs) split over K with a fixed-order
+    reduce: the reference product to fp32 rounding, bitwise repeatable.  K = 1000 has 16 k-blocks, a ragged last
+    one, split in 2; 144 tiles fill a wave and stay one pass."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn(K, M, device="cuda", generator=g).bfloat16()     # X [tokens][M], read MN-major (wgrad form)
+    B = torch.randn(K, N, device="cuda", generator=g).bfloat16()     # dY [tokens][N]
+    acc_in = torch.randn(M, N, device="cuda", generator=g) if acc else None
+    ws = torch.empty(16 * M * N, device="cuda")
+    outs = []
+    for _ in range(2):
+        out = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16 if obf else torch.float32)
+        used = C.c_int(0)
+        r = L.lgatest_gemm_ws(M, N, K, P(A), M, 0, P(B), N, 0, None, 0, P(acc_in), P(out), N, DT(out), P(ws), ws.numel(),
+                              C.byref(used), stream())
+        assert r == 0
+        torch.cuda.synchronize()
+        outs.append(out.clone())
+    ref = A.float().t() @ B.float() + (acc_in if acc else 0)
+    assert relerr(outs[0].float(), ref) < (5e-3 if obf else 1e-5)
+    assert torch.equal(outs[0], outs[1])
+    assert (used.value > 1) == split, used.value
+
+
 @pytest.mark.parametrize("amaj,bmaj", [(True, True), (True, False), (False, False)])
 def test_simt_gemm_f32(amaj, bmaj):
     M, N, K = 131, 77, 93
