@@ -20,7 +20,9 @@ extern "C" {
  * B[k*ldb+n].  path 0 = fp32 SIMT (operands fp32), 1 = tcgen05 (operands bf16). */
 int lgatest_gemm(int path, int M, int N, int K, const void* A, int64_t lda, int a_kmajor, const void* B,
                  int64_t ldb, int b_kmajor, int kind, const void* bias, int bias_dt, const float* res,
-                 const float* acc_in, void* aux, int aux_dt, void* out, int64_t ldo, int out_dt, uintptr_t stream);
+                 const float* acc_in, void* aux, int aux_dt, void* out, int64_t ldo, int out_dt, float* colsum,
+                 uintptr_t stream);
+/* colsum (path 1, kind 2 = GELU bwd, may be NULL): per 32-row strip column sums of out, ceil(M/32) x N fp32. */
 
 /* lgatest_gemm with a split-K workspace of ws_floats fp32 (device): tile-starved shapes (fewer 128 x 128 tiles
  * than SMs, M % 128 == 0, plain-store epilogue) then run split over K with a fixed-order reduce.  Returns the
@@ -34,7 +36,9 @@ int lgatest_gemm_ws(int M, int N, int K, const void* A, int64_t lda, int a_kmajo
 int lgatest_attn_fwd(int path, int nseq, int seq, int heads, int dh, int causal, const void* qkv, void* o, float* lse,
                      uintptr_t stream);
 int lgatest_attn_bwd(int path, int nseq, int seq, int heads, int dh, int causal, const void* qkv, const void* o,
-                     const float* lse, const void* dO, float* dsum, void* dqkv, uintptr_t stream);
+                     const float* lse, const void* dO, float* dsum, void* dqkv, float* colsum, uintptr_t stream);
+/* colsum (path 1, may be NULL): column sums of dqkv per (sequence, 128-row tile, 32-row quadrant),
+ * [nseq * ceil(seq/128) * 4][3 d] fp32. */
 
 /* LayerNorm forward (reading A-1): y = (x - mu) rstd gamma + beta over rows of d; x fp32, gamma / beta in
  * p_dt, y in y_dt, stats[r] = (mu, rstd) as float2. */
@@ -44,8 +48,9 @@ int lgatest_ln_fwd(const float* x, const void* gamma, const void* beta, int p_dt
  * (e_dt), plus deterministic column partials; the fixed-order finisher then writes dgamma = sum dout * xhat and
  * dbeta = sum dout (fp32, d each).  `partial` is scratch of lgatest_ln_bwd_partial_floats(rows, d) floats. */
 int lgatest_ln_bwd(const float* dout, const float* x, const float* stats, const void* gamma, int p_dt,
-                   const float* resid, float* dx, void* dx_e, int e_dt, float* dgamma, float* dbeta, float* partial,
-                   int rows, int d, uintptr_t stream);
+                   const float* resid, float* dx, void* dx_e, int e_dt, float* dgamma, float* dbeta, float* sum_resid,
+                   float* sum_dx, float* partial, int rows, int d, uintptr_t stream);
+/* sum_resid / sum_dx (may be NULL; either non-NULL selects the 4-sum kernels): column sums of resid and dx. */
 int64_t lgatest_ln_bwd_partial_floats(int rows, int d);
 /* Bias gradient as the step computes it: out[n] = (acc_in ? acc_in[n] : 0) + sum_r X[r][n] (fixed row
  * blocks, fixed order); X in x_dt with leading dimension ldx; out in out_dt.  `partial` is scratch of

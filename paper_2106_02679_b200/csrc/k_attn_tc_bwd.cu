@@ -66,13 +66,22 @@ __global__ void __launch_bounds__(256) dsum_kernel(AttnArgs a) {
 }
 
 // TMEM row -> bf16 global row.  tcgen05.ld is warp-collective: every lane executes it, only
-// lanes with `valid` store.
+// lanes with `valid` store.  csum != nullptr: also the column sums over the warp's 32 rows (invalid rows count
+// 0) into csum[0 .. ncols) -- this warp's partial of the qkv bias gradient (fp32, before the bf16 rounding).
 __device__ __forceinline__ void store_row_bf16_global(__nv_bfloat16* dst, uint32_t taddr, int ncols, float scale,
-                                                      bool valid) {
+                                                      bool valid, float* csum = nullptr) {
+  const int lane = threadIdx.x & 31;
   for (int c = 0; c < ncols; c += 16) {   // ncols is a multiple of 16
     uint32_t r[16];
     tmem_ld16_nowait(taddr + c, r);
     tmem_wait_ld();
+    if (csum) {
+      float w[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) w[i] = valid ? __uint_as_float(r[i]) * scale : 0.f;
+      const float cs = warp_colsum16(w);
+      if (lane < 16) csum[c + lane] = cs;
+    }
     if (!valid) continue;
     float t[16];
 #pragma unroll
@@ -362,8 +371,9 @@ __global__ void __launch_bounds__(NT, 1)
     constexpr int OC = DH / 4;   // output columns per (group, half)
     const int oq = grp * 2 + hf;
     __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + kj) * 3 * d + h * DH + oq * OC;
-    store_row_bf16_global(out + d, t_dk + lrow + oq * OC, OC, 1.f, kj < s);
-    store_row_bf16_global(out + 2 * d, t_dv + lrow + oq * OC, OC, 1.f, kj < s);
+    float* cs = a.colsum ? a.colsum + ((int64_t)(sq * gridDim.x + kt) * 4 + qd) * 3 * d + h * DH + oq * OC : nullptr;
+    store_row_bf16_global(out + d, t_dk + lrow + oq * OC, OC, 1.f, kj < s, cs ? cs + d : nullptr);
+    store_row_bf16_global(out + 2 * d, t_dv + lrow + oq * OC, OC, 1.f, kj < s, cs ? cs + 2 * d : nullptr);
   }
   fence_before();
   __syncthreads();
@@ -586,7 +596,8 @@ __global__ void __launch_bounds__(NT, 1)
     fence_after();
     constexpr int OC = DH / 4;
     __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + q) * 3 * d + h * DH + cg * OC;
-    store_row_bf16_global(out, t_dq + lrow + cg * OC, OC, 1.f, q < s);
+    float* cs = a.colsum ? a.colsum + ((int64_t)(sq * nqt + qt) * 4 + qd) * 3 * d + h * DH + cg * OC : nullptr;
+    store_row_bf16_global(out, t_dq + lrow + cg * OC, OC, 1.f, q < s, cs);
   }
   fence_before();
   __syncthreads();

@@ -256,6 +256,14 @@ __device__ __forceinline__ void epilogue_loop(const GemmArgs& g, const EpiMaps& 
           tma_store_2d(&em.out, sb, n0, m0w);
           bulk_commit();
         }
+        if (e.colsum) {   // bias gradient partial of this 32-row strip (rows past M contribute 0)
+          if (m0w + lane >= g.M) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+          const float cs = warp_colsum32(v);
+          if (n0 + lane < g.N) e.colsum[(int64_t)(m0w >> 5) * g.N + n0 + lane] = cs;
+        }
         buf ^= 1;
       }
       fence_before();
@@ -281,6 +289,14 @@ __device__ __forceinline__ void epilogue_loop(const GemmArgs& g, const EpiMaps& 
       if (!TMA_EPI) {
         float v[32];
         tmem_ld32(taddr + ch * 32, v);
+        if (e.kind == EPI_GELU_BWD && e.colsum && n0 < g.N) {   // bias gradient partial (see the staged path)
+          float w[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            w[i] = (m < g.M && n0 + i < g.N) ? v[i] * gelu_grad_f(ld_elem(e.aux, m * e.ldaux + n0 + i, e.aux_dt)) : 0.f;
+          const float cs = warp_colsum32(w);
+          if (n0 + lane < g.N) e.colsum[(int64_t)(m0w >> 5) * g.N + n0 + lane] = cs;
+        }
         if (m < g.M && n0 < g.N) epi_chunk_direct(e, m, n0, (int)min(32, g.N - n0), v);
         continue;
       }

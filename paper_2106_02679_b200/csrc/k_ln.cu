@@ -204,7 +204,9 @@ __global__ void __launch_bounds__(256) ln_bwd_block(const float* __restrict__ do
 constexpr int LNF_ROWS = 4;
 static int lnf_grid(int rows) { return std::max(1, std::min((rows + LNF_ROWS - 1) / LNF_ROWS, num_sms() * 2)); }
 
-template <int CPL>
+// EXTRA: also the column sums of resid and of dx (partial rows 2 and 3 of each block's 4 d floats): the bias
+// gradients that are column sums of this kernel's input / output (pre-LN LN2: db2 = sum dY, db_o = sum dh1).
+template <int CPL, bool EXTRA>
 __global__ void __launch_bounds__(256, 2) ln_bwd_fused(const float* __restrict__ dout, const float* __restrict__ x,
                                                     const float2* __restrict__ stats, const void* gamma, DT pdt,
                                                     const float* __restrict__ resid, float* __restrict__ dx,
@@ -212,14 +214,25 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_fused(const float* __restrict__
   __shared__ float2 red[LNF_ROWS][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = warp * (32 * CPL) + lane * CPL;
-  float g[CPL], dg[CPL], db[CPL];
+  float g[CPL];
+  // column accumulators: dgamma, dbeta (+ EXTRA: sum resid, sum dx).  In registers without EXTRA; with it all
+  // four live in shared memory ([k][thread]: conflict-free) -- registers are full at CPL = 8 and would spill
+  float dg_r[EXTRA ? 1 : CPL], db_r[EXTRA ? 1 : CPL];
+  __shared__ float acc_x[EXTRA ? 4 * CPL : 1][EXTRA ? 256 : 1];
+  auto acc = [&](int which, int k) -> float& {   // which: 0 dgamma, 1 dbeta, 2 sum resid, 3 sum dx
+    if (EXTRA) return acc_x[which * CPL + k][threadIdx.x];
+    return which == 0 ? dg_r[EXTRA ? 0 : k] : db_r[EXTRA ? 0 : k];
+  };
 #pragma unroll
   for (int k = 0; k < CPL; k += 4) {
     const float4 t = ld4(gamma, pdt, c0 + k);
     g[k] = t.x, g[k + 1] = t.y, g[k + 2] = t.z, g[k + 3] = t.w;
   }
 #pragma unroll
-  for (int k = 0; k < CPL; ++k) dg[k] = 0.f, db[k] = 0.f;
+  for (int k = 0; k < CPL; ++k) {
+    acc(0, k) = 0.f, acc(1, k) = 0.f;
+    if (EXTRA) acc(2, k) = 0.f, acc(3, k) = 0.f;
+  }
   const float inv_d = 1.f / (float)d;
   for (int r0 = blockIdx.x * LNF_ROWS; r0 < rows; r0 += gridDim.x * LNF_ROWS) {
     float go[LNF_ROWS][CPL], xc[LNF_ROWS][CPL];
@@ -275,24 +288,28 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_fused(const float* __restrict__
         for (int e = 0; e < 4; ++e) {
           const float xh = xc[rr][k + e] * rstd;
           v[e] = rstd * (go[rr][k + e] * g[k + e] - m1[rr] - xh * m2[rr]);
-          dg[k + e] += go[rr][k + e] * xh;
-          db[k + e] += go[rr][k + e];
+          acc(0, k + e) += go[rr][k + e] * xh;
+          acc(1, k + e) += go[rr][k + e];
         }
         float4 o = make_float4(v[0], v[1], v[2], v[3]);
         if (resid) {
           const float4 q = *reinterpret_cast<const float4*>(resid + base + k);
           o.x += q.x, o.y += q.y, o.z += q.z, o.w += q.w;
+          if (EXTRA) acc(2, k) += q.x, acc(2, k + 1) += q.y, acc(2, k + 2) += q.z, acc(2, k + 3) += q.w;
         }
+        if (EXTRA) acc(3, k) += o.x, acc(3, k + 1) += o.y, acc(3, k + 2) += o.z, acc(3, k + 3) += o.w;
         *reinterpret_cast<float4*>(dx + base + k) = o;
         if (dx_e) st4(dx_e, edt, base + k, o);
       }
     }
   }
-  float* pg = partial + (int64_t)blockIdx.x * 2 * d + c0;
+  constexpr int NP = EXTRA ? 4 : 2;   // partial rows per block
+  float* pg = partial + (int64_t)blockIdx.x * NP * d + c0;
 #pragma unroll
   for (int k = 0; k < CPL; k += 4) {
-    *reinterpret_cast<float4*>(pg + k) = make_float4(dg[k], dg[k + 1], dg[k + 2], dg[k + 3]);
-    *reinterpret_cast<float4*>(pg + d + k) = make_float4(db[k], db[k + 1], db[k + 2], db[k + 3]);
+#pragma unroll
+    for (int w = 0; w < NP; ++w)
+      *reinterpret_cast<float4*>(pg + w * d + k) = make_float4(acc(w, k), acc(w, k + 1), acc(w, k + 2), acc(w, k + 3));
   }
 }
 
@@ -308,32 +325,43 @@ int ln_bwd_blocks(int rows, int d) {
   return lnf_ok(d) ? lnf_grid(rows) : (rows + LN_COL_ROWS - 1) / LN_COL_ROWS;
 }
 
+// sres / sdx (EXTRA): column sums of resid and of the dx the row kernel wrote (4 partial rows per block)
 __global__ void __launch_bounds__(256) ln_col_partial(const float* __restrict__ dout, const float* __restrict__ x,
-                                                      const float2* __restrict__ stats, float* __restrict__ partial,
-                                                      int rows, int d) {
+                                                      const float2* __restrict__ stats, const float* __restrict__ resid,
+                                                      const float* __restrict__ dx, bool extra,
+                                                      float* __restrict__ partial, int rows, int d) {
   const int c = blockIdx.x * 256 + threadIdx.x;
   if (c >= d) return;
   const int r0 = blockIdx.y * LN_COL_ROWS, r1 = min(rows, r0 + LN_COL_ROWS);
-  float dg = 0.f, db = 0.f;
+  float dg = 0.f, db = 0.f, sr_ = 0.f, sd = 0.f;
 #pragma unroll 4
   for (int r = r0; r < r1; ++r) {
     const float2 sr = stats[r];
     const float go = dout[(int64_t)r * d + c];
     dg += go * ((x[(int64_t)r * d + c] - sr.x) * sr.y);
     db += go;
+    if (extra) {
+      if (resid) sr_ += resid[(int64_t)r * d + c];
+      sd += dx[(int64_t)r * d + c];
+    }
   }
-  partial[(int64_t)blockIdx.y * 2 * d + c] = dg;
-  partial[(int64_t)blockIdx.y * 2 * d + d + c] = db;
+  const int np = extra ? 4 : 2;
+  partial[(int64_t)blockIdx.y * np * d + c] = dg;
+  partial[(int64_t)blockIdx.y * np * d + d + c] = db;
+  if (extra) {
+    partial[(int64_t)blockIdx.y * np * d + 2 * d + c] = sr_;
+    partial[(int64_t)blockIdx.y * np * d + 3 * d + c] = sd;
+  }
 }
 
 int ln_bwd(const float* dout, const float* x, const float2* stats, const void* gamma, DT pdt, const float* resid,
-           float* dx, void* dx_e, DT edt, float* partial, int rows, int d, cudaStream_t st) {
+           float* dx, void* dx_e, DT edt, float* partial, int rows, int d, cudaStream_t st, bool extra) {
   if (rows <= 0) return 0;
   if (lnf_ok(d)) {
     const int grid = lnf_grid(rows);
-#define LFU(C) note_launch(), ln_bwd_fused<C><<<grid, 256, 0, st>>>(dout, x, stats, gamma, pdt, resid, dx, dx_e, edt, partial, rows, d)
-    if (d == 1024) LFU(4);
-    else LFU(8);
+#define LFU(C, X) note_launch(), ln_bwd_fused<C, X><<<grid, 256, 0, st>>>(dout, x, stats, gamma, pdt, resid, dx, dx_e, edt, partial, rows, d)
+    if (d == 1024) { if (extra) LFU(4, true); else LFU(4, false); }
+    else { if (extra) LFU(8, true); else LFU(8, false); }
 #undef LFU
     return grid;
   }
@@ -360,7 +388,7 @@ int ln_bwd(const float* dout, const float* x, const float2* stats, const void* g
   }
   const int nblk = ln_bwd_blocks(rows, d);
   dim3 grid((d + 255) / 256, nblk);
-  note_launch(), ln_col_partial<<<grid, 256, 0, st>>>(dout, x, stats, partial, rows, d);
+  note_launch(), ln_col_partial<<<grid, 256, 0, st>>>(dout, x, stats, resid, dx, extra, partial, rows, d);
   return nblk;
 }
 

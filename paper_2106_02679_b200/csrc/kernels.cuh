@@ -31,6 +31,9 @@ struct Epi {
   const float* acc_in = nullptr; int64_t ldacc = 0;    // fp32 accumulator added (gradient accumulation)
   void* aux = nullptr; int64_t ldaux = 0; DT aux_dt = DT::F32;
   void* out = nullptr; int64_t ldo = 0; DT out_dt = DT::F32;
+  // EPI_GELU_BWD on the tensor-core path: also the column sums of out (the bias gradient of the GEMM that
+  // produced u, db1 = sum_rows dU) per 32-row strip: colsum[(m / 32) * N + n], ceil(M / 32) rows, fp32
+  float* colsum = nullptr;
 };
 
 struct GemmArgs {
@@ -65,6 +68,9 @@ struct AttnArgs {
   const void* dO = nullptr;   // [nseq*seq][d]
   float* dsum = nullptr;      // [nseq][heads][seq]
   void* dqkv = nullptr;       // [nseq*seq][3d]
+  // backward (tensor-core path): also the column sums of dqkv (the qkv bias gradient) per (sequence, 128-row
+  // tile, 32-row quadrant): colsum[((sq * ceil(seq/128) + tile) * 4 + quadrant) * 3d + col], fp32
+  float* colsum = nullptr;
 };
 void attn_fwd_f32(const AttnArgs& a, cudaStream_t st);
 void attn_bwd_f32(const AttnArgs& a, cudaStream_t st);
@@ -78,11 +84,13 @@ void ln_fwd(const float* x, const void* gamma, const void* beta, DT pdt, void* y
             float2* stats, int rows, int d, float eps, cudaStream_t st);
 // dx = rstd (dxhat - mean(dxhat) - xhat mean(dxhat xhat)) + resid, dxhat = dout * gamma (O5);
 // writes dx (fp32) and optionally dx_e (E copy), and deterministic column partials
-// partial[blk][0][:] = sum dout*xhat, partial[blk][1][:] = sum dout over the block's rows.
+// partial[blk][0][:] = sum dout*xhat, partial[blk][1][:] = sum dout over the block's rows; with `extra` also
+// partial[blk][2][:] = sum resid and partial[blk][3][:] = sum dx (the bias gradients that are column sums of
+// this kernel's input / output), block stride 4 d instead of 2 d.
 // Returns the number of row blocks (partial rows).
 int ln_bwd(const float* dout, const float* x, const float2* stats, const void* gamma, DT pdt,
            const float* resid, float* dx, void* dx_e, DT edt, float* partial, int rows, int d,
-           cudaStream_t st);
+           cudaStream_t st, bool extra = false);
 int ln_bwd_blocks(int rows, int d);
 
 // ------------------------------------------------------------------ column sums (bias grads)

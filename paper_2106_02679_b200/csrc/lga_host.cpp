@@ -354,8 +354,10 @@ static void plan_arena(lga_handle* h) {
   h->dh1 = A.take<float>(T * d);
   h->dsum = A.take<float>((int64_t)c.c * c.b * c.H * c.s);
   const int64_t pcol = (int64_t)colsum_blocks((int)T) * f;
-  const int64_t pln = (int64_t)ln_bwd_blocks((int)T, (int)d) * 2 * d;
-  h->partial_floats = std::max(pcol, pln);
+  const int64_t pln = (int64_t)ln_bwd_blocks((int)T, (int)d) * 4 * d;   // 4 sums per block with `extra`
+  const int64_t pgelu = (T + 31) / 32 * f;                                  // GELU-backward epilogue strips
+  const int64_t pattn = (int64_t)c.c * c.b * ((c.s + 127) / 128) * 4 * 3 * d;   // attention-backward quadrants
+  h->partial_floats = std::max(std::max(pcol, pln), std::max(pgelu, pattn));
   h->partial = A.take<float>(h->partial_floats);
   h->splitk_floats = c.bf16 ? std::min<int64_t>(16LL * 4 * d * d, (int64_t)1 << 25) : 0;
   h->splitk_ws = c.bf16 ? A.take<float>(h->splitk_floats) : nullptr;
@@ -629,11 +631,34 @@ static void wgrad(lga_handle* h, const void* X, int64_t ldx, const void* Dy, int
   gemm(h, g, st);
 }
 
+// bias gradient from the column partials a producing kernel wrote into h->partial (nrows x n, fp32)
+static void bias_from_partials(lga_handle* h, int64_t nrows, int n, const GradDst& dst, cudaStream_t st) {
+  colsum_finish(h->partial, (int)nrows, n, n, dst.acc_in, dst.out, dst.out_dt, st);
+  KCHECK();
+}
+
 static void bias_grad(lga_handle* h, const void* X, DT xdt, int64_t ldx, int n, int T, const GradDst& dst, cudaStream_t st) {
   const int nblk = colsum_partial(X, xdt, ldx, T, n, h->partial, st);
   KCHECK();
   colsum_finish(h->partial, nblk, n, n, dst.acc_in, dst.out, dst.out_dt, st);
   KCHECK();
+}
+
+// Attention backward -> dqkv (h->dO holds dO), and db_qkv = column sums of dqkv: on the tensor-core path the
+// attention kernels emit per-quadrant partials next to their dqkv stores (no separate pass over dqkv)
+static void attn_bwd_and_bias(lga_handle* h, const Ws& w, int T, const GradDst& bq, cudaStream_t st) {
+  const Cfg& c = h->c;
+  AttnArgs a;
+  a.nseq = c.c * c.b; a.seq = c.s; a.heads = c.H; a.dh = c.dh; a.d = c.d; a.causal = c.causal;
+  a.scale = 1.0f / sqrtf((float)c.dh);
+  a.qkv = w.qkv; a.o = w.o; a.lse = w.lse; a.dO = h->dO; a.dsum = h->dsum; a.dqkv = h->dqkv;
+  a.colsum = c.bf16 ? h->partial : nullptr;
+  const int p = prof_begin(h, st);
+  if (c.bf16) CK(attn_bwd_bf16(a, st)); else attn_bwd_f32(a, st);
+  KCHECK();
+  prof_end(h, p, st, FAM_ATTN, 2.0 * attn_flops_fwd(c, a.nseq));
+  if (c.bf16) bias_from_partials(h, (int64_t)a.nseq * ((c.s + 127) / 128) * 4, 3 * c.d, bq, st);
+  else bias_grad(h, h->dqkv, c.E, 3 * c.d, 3 * c.d, T, bq, st);
 }
 
 // Backward of local layer j over one chunk; the layer's intermediates are in the workspace
@@ -660,22 +685,23 @@ static void layer_bwd(lga_handle* h, const Ws& w, const void* W, const float* x_
     dYe = h->dYe;
   }
   auto dst = [&](int64_t off) { return grad_dst(h, chunk_idx, nchunks, jl, off); };
-  // ---- FFN2: y = h1 + g W2 + b2
+  // ---- FFN2: y = h1 + g W2 + b2 (db2 = sum dY comes out of the LN2 backward below, which reads dY)
   wgrad(h, w.g, f, dYe, d, f, d, T, dst(c.o_w2), c.o_w2, st);
-  bias_grad(h, dY, DT::F32, d, d, T, dst(c.o_b2), st);
-  {  // dU = (dY W2^T) * GELU'(u), written over u
+  {  // dU = (dY W2^T) * GELU'(u), written over u; bf16: the epilogue also emits db1 = sum dU per 32-row strip
     GemmArgs g;
     g.M = T; g.N = f; g.K = d;
     g.A = dYe; g.lda = d; g.a_kmajor = true;
     g.B = eoff((void*)W, E, c.o_w2); g.ldb = d; g.b_kmajor = true;
     g.epi.kind = EPI_GELU_BWD; g.epi.aux = w.u; g.epi.ldaux = f; g.epi.aux_dt = E;
     g.epi.out = w.u; g.epi.ldo = f; g.epi.out_dt = E;
+    g.epi.colsum = c.bf16 ? h->partial : nullptr;
     gemm(h, g, st);
   }
   void* dU = w.u;
+  if (c.bf16) bias_from_partials(h, (T + 31) / 32, f, dst(c.o_b1), st);
+  else bias_grad(h, dU, E, f, f, T, dst(c.o_b1), st);
   // ---- FFN1: u = c W1 + b1
   wgrad(h, w.cn, d, dU, f, d, f, T, dst(c.o_w1), c.o_w1, st);
-  bias_grad(h, dU, E, f, f, T, dst(c.o_b1), st);
   {  // dC = dU W1^T
     GemmArgs g;
     g.M = T; g.N = d; g.K = f;
@@ -684,20 +710,22 @@ static void layer_bwd(lga_handle* h, const Ws& w, const void* W, const float* x_
     g.epi.out = h->dC; g.epi.ldo = d; g.epi.out_dt = DT::F32;
     gemm(h, g, st);
   }
-  // ---- LN2 backward + residual: dh1 = dY + LN2'(dC)
+  // ---- LN2 backward + residual: dh1 = dY + LN2'(dC); its column partials also give db2 = sum dY (its
+  // residual input) and db_o = sum dh1 (its output): no separate pass over dY / dh1
   {
     const int nblk = ln_bwd(h->dC, w.h1, w.st2, eoff((void*)W, E, c.o_ln2w), E, dY, h->dh1, c.bf16 ? h->dh1e : nullptr, E,
-                            h->partial, T, d, st);
+                            h->partial, T, d, st, /*extra=*/true);
     KCHECK();
-    GradDst gw = dst(c.o_ln2w), gbias = dst(c.o_ln2b);
-    colsum_finish(h->partial, nblk, 2LL * d, d, gw.acc_in, gw.out, gw.out_dt, st);
-    colsum_finish(h->partial + d, nblk, 2LL * d, d, gbias.acc_in, gbias.out, gbias.out_dt, st);
+    const int64_t o4[4] = {c.o_ln2w, c.o_ln2b, c.o_b2, c.o_bo};
+    for (int k = 0; k < 4; ++k) {
+      GradDst gd = dst(o4[k]);
+      colsum_finish(h->partial + k * d, nblk, 4LL * d, d, gd.acc_in, gd.out, gd.out_dt, st);
+    }
     KCHECK();
   }
   const void* dh1e = c.bf16 ? (const void*)h->dh1e : (const void*)h->dh1;
   // ---- O projection: h1 = x + o Wo + bo
   wgrad(h, w.o, d, dh1e, d, d, d, T, dst(c.o_wo), c.o_wo, st);
-  bias_grad(h, h->dh1, DT::F32, d, d, T, dst(c.o_bo), st);
   {  // dO = dh1 Wo^T
     GemmArgs g;
     g.M = T; g.N = d; g.K = d;
@@ -706,19 +734,9 @@ static void layer_bwd(lga_handle* h, const Ws& w, const void* W, const float* x_
     g.epi.out = h->dO; g.epi.ldo = d; g.epi.out_dt = E;
     gemm(h, g, st);
   }
-  {  // attention backward -> dqkv
-    AttnArgs a;
-    a.nseq = c.c * c.b; a.seq = c.s; a.heads = c.H; a.dh = c.dh; a.d = d; a.causal = c.causal;
-    a.scale = 1.0f / sqrtf((float)c.dh);
-    a.qkv = w.qkv; a.o = w.o; a.lse = w.lse; a.dO = h->dO; a.dsum = h->dsum; a.dqkv = h->dqkv;
-    const int p = prof_begin(h, st);
-    if (c.bf16) CK(attn_bwd_bf16(a, st)); else attn_bwd_f32(a, st);
-    KCHECK();
-    prof_end(h, p, st, FAM_ATTN, 2.0 * attn_flops_fwd(c, a.nseq));
-  }
+  attn_bwd_and_bias(h, w, T, dst(c.o_bqkv), st);
   // ---- QKV: qkv = a Wqkv + bqkv
   wgrad(h, w.a, d, h->dqkv, 3 * d, d, 3 * d, T, dst(c.o_wqkv), c.o_wqkv, st);
-  bias_grad(h, h->dqkv, E, 3 * d, 3 * d, T, dst(c.o_bqkv), st);
   {  // dA = dqkv Wqkv^T  (into dC, free now)
     GemmArgs g;
     g.M = T; g.N = d; g.K = 3 * d;
@@ -749,35 +767,40 @@ static void layer_bwd_post(lga_handle* h, const Ws& w, const void* W, const floa
   const int d = c.d, f = c.f;
   const DT E = c.E;
   auto dst = [&](int64_t off) { return grad_dst(h, chunk_idx, nchunks, jl, off); };
-  auto ln_back = [&](const float* dout, const float* xin, const float2* stats, int64_t ow, int64_t ob) {
-    // -> h->dh1 (fp32) and, bf16 mode, h->dh1e; gamma / beta gradients from the column partials
+  auto ln_back = [&](const float* dout, const float* xin, const float2* stats, int64_t ow, int64_t ob, int64_t osum) {
+    // -> h->dh1 (fp32) and, bf16 mode, h->dh1e; gamma / beta gradients from the column partials, and the bias
+    // whose gradient is the column sum of this output (osum: db2 = sum ds2, db_o = sum ds1)
     const int nblk = ln_bwd(dout, xin, stats, eoff((void*)W, E, ow), E, nullptr, h->dh1, c.bf16 ? h->dh1e : nullptr, E,
-                            h->partial, T, d, st);
+                            h->partial, T, d, st, /*extra=*/true);
     KCHECK();
-    GradDst gw = dst(ow), gbias = dst(ob);
-    colsum_finish(h->partial, nblk, 2LL * d, d, gw.acc_in, gw.out, gw.out_dt, st);
-    colsum_finish(h->partial + d, nblk, 2LL * d, d, gbias.acc_in, gbias.out, gbias.out_dt, st);
+    const int64_t o4[4] = {ow, ob, -1, osum};
+    for (int k = 0; k < 4; ++k) {
+      if (o4[k] < 0) continue;
+      GradDst gd = dst(o4[k]);
+      colsum_finish(h->partial + k * d, nblk, 4LL * d, d, gd.acc_in, gd.out, gd.out_dt, st);
+    }
     KCHECK();
   };
   const void* dse = c.bf16 ? (const void*)h->dh1e : (const void*)h->dh1;   // ds2, then ds1, as GEMM operand
   // ---- LN2: y = LN2(s2)
-  ln_back(dY, w.s2, w.st2, c.o_ln2w, c.o_ln2b);
+  ln_back(dY, w.s2, w.st2, c.o_ln2w, c.o_ln2b, c.o_b2);
   // ---- FFN2: s2 = h1 + g W2 + b2
   wgrad(h, w.g, f, dse, d, f, d, T, dst(c.o_w2), c.o_w2, st);
-  bias_grad(h, h->dh1, DT::F32, d, d, T, dst(c.o_b2), st);
-  {  // dU = (ds2 W2^T) * GELU'(u), written over u
+  {  // dU = (ds2 W2^T) * GELU'(u), written over u (bf16: + the db1 strip partials)
     GemmArgs g;
     g.M = T; g.N = f; g.K = d;
     g.A = dse; g.lda = d; g.a_kmajor = true;
     g.B = eoff((void*)W, E, c.o_w2); g.ldb = d; g.b_kmajor = true;
     g.epi.kind = EPI_GELU_BWD; g.epi.aux = w.u; g.epi.ldaux = f; g.epi.aux_dt = E;
     g.epi.out = w.u; g.epi.ldo = f; g.epi.out_dt = E;
+    g.epi.colsum = c.bf16 ? h->partial : nullptr;
     gemm(h, g, st);
   }
   void* dU = w.u;
+  if (c.bf16) bias_from_partials(h, (T + 31) / 32, f, dst(c.o_b1), st);
+  else bias_grad(h, dU, E, f, f, T, dst(c.o_b1), st);
   // ---- FFN1: u = h1 W1 + b1
   wgrad(h, w.cn, d, dU, f, d, f, T, dst(c.o_w1), c.o_w1, st);
-  bias_grad(h, dU, E, f, f, T, dst(c.o_b1), st);
   {  // dh1 = dU W1^T + ds2
     GemmArgs g;
     g.M = T; g.N = d; g.K = f;
@@ -788,10 +811,9 @@ static void layer_bwd_post(lga_handle* h, const Ws& w, const void* W, const floa
     gemm(h, g, st);
   }
   // ---- LN1: h1 = LN1(s1)
-  ln_back(h->dC, w.h1, w.st1, c.o_ln1w, c.o_ln1b);
+  ln_back(h->dC, w.h1, w.st1, c.o_ln1w, c.o_ln1b, c.o_bo);
   // ---- O projection: s1 = x + o Wo + bo
   wgrad(h, w.o, d, dse, d, d, d, T, dst(c.o_wo), c.o_wo, st);
-  bias_grad(h, h->dh1, DT::F32, d, d, T, dst(c.o_bo), st);
   {  // dO = ds1 Wo^T
     GemmArgs g;
     g.M = T; g.N = d; g.K = d;
@@ -800,19 +822,9 @@ static void layer_bwd_post(lga_handle* h, const Ws& w, const void* W, const floa
     g.epi.out = h->dO; g.epi.ldo = d; g.epi.out_dt = E;
     gemm(h, g, st);
   }
-  {  // attention backward -> dqkv
-    AttnArgs a;
-    a.nseq = c.c * c.b; a.seq = c.s; a.heads = c.H; a.dh = c.dh; a.d = d; a.causal = c.causal;
-    a.scale = 1.0f / sqrtf((float)c.dh);
-    a.qkv = w.qkv; a.o = w.o; a.lse = w.lse; a.dO = h->dO; a.dsum = h->dsum; a.dqkv = h->dqkv;
-    const int p = prof_begin(h, st);
-    if (c.bf16) CK(attn_bwd_bf16(a, st)); else attn_bwd_f32(a, st);
-    KCHECK();
-    prof_end(h, p, st, FAM_ATTN, 2.0 * attn_flops_fwd(c, a.nseq));
-  }
+  attn_bwd_and_bias(h, w, T, dst(c.o_bqkv), st);
   // ---- QKV: qkv = x Wqkv + bqkv
   wgrad(h, w.a, d, h->dqkv, 3 * d, d, 3 * d, T, dst(c.o_wqkv), c.o_wqkv, st);
-  bias_grad(h, h->dqkv, E, 3 * d, 3 * d, T, dst(c.o_bqkv), st);
   {  // dX = dqkv Wqkv^T + ds1
     GemmArgs g;
     g.M = T; g.N = d; g.K = 3 * d;

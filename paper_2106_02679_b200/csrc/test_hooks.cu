@@ -9,7 +9,7 @@ using namespace lga;
 extern "C" int lgatest_gemm(int path, int M, int N, int K, const void* A, int64_t lda, int a_kmajor, const void* B,
                             int64_t ldb, int b_kmajor, int kind, const void* bias, int bias_dt, const float* res,
                             const float* acc_in, void* aux, int aux_dt, void* out, int64_t ldo, int out_dt,
-                            uintptr_t stream) {
+                            float* colsum, uintptr_t stream) {
   GemmArgs g;
   g.M = M; g.N = N; g.K = K;
   g.A = A; g.lda = lda; g.a_kmajor = a_kmajor != 0;
@@ -20,6 +20,7 @@ extern "C" int lgatest_gemm(int path, int M, int N, int K, const void* A, int64_
   g.epi.acc_in = acc_in; g.epi.ldacc = ldo;
   g.epi.aux = aux; g.epi.ldaux = ldo; g.epi.aux_dt = (DT)aux_dt;
   g.epi.out = out; g.epi.ldo = ldo; g.epi.out_dt = (DT)out_dt;
+  g.epi.colsum = colsum;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (path == 0) {
     gemm_f32_simt(g, st);
@@ -72,9 +73,10 @@ extern "C" int lgatest_attn_fwd(int path, int nseq, int seq, int heads, int dh, 
 
 extern "C" int lgatest_attn_bwd(int path, int nseq, int seq, int heads, int dh, int causal, const void* qkv,
                                 const void* o, const float* lse, const void* dO, float* dsum, void* dqkv,
-                                uintptr_t stream) {
+                                float* colsum, uintptr_t stream) {
   AttnArgs a = mk(nseq, seq, heads, dh, causal);
   a.qkv = qkv; a.o = (void*)o; a.lse = (float*)lse; a.dO = dO; a.dsum = dsum; a.dqkv = dqkv;
+  a.colsum = colsum;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (path == 0) {
     attn_bwd_f32(a, st);
@@ -98,12 +100,15 @@ extern "C" int64_t lgatest_ln_bwd_partial_floats(int rows, int d) { return (int6
 
 extern "C" int lgatest_ln_bwd(const float* dout, const float* x, const float* stats, const void* gamma, int p_dt,
                               const float* resid, float* dx, void* dx_e, int e_dt, float* dgamma, float* dbeta,
-                              float* partial, int rows, int d, uintptr_t stream) {
+                              float* sum_resid, float* sum_dx, float* partial, int rows, int d, uintptr_t stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool extra = sum_resid || sum_dx;
   const int nblk = ln_bwd(dout, x, reinterpret_cast<const float2*>(stats), gamma, (DT)p_dt, resid, dx, dx_e, (DT)e_dt,
-                          partial, rows, d, st);
-  colsum_finish(partial, nblk, 2LL * d, d, nullptr, dgamma, DT::F32, st);
-  colsum_finish(partial + d, nblk, 2LL * d, d, nullptr, dbeta, DT::F32, st);
+                          partial, rows, d, st, extra);
+  const int64_t ps = (extra ? 4LL : 2LL) * d;
+  float* outs[4] = {dgamma, dbeta, sum_resid, sum_dx};
+  for (int k = 0; k < (extra ? 4 : 2); ++k)
+    if (outs[k]) colsum_finish(partial + k * d, nblk, ps, d, nullptr, outs[k], DT::F32, st);
   return (int)cudaGetLastError();
 }
 

@@ -24,7 +24,7 @@ from paper_2106_02679_b200 import _abi  # noqa: E402
 L = _abi.lib()
 VP, I, I64, F = C.c_void_p, C.c_int, C.c_int64, C.c_float
 L.lgatest_ln_fwd.argtypes = [VP, VP, VP, I, VP, I, VP, I, I, F, VP]
-L.lgatest_ln_bwd.argtypes = [VP, VP, VP, VP, I, VP, VP, VP, I, VP, VP, VP, I, I, VP]
+L.lgatest_ln_bwd.argtypes = [VP, VP, VP, VP, I, VP, VP, VP, I, VP, VP, VP, VP, VP, I, I, VP]
 L.lgatest_ln_bwd_partial_floats.restype = I64
 L.lgatest_ln_bwd_partial_floats.argtypes = [I, I]
 L.lgatest_colsum.argtypes = [VP, I, I64, I, I, VP, VP, I, VP, VP]
@@ -90,8 +90,11 @@ def test_layernorm_fwd(d, bf):
 
 
 @pytest.mark.parametrize("d", WIDTHS)
-@pytest.mark.parametrize("bf,resid", [(False, True), (True, True), (False, False)])
-def test_layernorm_bwd_and_gamma_beta_grads(d, bf, resid):
+@pytest.mark.parametrize("bf,resid,extra", [(False, True, False), (True, True, True), (False, False, True),
+                                            (True, True, False)])
+def test_layernorm_bwd_and_gamma_beta_grads(d, bf, resid, extra):
+    """LayerNorm backward: dx (+ resid), dgamma, dbeta and, with `extra`, the column sums of resid and dx that the
+    step takes as bias gradients (pre-LN LN2: db2 = sum dY, db_o = sum dh1)."""
     rows = 333 if d != 2048 else 1000   # several row groups of the fused kernel, ragged tail
     pdt = torch.bfloat16 if bf else torch.float32
     g, x, gamma, beta = _ln_inputs(rows, d, pdt, 7 * d + 1)
@@ -104,9 +107,11 @@ def test_layernorm_bwd_and_gamma_beta_grads(d, bf, resid):
     dxe = torch.empty(rows, d, device="cuda", dtype=pdt)
     dgam = torch.full((d,), float("nan"), device="cuda")
     dbet = torch.full((d,), float("nan"), device="cuda")
-    part = torch.empty(int(L.lgatest_ln_bwd_partial_floats(rows, d)), device="cuda")
+    sres = torch.full((d,), float("nan"), device="cuda") if extra else None
+    sdx = torch.full((d,), float("nan"), device="cuda") if extra else None
+    part = torch.empty(2 * int(L.lgatest_ln_bwd_partial_floats(rows, d)), device="cuda")
     assert L.lgatest_ln_bwd(P(dout), P(x), P(stats), P(gamma), DT(gamma), P(res), P(dx), P(dxe), DT(dxe), P(dgam),
-                            P(dbet), P(part), rows, d, S()) == 0
+                            P(dbet), P(sres), P(sdx), P(part), rows, d, S()) == 0
     torch.cuda.synchronize()
     _, cache = om.layernorm_fwd(f64(x), f64(gamma), f64(beta), 1e-5)
     rdx, rdg, rdb = om.layernorm_bwd(f64(dout), f64(gamma), cache)
@@ -117,6 +122,9 @@ def test_layernorm_bwd_and_gamma_beta_grads(d, bf, resid):
     # column sums over `rows` terms: fp32 accumulation error grows like sqrt(rows) ulps
     close(f64(dgam), rdg, rtol=2e-5)
     close(f64(dbet), rdb, rtol=2e-5)
+    if extra:
+        close(f64(sres), f64(res).sum(0) if resid else np.zeros(d), rtol=2e-5, scale=1.0 if not resid else None)
+        close(f64(sdx), rdx.sum(0), rtol=2e-5)
 
 
 @pytest.mark.parametrize("n,ldx", [(64, 64), (768, 2304), (3 * 1024, 3 * 1024), (8192, 8192), (100, 132)])

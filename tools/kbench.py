@@ -19,11 +19,11 @@ L = _abi.lib()
 L.lgatest_gemm.restype = C.c_int
 L.lgatest_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64,
                            C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
-                           C.c_void_p, C.c_int64, C.c_int, C.c_void_p]
+                           C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]
 L.lgatest_attn_fwd.restype = C.c_int
 L.lgatest_attn_fwd.argtypes = [C.c_int] * 6 + [C.c_void_p] * 3 + [C.c_void_p]
 L.lgatest_attn_bwd.restype = C.c_int
-L.lgatest_attn_bwd.argtypes = [C.c_int] * 6 + [C.c_void_p] * 6 + [C.c_void_p]
+L.lgatest_attn_bwd.argtypes = [C.c_int] * 6 + [C.c_void_p] * 7 + [C.c_void_p]
 
 
 def P(t):
@@ -58,7 +58,7 @@ def attn(args):
         ms = timeit(lambda: L.lgatest_attn_fwd(path, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), st))
         print(f"attn {name:14s} nseq={nseq} s={s} H={H} dh={dh}: {ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s")
     L.lgatest_attn_fwd(1, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), st)
-    ms = timeit(lambda: L.lgatest_attn_bwd(1, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), P(dO), P(dsum), P(dqkv), st))
+    ms = timeit(lambda: L.lgatest_attn_bwd(1, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), P(dO), P(dsum), P(dqkv), None, st))
     print(f"attn {'bwd':14s} nseq={nseq} s={s} H={H} dh={dh}: {ms:.3f} ms  {2 * flops / ms / 1e9:.1f} TFLOP/s (algorithmic 2x fwd)")
 
 
@@ -88,7 +88,7 @@ def gemm(args):
         ek = 1 if kind == "gelu" else (2 if kind == "gelu_bwd" else 0)
         dt = lambda t: 0 if t is None or t.dtype == torch.float32 else 1
         fn = lambda: L.lgatest_gemm(1, M, N, K, P(A), A.shape[1], int(ak), P(B), B.shape[1], int(bk), ek, P(bias), dt(bias),
-                                    P(res), P(acc), P(aux), dt(aux), P(out), N, dt(out), st)
+                                    P(res), P(acc), P(aux), dt(aux), P(out), N, dt(out), None, st)
         assert fn() == 0
         ms = timeit(fn)
         print(f"gemm {name} M={M} N={N} K={K} {kind:12s}: {ms:.3f} ms  {2.0 * M * N * K / ms / 1e9:.1f} TFLOP/s")
