@@ -1,24 +1,33 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) by kernel: share, launches, ns.
 
-    python tools/launch_summary.py gpurun_out/launches_r1_final.csv [header lines...]
+    python tools/launch_summary.py gpurun_out/launches_r1_final.csv [--last N] [header lines...]
+
+--last N: only the last N launches of the list (one step: bench.py prints gpu_launches_per_step).
 """
 import csv
 import re
 import sys
 from collections import defaultdict
 
+args = sys.argv[2:]
+last = None
+if args[:1] == ["--last"]:
+    last, args = int(args[1]), args[2:]
 rows = list(csv.reader(l for l in open(sys.argv[1]) if not l.startswith("==")))
 hdr = rows[0]
 ik, iv, im = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
+iid = hdr.index("ID")
+ids = sorted({int(r[iid]) for r in rows[1:] if len(r) > iv})
+keep = set(ids[-last:]) if last else set(ids)
 tot, cnt = defaultdict(float), defaultdict(int)
 for r in rows[1:]:
-    if len(r) <= iv or r[im] != "gpu__time_duration.sum":
+    if len(r) <= iv or r[im] != "gpu__time_duration.sum" or int(r[iid]) not in keep:
         continue
     name = re.sub(r"\(.*", "", r[ik]).replace("lga::", "")
     tot[name] += float(r[iv].replace(",", ""))
     cnt[name] += 1
 s = sum(tot.values())
-for line in sys.argv[2:]:
+for line in args:
     print("#", line)
 print(f"# {sum(cnt.values())} launches; unit ns\n")
 print(f"  share launches         sum_ns  kernel")
