@@ -73,6 +73,13 @@ int lgatest_adamw_rs(const void* const* gbase, int64_t goff, int D, int g_dt, fl
 int lgatest_peer_reduce(const void* const* gbase, int64_t goff, int D, int g_dt, float* acc, int first, void* out,
                         int64_t n, uintptr_t stream);
 
+/* Guard-mode arena check (lga_init with env LGA_ARENA_GUARD=1: a 4 KB canary after every arena buffer):
+ * the number of canary bytes overwritten so far (an out-of-bounds write past a buffer's end), after
+ * synchronising the handle's streams; -1 if the handle is not in guard mode.  `h` is an lga_handle*. */
+int64_t lgatest_arena_guard_check(void* h);
+/* Negative control: overwrite one byte of the last canary (returns a cudaError_t, -1 if not in guard mode). */
+int lgatest_arena_guard_poke(void* h);
+
 #ifdef __cplusplus
 }
 #endif

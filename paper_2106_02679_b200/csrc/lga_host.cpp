@@ -147,15 +147,26 @@ static lga_status validate(const lga_config* c, int world, Cfg* out) {
 }
 
 // ------------------------------------------------------------------ arena (one allocation, M10 / P:96)
+// Guard mode (env LGA_ARENA_GUARD=1; compute-sanitizer is unavailable on the GPU pool): every buffer is
+// followed by a GUARD-byte canary filled with a pattern at init; lgatest_arena_guard_check counts the
+// canary bytes a kernel overwrote -- an out-of-bounds write past the end of any arena buffer.
+constexpr size_t GUARD = 4096;
+constexpr unsigned char GUARD_BYTE = 0xA5;
 struct Arena {
   char* base = nullptr;
   size_t cap = 0, used = 0;
   bool planning = true;
+  bool guard = false;
+  std::vector<size_t> guards;   // offsets of the canaries (guard mode)
   template <typename T>
   T* take(size_t count) {
     size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
     T* p = planning ? nullptr : reinterpret_cast<T*>(base + used);
     used += bytes;
+    if (guard) {
+      if (!planning) guards.push_back(used);
+      used += GUARD;
+    }
     return p;
   }
   void* take_bytes(size_t bytes) { return take<char>(bytes); }
@@ -1493,6 +1504,10 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
   CK(cudaEventCreate(&h->ev_t1));
   CK(cudaEventCreate(&h->ev_fwd_end));
   // arena: plan, allocate once, carve
+  {
+    const char* gv = getenv("LGA_ARENA_GUARD");
+    h->arena.guard = gv && gv[0] == '1';
+  }
   h->arena.planning = true;
   plan_arena(h);
   const size_t need = h->arena.used + 4096;
@@ -1504,8 +1519,10 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
   }
   h->arena.cap = need;
   h->arena.planning = false;
+  h->arena.guards.clear();
   plan_arena(h);
   CK(cudaMemsetAsync(h->arena.base, 0, need, h->s_comp));
+  for (size_t g : h->arena.guards) CK(cudaMemsetAsync(h->arena.base + g, GUARD_BYTE, GUARD, h->s_comp));
   CK(cudaMallocHost(&h->loss_host, 8 * sizeof(double)));
   // NCCL only for the baseline (LGA_FLAG_NCCL_DP) or, without an allgather callback, for the bootstrap exchange
   if (world > 1 && nccl_id) {
@@ -1917,5 +1934,28 @@ lga_status lga_timing_last(lga_handle* h, lga_timing* out) {
 }
 
 void lga_destroy(lga_handle* h) { free_handle(h); }
+
+// negative control of the guard check: overwrite one byte of the last canary (as a kernel writing one byte past
+// the end of the last arena buffer would)
+int lgatest_arena_guard_poke(lga_handle* h) {
+  if (!h || !h->arena.guard || h->arena.guards.empty()) return -1;
+  return (int)cudaMemset(h->arena.base + h->arena.guards.back(), 0, 1);
+}
+
+// test hook (include/lga_testing.h): canary bytes overwritten in the guard-mode arena; -1 = not in guard mode
+int64_t lgatest_arena_guard_check(lga_handle* h) {
+  if (!h || !h->arena.guard) return -1;
+  cudaSetDevice(h->dev);
+  if (h->stepped) cudaEventSynchronize(h->ev_t1);
+  cudaStreamSynchronize(h->s_comp);
+  cudaStreamSynchronize(h->s_comm);
+  std::vector<unsigned char> buf(GUARD);
+  int64_t bad = 0;
+  for (size_t g : h->arena.guards) {
+    if (cudaMemcpy(buf.data(), h->arena.base + g, GUARD, cudaMemcpyDeviceToHost) != cudaSuccess) return -2;
+    for (unsigned char b : buf) bad += b != GUARD_BYTE;
+  }
+  return bad;
+}
 
 }  // extern "C"

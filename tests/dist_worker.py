@@ -46,7 +46,15 @@ def main():
         t = torch.from_numpy(T[r]).cuda()
         losses.append(tr.step(x, t))
     last, tot = tr.comm_stats()
+    guard = -1
+    if os.environ.get("LGA_ARENA_GUARD") == "1":
+        import ctypes as C
+        from paper_2106_02679_b200 import _abi
+        f = _abi.lib().lgatest_arena_guard_check
+        f.restype, f.argtypes = C.c_int64, [C.c_void_p]
+        guard = int(f(tr._h))
     out = dict(grads=tr.grads(), params=tr.params(), losses=np.array(losses), stage=tr.stage, replica=tr.replica,
+               guard=guard,
                stages=np.array(tr.layer_stage()), timing=json.dumps(tr.timing()), last=json.dumps(last),
                total=json.dumps(tot))
     np.savez(os.path.join(a.out, f"rank{rank}.npz"), **out)
