@@ -157,6 +157,15 @@ struct DkvSmem {
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
+// Persistent: one CTA per SM loops over work items (key tile, head, sequence) in chunks of DKV_G (sequence,
+// head) pairs -- the Q / dO tiles of a chunk stay in L2 -- with the heaviest key tiles (most queries after
+// them under the causal mask) first.  Everything per item is pipelined across items: the Q / dO ring,
+// the S^T / dP^T TMEM buffers and the element-wise groups run on GLOBAL iteration counters; the next item's
+// K / V tiles are loaded as soon as the current item's last S^T / dP^T MMAs have read them (kv_empty), and
+// its first S^T / dP^T MMAs run while the element-wise warps drain the previous item's dK / dV from TMEM;
+// only its first dV / dK MMAs wait for that drain (acc_free).
+constexpr int DKV_G = 8;
+
 template <int DH>
 __global__ void __launch_bounds__(NT, 1)
     dkdv_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
@@ -166,32 +175,43 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps shared provenance
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
   constexpr int NST = SM::NST;
+  constexpr int EW_ALL = EW_WARPS * 32;
   uint64_t* kv_full = bars + 0;
   uint64_t* q_full = bars + 1;              // [NST] (expect_tx + 32 cp.async arrivals)
   uint64_t* q_empty = q_full + NST;         // [NST]
   uint64_t* s_full = q_empty + NST;         // [2] per group / TMEM buffer
   uint64_t* p_full = s_full + 2;            // [2] (GRP_THREADS arrivals)
   uint64_t* g_done = p_full + 2;            // [2]
-  constexpr int NBAR = 2 * NST + 7;
+  uint64_t* kv_empty = g_done + 2;          // K / V read by the item's last S^T / dP^T MMAs
+  uint64_t* acc_free = kv_empty + 1;        // dK / dV drained from TMEM by every element-wise thread
+  constexpr int NBAR = 2 * NST + 9;
   static_assert(NBAR * 8 + 4 <= 256, "barrier area");
   static_assert(SM::TOTAL <= 232448, "shared memory");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kt = blockIdx.x, h = blockIdx.y, sq = blockIdx.z;
   const int s = a.seq, d = a.d;
-  const int k0 = kt * KB;
+  const int nkt = (s + KB - 1) / KB;
   const int nq_all = (s + QB - 1) / QB;
-  const int qstart = a.causal ? k0 / QB : 0;
-  const int nq = nq_all - qstart;
-  const int rb = (sq * a.heads + h) * s;   // row base of lse / dsum
+  const int pairs = a.heads * a.nseq;
+  const int n_items = nkt * pairs;
+  // work item t -> key tile, head, sequence; its query iterations start at qstart (causal: the diagonal)
+  auto item = [&](int t, int& kt, int& h, int& sq, int& qstart, int& nq) {
+    const int chunk = t / (DKV_G * nkt), w = t % (DKV_G * nkt);
+    const int np = min(DKV_G, pairs - chunk * DKV_G);
+    kt = w / np;   // ascending: heaviest first under causal masking
+    const int pair = chunk * DKV_G + w % np;
+    h = pair % a.heads;
+    sq = pair / a.heads;
+    qstart = a.causal ? kt * KB / QB : 0;
+    nq = nq_all - qstart;
+  };
 
   if (warp == 0 && lane == 0) {
-    BTR(39, 0);
     for (int i = 0; i < NBAR; ++i) {
       const bool qf = (&bars[i] >= q_full && &bars[i] < q_empty);
       const bool ew = (&bars[i] >= p_full && &bars[i] < g_done);
-      mbar_init(&bars[i], qf ? 33 : ew ? GRP_THREADS : 1);
+      mbar_init(&bars[i], qf ? 33 : ew ? GRP_THREADS : (&bars[i] == acc_free ? EW_ALL : 1));
     }
     mbar_fence_init();
     prefetch_tmap(&tm_kv);
@@ -208,34 +228,42 @@ __global__ void __launch_bounds__(NT, 1)
   const uint32_t t_dv = tb + 256, t_dk = tb + 256 + DH;
 
   if (warp == 0) {  // ===== producer: TMA (lane 0) + lse / dsum cp.async (all lanes)
-    if (lane == 0) {
-      mbar_expect_tx(kv_full, 2 * SM::KT);
-#pragma unroll
-      for (int i = 0; i < DH / 64; ++i) {
-        tma_load_3d(smem + SM::K_OFF + i * SM::SUB128, &tm_kv, kv_full, d + h * DH + 64 * i, k0, sq);
-        tma_load_3d(smem + SM::V_OFF + i * SM::SUB128, &tm_kv, kv_full, 2 * d + h * DH + 64 * i, k0, sq);
-      }
-    }
-    for (int i = 0; i < nq; ++i) {
-      const int st = i % NST;
-      const int q0 = (qstart + i) * QB;
-      mbar_wait(&q_empty[st], ((i / NST) & 1) ^ 1);
+    int gi = 0, it = 0;
+    for (int t = blockIdx.x; t < n_items; t += gridDim.x, ++it) {
+      int kt, h, sq, qstart, nq;
+      item(t, kt, h, sq, qstart, nq);
+      const int k0 = kt * KB;
+      const int rb = (sq * a.heads + h) * s;   // row base of lse / dsum
       if (lane == 0) {
-        mbar_expect_tx(&q_full[st], 2 * SM::QT);
+        mbar_wait(kv_empty, (it & 1) ^ 1);   // the previous item's S^T / dP^T MMAs have read K / V
+        mbar_expect_tx(kv_full, 2 * SM::KT);
 #pragma unroll
-        for (int c = 0; c < DH / 64; ++c) {
-          tma_load_3d(smem + SM::Q_OFF + st * SM::QT + c * SM::SUB64, &tm_q, &q_full[st], h * DH + 64 * c, q0, sq);
-          tma_load_3d(smem + SM::G_OFF + st * SM::QT + c * SM::SUB64, &tm_g, &q_full[st], h * DH + 64 * c, q0, sq);
+        for (int i = 0; i < DH / 64; ++i) {
+          tma_load_3d(smem + SM::K_OFF + i * SM::SUB128, &tm_kv, kv_full, d + h * DH + 64 * i, k0, sq);
+          tma_load_3d(smem + SM::V_OFF + i * SM::SUB128, &tm_kv, kv_full, 2 * d + h * DH + 64 * i, k0, sq);
         }
       }
-      // lse / dsum of the 64 queries (zero past the sequence end; those queries are masked)
-      float* ld = reinterpret_cast<float*>(smem + SM::LD_OFF + st * 512);
+      for (int i = 0; i < nq; ++i, ++gi) {
+        const int st = gi % NST;
+        const int q0 = (qstart + i) * QB;
+        mbar_wait(&q_empty[st], ((gi / NST) & 1) ^ 1);
+        if (lane == 0) {
+          mbar_expect_tx(&q_full[st], 2 * SM::QT);
 #pragma unroll
-      for (int e = lane; e < 128; e += 32) {
-        const int q = q0 + (e & 63);
-        cp_async4(ld + e, (e < 64 ? a.lse : a.dsum) + rb + min(q, s - 1), q < s);
+          for (int c = 0; c < DH / 64; ++c) {
+            tma_load_3d(smem + SM::Q_OFF + st * SM::QT + c * SM::SUB64, &tm_q, &q_full[st], h * DH + 64 * c, q0, sq);
+            tma_load_3d(smem + SM::G_OFF + st * SM::QT + c * SM::SUB64, &tm_g, &q_full[st], h * DH + 64 * c, q0, sq);
+          }
+        }
+        // lse / dsum of the 64 queries (zero past the sequence end; those queries are masked)
+        float* ld = reinterpret_cast<float*>(smem + SM::LD_OFF + st * 512);
+#pragma unroll
+        for (int e = lane; e < 128; e += 32) {
+          const int q = q0 + (e & 63);
+          cp_async4(ld + e, (e < 64 ? a.lse : a.dsum) + rb + min(q, s - 1), q < s);
+        }
+        cp_async_mbar_arrive(&q_full[st]);
       }
-      cp_async_mbar_arrive(&q_full[st]);
     }
   } else if (warp == 1) {  // ===== MMA issuer (whole warp; one elected lane issues)
     constexpr uint32_t idesc_s = make_idesc(128, QB, false, false);
@@ -247,133 +275,133 @@ __global__ void __launch_bounds__(NT, 1)
     const uint64_t dGk = make_desc(smem_u32(smem + SM::G_OFF), 16, 1024);          // dO, K-major
     const uint64_t dQm = make_desc(smem_u32(smem + SM::Q_OFF), SM::SUB64, 1024);   // Q, MN-major
     const uint64_t dGm = make_desc(smem_u32(smem + SM::G_OFF), SM::SUB64, 1024);   // dO, MN-major
-    auto issue_s = [&](int i) {   // S^T(i) = K Q^T, dP^T(i) = V dO^T into buffer i & 1
-      const int st = i % NST, b = i & 1;
-      mbar_wait(&q_full[st], (i / NST) & 1);
-      BTR(i, 3);
-      fence_after();
-      const uint64_t dq = desc_add(dQk, st * SM::QT), dg = desc_add(dGk, st * SM::QT);
-      if (leader) {
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t oa = (kk >> 2) * SM::SUB128 + (kk & 3) * 32, ob = (kk >> 2) * SM::SUB64 + (kk & 3) * 32;
-          umma_f16(t_st(b), desc_add(dK, oa), desc_add(dq, ob), idesc_s, kk > 0);
-          umma_f16(t_dpt(b), desc_add(dV, oa), desc_add(dg, ob), idesc_s, kk > 0);
-        }
-        umma_commit(&s_full[b]);
-      }
-      __syncwarp();
-    };
-    mbar_wait(kv_full, 0);
-    BTR(39, 1);
-    issue_s(0);
-    if (nq > 1) issue_s(1);
-    for (int i = 0; i < nq; ++i) {  // dV += P^T dO, dK += dS^T Q (A from TMEM), then S^T(i+2)
-      const int st = i % NST, b = i & 1;
-      mbar_wait(&p_full[b], (i >> 1) & 1);
-      BTR(i, 0);
-      fence_after();
-      const uint64_t dq = desc_add(dQm, st * SM::QT), dg = desc_add(dGm, st * SM::QT);
-      if (leader) {
-#pragma unroll
-        for (int kk = 0; kk < QB / 16; ++kk) {
-          const uint32_t ta = 32 * (kk >> 1) + 8 * (kk & 1);   // 16 queries: owner half, 8 packed columns
-          const uint32_t ob = kk * 16 * 128;                   // MN-major B: 16 query rows
-          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-          umma_f16_ts(t_dv, t_st(b) + ta, desc_add(dg, ob), idesc_g, acc);
-          umma_f16_ts(t_dk, t_dpt(b) + ta, desc_add(dq, ob), idesc_g, acc);
-        }
-        umma_commit(&g_done[b]);
-        umma_commit(&q_empty[st]);
-      }
-      __syncwarp();
-      if (i + 2 < nq) {
-#ifndef LGA_EXP_NO_GDONE_WAIT
-        mbar_wait(&g_done[b], (i >> 1) & 1);   // P^T / dS^T of iteration i consumed: buffer b free
-#endif
-        BTR(i, 2);
+    int gi = 0, it = 0;
+    for (int t = blockIdx.x; t < n_items; t += gridDim.x, ++it) {
+      int kt, h, sq, qstart, nq;
+      item(t, kt, h, sq, qstart, nq);
+      // S^T(g) = K Q^T, dP^T(g) = V dO^T into buffer g & 1 (global iteration g = local i of this item), once
+      // the gradient MMAs of iteration g - 2 have consumed the P^T / dS^T that buffer held
+      auto issue_s = [&](int g, int i) {
+        const int st = g % NST, b = g & 1;
+        if (g >= 2) mbar_wait(&g_done[b], ((g - 2) >> 1) & 1);
+        mbar_wait(&q_full[st], (g / NST) & 1);
         fence_after();
-        issue_s(i + 2);
+        const uint64_t dq = desc_add(dQk, st * SM::QT), dg = desc_add(dGk, st * SM::QT);
+        if (leader) {
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk) {
+            const uint32_t oa = (kk >> 2) * SM::SUB128 + (kk & 3) * 32, ob = (kk >> 2) * SM::SUB64 + (kk & 3) * 32;
+            umma_f16(t_st(b), desc_add(dK, oa), desc_add(dq, ob), idesc_s, kk > 0);
+            umma_f16(t_dpt(b), desc_add(dV, oa), desc_add(dg, ob), idesc_s, kk > 0);
+          }
+          umma_commit(&s_full[b]);
+          if (i == nq - 1) umma_commit(kv_empty);   // K / V of this item fully read
+        }
+        __syncwarp();
+      };
+      mbar_wait(kv_full, it & 1);
+      issue_s(gi, 0);
+      if (nq > 1) issue_s(gi + 1, 1);
+      for (int i = 0; i < nq; ++i) {  // dV += P^T dO, dK += dS^T Q (A from TMEM), then S^T(i+2)
+        const int g = gi + i, st = g % NST, b = g & 1;
+        if (i == 0 && it > 0) mbar_wait(acc_free, (it - 1) & 1);   // the previous item's dK / dV drained
+        mbar_wait(&p_full[b], (g >> 1) & 1);
+        fence_after();
+        const uint64_t dq = desc_add(dQm, st * SM::QT), dg = desc_add(dGm, st * SM::QT);
+        if (leader) {
+#pragma unroll
+          for (int kk = 0; kk < QB / 16; ++kk) {
+            const uint32_t ta = 32 * (kk >> 1) + 8 * (kk & 1);   // 16 queries: owner half, 8 packed columns
+            const uint32_t ob = kk * 16 * 128;                   // MN-major B: 16 query rows
+            const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+            umma_f16_ts(t_dv, t_st(b) + ta, desc_add(dg, ob), idesc_g, acc);
+            umma_f16_ts(t_dk, t_dpt(b) + ta, desc_add(dq, ob), idesc_g, acc);
+          }
+          umma_commit(&g_done[b]);
+          umma_commit(&q_empty[st]);
+        }
+        __syncwarp();
+        if (i + 2 < nq) issue_s(g + 2, i + 2);
       }
+      gi += nq;
     }
   } else if (warp >= 4) {  // ===== element-wise: ping-pong groups, one key row per 2 threads of a group
     const int grp = (warp - 4) >> 3;
     const int hf = ((warp - 4) >> 2) & 1;       // half (32 columns) of the 64 query columns
     const int qd = warp & 3;
     const int r = qd * 32 + lane;
-    const int kj = k0 + r;
     const uint32_t lrow = (uint32_t)(qd * 32) << 16;
     const float sl2 = a.scale * LOG2E;
-    for (int i = grp; i < nq; i += 2) {
-      const int st = i % NST;
-      const int qa = (qstart + i) * QB + hf * 32;
-      const float* ls = reinterpret_cast<const float*>(smem + SM::LD_OFF + st * 512) + hf * 32;
-      const float* dsm = ls + 64;
-      // valid iff q < s, kj < s and (causal) kj <= q; only tiles touching the diagonal / the end mask
-      const bool need_mask = kj >= s || qa + 32 > s || (a.causal && kj > qa);
-      mbar_wait(&s_full[grp], (i >> 1) & 1);
-      if ((warp & 7) == 4 && lane == 0) BTR(i, 4);
-      fence_after();
-      mbar_wait(&q_full[st], (i / NST) & 1);   // lse / dsum of tile i landed with Q / dO
+    int gi = 0;
+    for (int t = blockIdx.x; t < n_items; t += gridDim.x) {
+      int kt, h, sq, qstart, nq;
+      item(t, kt, h, sq, qstart, nq);
+      const int k0 = kt * KB, kj = k0 + r;
+      for (int i = (grp - gi) & 1; i < nq; i += 2) {   // this group's iterations: global parity == grp
+        const int g = gi + i, st = g % NST;
+        const int qa = (qstart + i) * QB + hf * 32;
+        const float* ls = reinterpret_cast<const float*>(smem + SM::LD_OFF + st * 512) + hf * 32;
+        const float* dsm = ls + 64;
+        // valid iff q < s, kj < s and (causal) kj <= q; only tiles touching the diagonal / the end mask
+        const bool need_mask = kj >= s || qa + 32 > s || (a.causal && kj > qa);
+        mbar_wait(&s_full[grp], (g >> 1) & 1);
+        fence_after();
+        mbar_wait(&q_full[st], (g / NST) & 1);   // lse / dsum of tile g landed with Q / dO
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
-        uint32_t rsv[16], rdp[16];
-#ifdef LGA_EXP_NO_TMEM_LD
+        for (int ch = 0; ch < 2; ++ch) {
+          uint32_t rsv[16], rdp[16];
+          tmem_ld16_nowait(t_st(grp) + lrow + hf * 32 + ch * 16, rsv);
+          tmem_ld16_nowait(t_dpt(grp) + lrow + hf * 32 + ch * 16, rdp);
+          tmem_wait_ld();
+          float sc[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) rsv[c] = __float_as_uint(0.01f * c), rdp[c] = 0;
-#else
-        tmem_ld16_nowait(t_st(grp) + lrow + hf * 32 + ch * 16, rsv);
-        tmem_ld16_nowait(t_dpt(grp) + lrow + hf * 32 + ch * 16, rdp);
-        tmem_wait_ld();
-#endif
-        float sc[16];
+          for (int c = 0; c < 16; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -ls[ch * 16 + c] * LOG2E);
+          if (need_mask) {
 #pragma unroll
-        for (int c = 0; c < 16; ++c) sc[c] = fmaf(__uint_as_float(rsv[c]), sl2, -ls[ch * 16 + c] * LOG2E);
-#ifdef LGA_EXP_EW_FAST
-        if (true) {
+            for (int c = 0; c < 16; ++c) {
+              const int q = qa + ch * 16 + c;
+              if (!(q < s && kj < s && (!a.causal || kj <= q))) sc[c] = -INFINITY;
+            }
+          }
           uint32_t pp[8], pd[8];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) pp[c] = __float_as_uint(sc[2 * c]) ^ rdp[2 * c], pd[c] = rdp[2 * c + 1];
+          for (int c = 0; c < 16; c += 2) {
+            float p[2], gg[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              p[e] = ex2(sc[c + e]);
+              gg[e] = p[e] * (__uint_as_float(rdp[c + e]) - dsm[ch * 16 + c + e]) * a.scale;
+            }
+            pp[c / 2] = pack_bf16x2(p[0], p[1]);
+            pd[c / 2] = pack_bf16x2(gg[0], gg[1]);
+          }
+          // packed columns 32h + 8ch .. +7 lie inside chunk 0's range, already read by this thread
           tmem_st8_nowait(t_st(grp) + lrow + hf * 32 + ch * 8, pp);
           tmem_st8_nowait(t_dpt(grp) + lrow + hf * 32 + ch * 8, pd);
-          continue;
         }
-#endif
-        if (need_mask) {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const int q = qa + ch * 16 + c;
-            if (!(q < s && kj < s && (!a.causal || kj <= q))) sc[c] = -INFINITY;
-          }
-        }
-        uint32_t pp[8], pd[8];
-#pragma unroll
-        for (int c = 0; c < 16; c += 2) {
-          float p[2], g[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            p[e] = ex2(sc[c + e]);
-            g[e] = p[e] * (__uint_as_float(rdp[c + e]) - dsm[ch * 16 + c + e]) * a.scale;
-          }
-          pp[c / 2] = pack_bf16x2(p[0], p[1]);
-          pd[c / 2] = pack_bf16x2(g[0], g[1]);
-        }
-        // packed columns 32h + 8ch .. +7 lie inside chunk 0's range, already read by this thread
-        tmem_st8_nowait(t_st(grp) + lrow + hf * 32 + ch * 8, pp);
-        tmem_st8_nowait(t_dpt(grp) + lrow + hf * 32 + ch * 8, pd);
+        tmem_wait_st();
+        fence_before();
+        mbar_arrive(&p_full[grp]);
       }
-      tmem_wait_st();
-      if ((warp & 7) == 4 && lane == 0) BTR(i, 5);
+      // every gradient MMA of this item done: this group's last one (its own barrier: cannot alias an older
+      // phase), then the item's very last one (the next phase of that barrier needs this thread's acc_free)
+      {
+        const int gl = gi + nq - 1;
+        const int own = gl - ((gl - grp) & 1);   // last global iteration <= gl of this group's parity
+        if (own >= gi) mbar_wait(&g_done[grp], (own >> 1) & 1);
+        if (own != gl) mbar_wait(&g_done[gl & 1], (gl >> 1) & 1);
+        fence_after();
+      }
+      constexpr int OC = DH / 4;   // output columns per (group, half)
+      const int oq = grp * 2 + hf;
+      __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + kj) * 3 * d + h * DH + oq * OC;
+      float* cs = a.colsum ? a.colsum + ((int64_t)(sq * nkt + kt) * 4 + qd) * 3 * d + h * DH + oq * OC : nullptr;
+      store_row_bf16_global(out + d, t_dk + lrow + oq * OC, OC, 1.f, kj < s, cs ? cs + d : nullptr);
+      store_row_bf16_global(out + 2 * d, t_dv + lrow + oq * OC, OC, 1.f, kj < s, cs ? cs + 2 * d : nullptr);
       fence_before();
-      mbar_arrive(&p_full[grp]);
+      mbar_arrive(acc_free);   // dK / dV accumulators free for the next item
+      gi += nq;
     }
-    wait_all_done(g_done, grp, nq);
-    constexpr int OC = DH / 4;   // output columns per (group, half)
-    const int oq = grp * 2 + hf;
-    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + kj) * 3 * d + h * DH + oq * OC;
-    float* cs = a.colsum ? a.colsum + ((int64_t)(sq * gridDim.x + kt) * 4 + qd) * 3 * d + h * DH + oq * OC : nullptr;
-    store_row_bf16_global(out + d, t_dk + lrow + oq * OC, OC, 1.f, kj < s, cs ? cs + d : nullptr);
-    store_row_bf16_global(out + 2 * d, t_dv + lrow + oq * OC, OC, 1.f, kj < s, cs ? cs + 2 * d : nullptr);
   }
   fence_before();
   __syncthreads();
@@ -381,7 +409,6 @@ __global__ void __launch_bounds__(NT, 1)
     fence_after();
     tmem_dealloc(tb, 512);
   }
-  if (threadIdx.x == 0) BTR(39, 2);
 }
 
 // =============================================================================== dQ
@@ -408,6 +435,12 @@ struct DqSmem {
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
+// Persistent like the dK / dV kernel: items (query tile, head, sequence) in chunks of DQ_G (sequence, head)
+// pairs (their K / V tiles stay in L2), heaviest query tiles first; K / V rings, the S / dP buffer and the dS
+// buffers run on global counters; the next item's Q / dO tiles load once the current item's last S / dP MMAs
+// have read them (qg_empty), and only its first dQ MMA waits for the previous dQ drain (acc_free).
+constexpr int DQ_G = 16;
+
 template <int DH>
 __global__ void __launch_bounds__(NT, 1)
     dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_g,
@@ -427,23 +460,32 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* s_empty = s_full + 1;           // ... loaded by every element-wise thread (EW_ALL)
   uint64_t* p_full = s_empty + 1;           // [2] per dS buffer (EW_ALL)
   uint64_t* g_done = p_full + 2;            // [2] per dS buffer: dQ MMAs done
-  constexpr int NBAR = 2 * NK + 2 * NV + 7;
+  uint64_t* qg_empty = g_done + 2;          // Q / dO read by the item's last S / dP MMAs
+  uint64_t* acc_free = qg_empty + 1;        // dQ drained (EW_ALL)
+  constexpr int NBAR = 2 * NK + 2 * NV + 9;
   static_assert(NBAR * 8 + 4 <= 256, "barrier area");
   static_assert(SM::TOTAL <= 232448, "shared memory");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqt = gridDim.x;
-  const int qt = a.causal ? nqt - 1 - (int)blockIdx.x : (int)blockIdx.x;
-  const int h = blockIdx.y, sq = blockIdx.z;
   const int s = a.seq, d = a.d;
-  const int q0 = qt * QB2;
-  const int kend = a.causal ? min(s, q0 + QB2) : s;
-  const int nk = (kend + KB2 - 1) / KB2;
+  const int nqt = (s + QB2 - 1) / QB2;
+  const int pairs = a.heads * a.nseq;
+  const int n_items = nqt * pairs;
+  auto item = [&](int t, int& qt, int& h, int& sq, int& nk) {
+    const int chunk = t / (DQ_G * nqt), w = t % (DQ_G * nqt);
+    const int np = min(DQ_G, pairs - chunk * DQ_G);
+    const int qi = w / np, pair = chunk * DQ_G + w % np;
+    qt = a.causal ? nqt - 1 - qi : qi;   // heaviest (most keys) first under causal masking
+    h = pair % a.heads;
+    sq = pair / a.heads;
+    const int kend = a.causal ? min(s, qt * QB2 + QB2) : s;
+    nk = (kend + KB2 - 1) / KB2;
+  };
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < NBAR; ++i) {
-      const bool ew = (&bars[i] >= s_empty && &bars[i] < g_done);
+      const bool ew = (&bars[i] >= s_empty && &bars[i] < g_done) || &bars[i] == acc_free;
       mbar_init(&bars[i], ew ? EW_ALL : 1);
     }
     mbar_fence_init();
@@ -461,26 +503,32 @@ __global__ void __launch_bounds__(NT, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer
-      mbar_expect_tx(qg_full, 2 * SM::QT);
+      int jg = 0, it = 0;
+      for (int t = blockIdx.x; t < n_items; t += gridDim.x, ++it) {
+        int qt, h, sq, nk;
+        item(t, qt, h, sq, nk);
+        mbar_wait(qg_empty, (it & 1) ^ 1);   // the previous item's last S / dP MMAs read Q / dO
+        mbar_expect_tx(qg_full, 2 * SM::QT);
 #pragma unroll
-      for (int c = 0; c < DH / 64; ++c) {
-        tma_load_3d(smem + SM::Q_OFF + c * SM::SUB128, &tm_q, qg_full, h * DH + 64 * c, q0, sq);
-        tma_load_3d(smem + SM::G_OFF + c * SM::SUB128, &tm_g, qg_full, h * DH + 64 * c, q0, sq);
-      }
-      for (int j = 0; j < nk; ++j) {
-        const int sk = j % NK, sv = j % NV;
-        mbar_wait(&k_empty[sk], ((j / NK) & 1) ^ 1);
-        mbar_expect_tx(&k_full[sk], SM::KT);
+        for (int c = 0; c < DH / 64; ++c) {
+          tma_load_3d(smem + SM::Q_OFF + c * SM::SUB128, &tm_q, qg_full, h * DH + 64 * c, qt * QB2, sq);
+          tma_load_3d(smem + SM::G_OFF + c * SM::SUB128, &tm_g, qg_full, h * DH + 64 * c, qt * QB2, sq);
+        }
+        for (int j = 0; j < nk; ++j, ++jg) {
+          const int sk = jg % NK, sv = jg % NV;
+          mbar_wait(&k_empty[sk], ((jg / NK) & 1) ^ 1);
+          mbar_expect_tx(&k_full[sk], SM::KT);
 #pragma unroll
-        for (int c = 0; c < DH / 64; ++c)
-          tma_load_3d(smem + SM::K_OFF + sk * SM::KT + c * SM::SUB128, &tm_kv, &k_full[sk], d + h * DH + 64 * c,
-                      j * KB2, sq);
-        mbar_wait(&v_empty[sv], ((j / NV) & 1) ^ 1);
-        mbar_expect_tx(&v_full[sv], SM::KT);
+          for (int c = 0; c < DH / 64; ++c)
+            tma_load_3d(smem + SM::K_OFF + sk * SM::KT + c * SM::SUB128, &tm_kv, &k_full[sk], d + h * DH + 64 * c,
+                        j * KB2, sq);
+          mbar_wait(&v_empty[sv], ((jg / NV) & 1) ^ 1);
+          mbar_expect_tx(&v_full[sv], SM::KT);
 #pragma unroll
-        for (int c = 0; c < DH / 64; ++c)
-          tma_load_3d(smem + SM::V_OFF + sv * SM::KT + c * SM::SUB128, &tm_kv, &v_full[sv], 2 * d + h * DH + 64 * c,
-                      j * KB2, sq);
+          for (int c = 0; c < DH / 64; ++c)
+            tma_load_3d(smem + SM::V_OFF + sv * SM::KT + c * SM::SUB128, &tm_kv, &v_full[sv], 2 * d + h * DH + 64 * c,
+                        j * KB2, sq);
+        }
       }
     }
   } else if (warp == 1) {  // ===== MMA issuer (whole warp; one elected lane issues)
@@ -492,112 +540,123 @@ __global__ void __launch_bounds__(NT, 1)
     const uint64_t dK = make_desc(smem_u32(smem + SM::K_OFF), 16, 1024);
     const uint64_t dV = make_desc(smem_u32(smem + SM::V_OFF), 16, 1024);
     const uint64_t dKm = make_desc(smem_u32(smem + SM::K_OFF), SM::SUB128, 1024);   // K, MN-major
-    mbar_wait(qg_full, 0);
-    // issue order S(0), S(1), dQ(0), S(2), dQ(1), ...: S(j+1) only needs S(j) loaded by the element-wise
-    // warps, dQ(j) needs dS(j)
-    for (int j = 0; j < nk + 1; ++j) {
-      if (j < nk) {  // S(j), dP(j)
-        const int sk = j % NK, sv = j % NV;
-        mbar_wait(&k_full[sk], (j / NK) & 1);
-        QTR(j, 0);
-        mbar_wait(&v_full[sv], (j / NV) & 1);
-        if (j > 0) mbar_wait(s_empty, (j - 1) & 1);
-        QTR(j, 1);
-        fence_after();
-        const uint64_t dk = desc_add(dK, sk * SM::KT), dv = desc_add(dV, sv * SM::KT);
-        if (leader) {
+    int jg = 0, it = 0;
+    for (int t = blockIdx.x; t < n_items; t += gridDim.x, ++it) {
+      int qt, h, sq, nk;
+      item(t, qt, h, sq, nk);
+      mbar_wait(qg_full, it & 1);
+      // issue order S(0), S(1), dQ(0), S(2), dQ(1), ...: S(j+1) only needs S(j) loaded by the element-wise
+      // warps, dQ(j) needs dS(j); all counters global (g = jg + j)
+      for (int j = 0; j < nk + 1; ++j) {
+        if (j < nk) {  // S(j), dP(j)
+          const int g = jg + j, sk = g % NK, sv = g % NV;
+          mbar_wait(&k_full[sk], (g / NK) & 1);
+          mbar_wait(&v_full[sv], (g / NV) & 1);
+          if (g > 0) mbar_wait(s_empty, (g - 1) & 1);
+          fence_after();
+          const uint64_t dk = desc_add(dK, sk * SM::KT), dv = desc_add(dV, sv * SM::KT);
+          if (leader) {
 #pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk) {
-            const uint32_t o = (kk >> 2) * SM::SUB128 + (kk & 3) * 32;
-            umma_f16(t_s, desc_add(dQ, o), desc_add(dk, o), idesc_s, kk > 0);
-            umma_f16(t_dp, desc_add(dG, o), desc_add(dv, o), idesc_s, kk > 0);
+            for (int kk = 0; kk < DH / 16; ++kk) {
+              const uint32_t o = (kk >> 2) * SM::SUB128 + (kk & 3) * 32;
+              umma_f16(t_s, desc_add(dQ, o), desc_add(dk, o), idesc_s, kk > 0);
+              umma_f16(t_dp, desc_add(dG, o), desc_add(dv, o), idesc_s, kk > 0);
+            }
+            umma_commit(s_full);
+            umma_commit(&v_empty[sv]);   // V consumed by dP
+            if (j == nk - 1) umma_commit(qg_empty);   // Q / dO of this item fully read
           }
-          umma_commit(s_full);
-          umma_commit(&v_empty[sv]);   // V consumed by dP
+          __syncwarp();
         }
-        __syncwarp();
-      }
-      if (j >= 1) {  // dQ += dS K of iteration j-1 (A = dS from TMEM)
-        const int jj = j - 1, sk = jj % NK, pb = jj & 1;
-        mbar_wait(&p_full[pb], (jj >> 1) & 1);
-        QTR(jj, 2);
-        fence_after();
-        const uint64_t dk = desc_add(dKm, sk * SM::KT);
-        if (leader) {
+        if (j >= 1) {  // dQ += dS K of iteration j-1 (A = dS from TMEM)
+          const int jj = j - 1, g = jg + jj, sk = g % NK, pb = g & 1;
+          if (jj == 0 && it > 0) mbar_wait(acc_free, (it - 1) & 1);   // the previous item's dQ drained
+          mbar_wait(&p_full[pb], (g >> 1) & 1);
+          fence_after();
+          const uint64_t dk = desc_add(dKm, sk * SM::KT);
+          if (leader) {
 #pragma unroll
-          for (int kk = 0; kk < KB2 / 16; ++kk)   // 16 keys = 8 packed dS columns, 16 K rows
-            umma_f16_ts(t_dq, t_ds(pb) + 8 * kk, desc_add(dk, kk * 16 * 128), idesc_q, (jj > 0 || kk > 0) ? 1u : 0u);
-          umma_commit(&g_done[pb]);
-          umma_commit(&k_empty[sk]);
+            for (int kk = 0; kk < KB2 / 16; ++kk)   // 16 keys = 8 packed dS columns, 16 K rows
+              umma_f16_ts(t_dq, t_ds(pb) + 8 * kk, desc_add(dk, kk * 16 * 128), idesc_q, (jj > 0 || kk > 0) ? 1u : 0u);
+            umma_commit(&g_done[pb]);
+            umma_commit(&k_empty[sk]);
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
+      jg += nk;
     }
   } else if (warp >= 4) {  // ===== element-wise: one query row per 4 threads, 32 key columns each
     const int cg = (warp - 4) >> 2;             // key-column group 0..3
     const int qd = warp & 3;
     const int r = qd * 32 + lane;
-    const int q = q0 + r;
     const uint32_t lrow = (uint32_t)(qd * 32) << 16;
     const float sl2 = a.scale * LOG2E;
-    const int64_t rb = ((int64_t)sq * a.heads + h) * s;
-    const float lse2 = q < s ? a.lse[rb + q] * LOG2E : 0.f;
-    const float Dq = q < s ? a.dsum[rb + q] : 0.f;
-    for (int j = 0; j < nk; ++j) {
-      const int ka = j * KB2 + cg * 32;
-      const bool need_mask = q >= s || ka + 32 > s || (a.causal && ka + 31 > q0 + qd * 32);
-      mbar_wait(s_full, j & 1);
-      if (warp == 4 && lane == 0) QTR(j, 3);
-      fence_after();
-      uint32_t rsv[2][16], rdp[2][16];
+    int jg = 0;
+    for (int t = blockIdx.x; t < n_items; t += gridDim.x) {
+      int qt, h, sq, nk;
+      item(t, qt, h, sq, nk);
+      const int q0 = qt * QB2, q = q0 + r;
+      const int64_t rb = ((int64_t)sq * a.heads + h) * s;
+      const float lse2 = q < s ? a.lse[rb + q] * LOG2E : 0.f;
+      const float Dq = q < s ? a.dsum[rb + q] : 0.f;
+      for (int j = 0; j < nk; ++j) {
+        const int g = jg + j;
+        const int ka = j * KB2 + cg * 32;
+        const bool need_mask = q >= s || ka + 32 > s || (a.causal && ka + 31 > q0 + qd * 32);
+        mbar_wait(s_full, g & 1);
+        fence_after();
+        uint32_t rsv[2][16], rdp[2][16];
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
-        tmem_ld16_nowait(t_s + lrow + cg * 32 + ch * 16, rsv[ch]);
-        tmem_ld16_nowait(t_dp + lrow + cg * 32 + ch * 16, rdp[ch]);
-      }
-      tmem_wait_ld();
-      if (warp == 4 && lane == 0) QTR(j, 4);
-      fence_before();
-      mbar_arrive(s_empty);   // S / dP buffer free for S(j+1)
-      uint32_t pd[16];
+        for (int ch = 0; ch < 2; ++ch) {
+          tmem_ld16_nowait(t_s + lrow + cg * 32 + ch * 16, rsv[ch]);
+          tmem_ld16_nowait(t_dp + lrow + cg * 32 + ch * 16, rdp[ch]);
+        }
+        tmem_wait_ld();
+        fence_before();
+        mbar_arrive(s_empty);   // S / dP buffer free for S(g+1)
+        uint32_t pd[16];
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
-        float sc[16];
+        for (int ch = 0; ch < 2; ++ch) {
+          float sc[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) sc[c] = fmaf(__uint_as_float(rsv[ch][c]), sl2, -lse2);
-        if (need_mask) {
+          for (int c = 0; c < 16; ++c) sc[c] = fmaf(__uint_as_float(rsv[ch][c]), sl2, -lse2);
+          if (need_mask) {
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const int kj = ka + ch * 16 + c;
-            if (!(q < s && kj < s && (!a.causal || kj <= q))) sc[c] = -INFINITY;
+            for (int c = 0; c < 16; ++c) {
+              const int kj = ka + ch * 16 + c;
+              if (!(q < s && kj < s && (!a.causal || kj <= q))) sc[c] = -INFINITY;
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 16; c += 2) {
+            float gg[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) gg[e] = ex2(sc[c + e]) * (__uint_as_float(rdp[ch][c + e]) - Dq) * a.scale;
+            pd[ch * 8 + c / 2] = pack_bf16x2(gg[0], gg[1]);
           }
         }
-#pragma unroll
-        for (int c = 0; c < 16; c += 2) {
-          float g[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) g[e] = ex2(sc[c + e]) * (__uint_as_float(rdp[ch][c + e]) - Dq) * a.scale;
-          pd[ch * 8 + c / 2] = pack_bf16x2(g[0], g[1]);
+        const int pb = g & 1;
+        if (g >= 2) {
+          mbar_wait(&g_done[pb], ((g >> 1) & 1) ^ 1);   // dQ MMAs of iteration g-2 done: dS buffer free
+          fence_after();
         }
+        tmem_st16_nowait(t_ds(pb) + lrow + cg * 16, pd);
+        tmem_wait_st();
+        fence_before();
+        mbar_arrive(&p_full[pb]);
       }
-      const int pb = j & 1;
-      if (j >= 2) {
-        mbar_wait(&g_done[pb], ((j >> 1) & 1) ^ 1);   // dQ MMAs of iteration j-2 done: dS buffer free
-        fence_after();
-      }
-      tmem_st16_nowait(t_ds(pb) + lrow + cg * 16, pd);
-      tmem_wait_st();
-      if (warp == 4 && lane == 0) QTR(j, 5);
-      if (warp == 19 && lane == 0) QTR(j, 6);
+      const int gl = jg + nk - 1;
+      mbar_wait(&g_done[gl & 1], (gl >> 1) & 1);   // the item's last dQ MMAs (and all before) done
+      fence_after();
+      constexpr int OC = DH / 4;
+      __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + q) * 3 * d + h * DH + cg * OC;
+      float* cs = a.colsum ? a.colsum + ((int64_t)(sq * nqt + qt) * 4 + qd) * 3 * d + h * DH + cg * OC : nullptr;
+      store_row_bf16_global(out, t_dq + lrow + cg * OC, OC, 1.f, q < s, cs);
       fence_before();
-      mbar_arrive(&p_full[pb]);
+      mbar_arrive(acc_free);   // dQ accumulator free for the next item
+      jg += nk;
     }
-    mbar_wait(&g_done[(nk - 1) & 1], ((nk - 1) >> 1) & 1);   // the last dQ MMAs (and all before) done
-    fence_after();
-    constexpr int OC = DH / 4;
-    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + q) * 3 * d + h * DH + cg * OC;
-    float* cs = a.colsum ? a.colsum + ((int64_t)(sq * nqt + qt) * 4 + qd) * 3 * d + h * DH + cg * OC : nullptr;
-    store_row_bf16_global(out, t_dq + lrow + cg * OC, OC, 1.f, q < s, cs);
   }
   fence_before();
   __syncthreads();
@@ -628,10 +687,10 @@ static cudaError_t run(const AttnArgs& a, cudaStream_t st) {
       return e;
     set = true;
   }
-  dim3 gk((a.seq + KB - 1) / KB, a.heads, a.nseq);
-  note_launch(), dkdv_kernel<DH><<<gk, NT, DkvSmem<DH>::TOTAL, st>>>(kv128, q64, g64, a);
-  dim3 gq((a.seq + QB2 - 1) / QB2, a.heads, a.nseq);
-  note_launch(), dq_kernel<DH><<<gq, NT, DqSmem<DH>::TOTAL, st>>>(q128, g128, kv128, a);
+  const int dkv_items = ((a.seq + KB - 1) / KB) * a.heads * a.nseq;
+  note_launch(), dkdv_kernel<DH><<<std::min(dkv_items, num_sms()), NT, DkvSmem<DH>::TOTAL, st>>>(kv128, q64, g64, a);
+  const int dq_items = ((a.seq + QB2 - 1) / QB2) * a.heads * a.nseq;
+  note_launch(), dq_kernel<DH><<<std::min(dq_items, num_sms()), NT, DqSmem<DH>::TOTAL, st>>>(q128, g128, kv128, a);
   return cudaGetLastError();
 }
 

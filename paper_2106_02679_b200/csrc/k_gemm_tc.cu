@@ -253,7 +253,7 @@ __device__ __forceinline__ void epilogue_loop(const GemmArgs& g, const EpiMaps& 
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&em.out, sb, n0, m0w);
+          tma_store_2d_hint(&em.out, sb, n0, m0w, policy_evict_first());
           bulk_commit();
         }
         if (e.colsum) {   // bias gradient partial of this 32-row strip (rows past M contribute 0)
@@ -355,11 +355,12 @@ __device__ __forceinline__ void epilogue_loop(const GemmArgs& g, const EpiMaps& 
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
+        const uint64_t pol = policy_evict_first();   // outputs stream out; keep L2 for the operands
         if (e.kind == EPI_GELU_FWD) {
-          tma_store_2d(&em.aux, sbuf, n0, m0w);
-          tma_store_2d(&em.out, sbuf + 2048, n0, m0w);
+          tma_store_2d_hint(&em.aux, sbuf, n0, m0w, pol);
+          tma_store_2d_hint(&em.out, sbuf + 2048, n0, m0w, pol);
         } else {
-          tma_store_2d(&em.out, sbuf, n0, m0w);
+          tma_store_2d_hint(&em.out, sbuf, n0, m0w, pol);
         }
         bulk_commit();
       }
@@ -402,7 +403,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     kb0 = ks * nkper;
     kb1 = min(nk_all, kb0 + nkper);
   };
-  constexpr int GM = 8;   // tile raster: groups of GM m-blocks sweep all n-blocks (L2 reuse of B)
+  // tile raster: groups of GM m-blocks sweep all n-blocks (L2 reuse of B).  (Groups sized to one wave of tiles,
+  // GM = grid / num_n, cut the FFN1 A over-fetch but raised FFN2's and the step time: measured, reverted.)
+  constexpr int GM = 8;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -430,6 +433,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer
+      // B re-read by every m-block of the grid: kept in L2 when it fits comfortably (the weights)
+      const uint64_t polB = g.b_keep_l2 ? policy_evict_last() : policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -450,10 +455,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int i = 0; i < BM / 64; ++i) tma_load_2d(sa + i * 64 * BK * 2, &tmA, &full[stage], m0 + 64 * i, k0);
           }
           if (!B_MN) {
-            tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+            tma_load_2d_hint(sb, &tmB, &full[stage], k0, n0, polB);
           } else {
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i) tma_load_2d(sb + i * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * i, k0);
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load_2d_hint(sb + i * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * i, k0, polB);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -579,6 +585,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer (both CTAs), completion counted on the leader's full barrier
+      // B re-read by every m-block of the grid: kept in L2 when it fits comfortably (the weights)
+      const uint64_t polB = g.b_keep_l2 ? policy_evict_last() : policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < num_tiles; t += npairs) {
@@ -598,11 +606,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             for (int i = 0; i < BM / 64; ++i) tma_load_2d_cg2(sa + i * 64 * BK * 2, &tmA, &full[stage], m0 + 64 * i, k0);
           }
           if (!B_MN) {
-            tma_load_2d_cg2(sb, &tmB, &full[stage], k0, n0);
+            tma_load_2d_cg2_hint(sb, &tmB, &full[stage], k0, n0, polB);
           } else {
 #pragma unroll
             for (int i = 0; i < (PAIR_N / 2) / 64; ++i)
-              tma_load_2d_cg2(sb + i * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * i, k0);
+              tma_load_2d_cg2_hint(sb + i * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * i, k0, polB);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -847,6 +855,8 @@ cudaError_t gemm_bf16_tc(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return cudaSuccess;
   if (g.K <= 0) return cudaErrorInvalidValue;
   const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
+  GemmArgs& gm = const_cast<GemmArgs&>(g);
+  gm.b_keep_l2 = (int64_t)g.N * g.K * 2 <= (int64_t)48 << 20;   // weights (<= 48 MB), not activation gradients
   // Kernel choice by a wave-count cost model: per-SM work of one wave (pair tile: 128 x 256 per SM) times
   // the number of waves, over the kernel's relative per-SM throughput (CTA pair 1.0, single-CTA 128 x 256
   // 0.85, 128 x 128 0.70 -- measured kbench ratios).  A pair wave that leaves SMs idle can still beat a

@@ -47,6 +47,7 @@ struct GemmArgs {
   int split_k = 1;
   float* splitk_ws = nullptr;
   int64_t splitk_ws_floats = 0;   // workspace capacity
+  bool b_keep_l2 = false;          // set by gemm_bf16_tc: B small enough to pin in L2 (evict_last TMA loads)
 };
 
 void gemm_f32_simt(const GemmArgs& g, cudaStream_t st);       // fp32 operands, CUDA cores
