@@ -286,6 +286,13 @@ def main():
         if dist is not None:
             dist.barrier()
 
+    def all_ranks(v: float) -> list:
+        if dist is None:
+            return [v]
+        out = [torch.zeros(1, device="cuda", dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(out, torch.tensor([v], device="cuda", dtype=torch.float64))
+        return [float(t.item()) for t in out]
+
     def max_over_ranks(v: float) -> float:
         if dist is None:
             return v
@@ -325,6 +332,8 @@ def main():
         torch.cuda.synchronize()
         clk = clocks.stop() if clocks else None
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    stall_ranks = all_ranks(prof["comm_wait_ms"] / args.steps)
+    p2p_ranks = all_ranks(prof["p2p_wait_ms"] / args.steps)
     stats_last, _ = tr.comm_stats()
     nvlink = None
     if nvl1 is not None:
@@ -439,6 +448,10 @@ def main():
         "exposed_comm_ab": ab,
         "nvlink": nvlink,
         "p2p_wait_ms_per_step": prof["p2p_wait_ms"] / args.steps,
+        # per rank (rank order): a pipeline stage on a faster GPU also waits for the slowest stage; the minimum
+        # over ranks is the bubble the schedule itself leaves
+        "exposed_comm_ms_per_step_ranks": stall_ranks,
+        "p2p_wait_ms_per_step_ranks": p2p_ranks,
         "model_tflops_per_gpu": value * fpt / world / 1e12,
         "mfu_vs_measured_peak": value * fpt / world / 1e12 / peaks.get("bf16_tflops", 1620.5),
         "roofline": roofline,

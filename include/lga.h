@@ -171,6 +171,21 @@ const char* lga_last_error(void);
  * Either output may be NULL. */
 lga_status lga_param_count(const lga_config* cfg, uint64_t* per_layer, uint64_t* total);
 
+/* The host-side plan of one rank, exactly as lga_init derives it (no device work; callable on a machine without
+ * a GPU): its stage and replica (rank grid above), its local layers (first_layer, first_layer + layer_stride,
+ * ... : i mod P = stage for the modular map P:127, a contiguous block with LGA_FLAG_CONTIGUOUS_PP), the
+ * micro-batches per kernel launch (chunk), the per-step pipeline transfers it sends / receives in forward and
+ * backward (the targets of its flag waits; their sum is lga_comm_stats.p2p_send_calls / p2p_recv_calls,
+ * P:598), and its training-state shard (S = padded layer / D elements per layer, reading A-10).
+ * Errors: as lga_init's configuration checks. */
+typedef struct {
+  int32_t stage, replica, local_layers, chunk;
+  int32_t first_layer, layer_stride;
+  uint64_t p2p_send_fwd, p2p_recv_fwd, p2p_send_bwd, p2p_recv_bwd;
+  uint64_t shard_elems, layer_elems_padded;
+} lga_rank_plan;
+lga_status lga_plan(const lga_config* cfg, int32_t rank, int32_t world, lga_rank_plan* out);
+
 /* Fill `out` (LGA_NCCL_ID_BYTES bytes, host) with a fresh NCCL unique id.  Rank 0 calls
  * it and the caller broadcasts the bytes to every rank (e.g. over torch.distributed)
  * before lga_init.  Needed only for the NCCL baseline (LGA_FLAG_NCCL_DP with dp > 1). */

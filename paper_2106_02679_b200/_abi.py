@@ -71,6 +71,15 @@ class lga_timing(C.Structure):
 # int32_t (*lga_allgather_fn)(void* ctx, const void* send, void* recv, uint64_t bytes)  (include/lga.h)
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
 
+class lga_rank_plan(C.Structure):
+    _fields_ = ([(n, C.c_int32) for n in ("stage", "replica", "local_layers", "chunk", "first_layer", "layer_stride")]
+                + [(n, C.c_uint64) for n in ("p2p_send_fwd", "p2p_recv_fwd", "p2p_send_bwd", "p2p_recv_bwd",
+                                             "shard_elems", "layer_elems_padded")])
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
 _lib = None
 
 
@@ -90,6 +99,7 @@ def lib():
         "lga_last_error": (C.c_char_p, []),
         "lga_param_count": (C.c_int, [C.POINTER(lga_config), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "lga_nccl_unique_id": (C.c_int, [C.c_char_p]),
+        "lga_plan": (C.c_int, [C.POINTER(lga_config), C.c_int32, C.c_int32, C.POINTER(lga_rank_plan)]),
         "lga_init": (C.c_int, [C.POINTER(lga_config), C.c_int32, C.c_int32, C.c_int32, ALLGATHER_FN, C.c_void_p,
                                C.c_char_p, C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(H)]),
         "lga_step": (C.c_int, [H, C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]),
@@ -116,6 +126,6 @@ def check(status: int):
         raise LgaError(status, lib().lga_last_error().decode(errors="replace"))
 
 
-EXPORTED = ["lga_abi_version", "lga_status_string", "lga_last_error", "lga_param_count", "lga_nccl_unique_id",
+EXPORTED = ["lga_abi_version", "lga_status_string", "lga_last_error", "lga_param_count", "lga_plan", "lga_nccl_unique_id",
             "lga_init", "lga_step", "lga_step_host", "lga_grads", "lga_params", "lga_comm_bytes", "lga_layer_stage",
             "lga_timing_last", "lga_destroy"]

@@ -47,6 +47,12 @@ class Config:
     def tokens_per_replica(self) -> int:
         return self.n_micro * self.micro_batch * self.seq_len
 
+    def plan(self, rank: int = 0):
+        """lga_plan: this configuration's host-side plan of `rank` (no GPU needed)."""
+        out = _abi.lga_rank_plan()
+        check(lib().lga_plan(C.byref(self.to_c()), rank, self.dp * self.pp, C.byref(out)))
+        return out.as_dict()
+
     def param_count(self):
         pl, tot = C.c_uint64(), C.c_uint64()
         check(lib().lga_param_count(C.byref(self.to_c()), C.byref(pl), C.byref(tot)))

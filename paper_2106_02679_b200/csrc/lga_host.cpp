@@ -300,8 +300,20 @@ namespace lga {
 // pipeline map: modular, layer i on stage i mod P; contiguous, stage i / (L/P)
 static int stage_of(const Cfg& c, int64_t i) { return c.contig ? (int)(i / c.Lloc) : (int)(i % c.P); }
 static int local_index(const Cfg& c, int64_t i) { return c.contig ? (int)(i % c.Lloc) : (int)(i / c.P); }
-static int64_t local_to_global(const lga_handle* h, int j) {
-  return h->c.contig ? (int64_t)h->stage * h->c.Lloc + j : (int64_t)h->stage + (int64_t)j * h->c.P;
+static int64_t local_to_global_s(const Cfg& c, int stage, int j) {
+  return c.contig ? (int64_t)stage * c.Lloc + j : (int64_t)stage + (int64_t)j * c.P;
+}
+static int64_t local_to_global(const lga_handle* h, int j) { return local_to_global_s(h->c, h->stage, j); }
+// Pipeline transfers per step of a stage (the flag epochs of the receive waits): N micro-batches at every
+// layer boundary crossing to / from another stage, forward and backward.  Shared by lga_init and lga_plan.
+static void plan_transfers(const Cfg& c, int stage, unsigned long long* send_fwd, unsigned long long* recv_fwd,
+                           unsigned long long* send_bwd, unsigned long long* recv_bwd) {
+  *send_fwd = *recv_fwd = *send_bwd = *recv_bwd = 0;
+  for (int j = 0; j < c.Lloc && c.P > 1; ++j) {
+    const int64_t i = local_to_global_s(c, stage, j);
+    if (i > 0 && stage_of(c, i - 1) != stage) *recv_fwd += c.N, *send_bwd += c.N;
+    if (i < c.L - 1 && stage_of(c, i + 1) != stage) *send_fwd += c.N, *recv_bwd += c.N;
+  }
 }
 static bool owns_last(const lga_handle* h) { return stage_of(h->c, h->c.L - 1) == h->stage; }
 static ncclDataType_t nccl_dt(DT t) { return t == DT::F32 ? ncclFloat32 : ncclBfloat16; }
@@ -1393,6 +1405,28 @@ lga_status lga_param_count(const lga_config* cfg, uint64_t* per_layer, uint64_t*
   return LGA_OK;
 }
 
+lga_status lga_plan(const lga_config* cfg, int32_t rank, int32_t world, lga_rank_plan* out) {
+  if (!out) return ERR(LGA_ERR_INVALID_ARG, "out is NULL");
+  Cfg c;
+  lga_status s = validate(cfg, world, &c);
+  if (s != LGA_OK) return s;
+  if (rank < 0 || rank >= world) return ERR(LGA_ERR_INVALID_ARG, "rank %d out of [0, %d)", rank, world);
+  lga_rank_plan p{};
+  p.stage = rank % c.P;
+  p.replica = rank / c.P;
+  p.local_layers = c.Lloc;
+  p.chunk = c.c;
+  p.first_layer = (int32_t)local_to_global_s(c, p.stage, 0);
+  p.layer_stride = c.contig ? 1 : c.P;
+  unsigned long long sf, rf, sb, rb;
+  plan_transfers(c, p.stage, &sf, &rf, &sb, &rb);
+  p.p2p_send_fwd = sf; p.p2p_recv_fwd = rf; p.p2p_send_bwd = sb; p.p2p_recv_bwd = rb;
+  p.shard_elems = (uint64_t)c.S;
+  p.layer_elems_padded = (uint64_t)c.plpad;
+  *out = p;
+  return LGA_OK;
+}
+
 lga_status lga_nccl_unique_id(uint8_t* out) {
   if (!out) return ERR(LGA_ERR_INVALID_ARG, "out is NULL");
   ncclUniqueId id;
@@ -1495,11 +1529,7 @@ lga_status lga_init(const lga_config* cfg, int32_t rank, int32_t world, int32_t 
   h->ev_x.assign(c.N, nullptr);
   for (auto& e : h->ev_x) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // pipeline transfers per step on this stage (flag epochs): chunks of every layer boundary it crosses
-  for (int j = 0; j < c.Lloc && c.P > 1; ++j) {
-    const int64_t i = local_to_global(h, j);
-    if (i > 0 && stage_of(c, i - 1) != h->stage) h->k_recv_fwd += c.N, h->k_send_bwd += c.N;
-    if (i < c.L - 1 && stage_of(c, i + 1) != h->stage) h->k_send_fwd += c.N, h->k_recv_bwd += c.N;
-  }
+  plan_transfers(c, h->stage, &h->k_send_fwd, &h->k_recv_fwd, &h->k_send_bwd, &h->k_recv_bwd);
   CK(cudaEventCreate(&h->ev_t0));
   CK(cudaEventCreate(&h->ev_t1));
   CK(cudaEventCreate(&h->ev_fwd_end));

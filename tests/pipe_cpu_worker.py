@@ -1,5 +1,6 @@
 """One rank (stage = rank mod P of replica = rank div P, the rank grid of include/lga.h) of the CPU (gloo)
-modular-pipeline test, launched by tests/test_dist_cpu.py through torchrun.  It plays the host-side
+modular-pipeline ORACLE-CONSISTENCY test, launched by tests/test_dist_cpu.py through torchrun (it does not
+call liblga; lga_plan is checked against the same closed forms in test_abi_cpu.py).  It plays the
 protocol of the library's modular pipeline with the fp64 oracle as the compute (TEST
 INFRASTRUCTURE): layer i lives on stage i mod P (reading A-11); the layered schedule runs every
 layer over all N micro-batches before the next; after the forward of (layer i, micro-batch m) the

@@ -84,3 +84,31 @@ def test_status_strings():
     L = _abi.lib()
     for k, v in _abi.STATUS.items():
         assert L.lga_status_string(k).decode() == v
+
+
+@pytest.mark.parametrize("L,P,D,N,contig", [(4, 2, 1, 4, False), (8, 4, 1, 4, False), (4, 2, 2, 4, False),
+                                            (48, 4, 2, 32, False), (8, 4, 1, 8, True), (4, 2, 2, 4, True),
+                                            (24, 1, 8, 16, False)])
+def test_rank_plan_matches_closed_forms(L, P, D, N, contig):
+    """lga_plan (no GPU): the library's host-side rank plan -- the same function lga_init uses for the pipeline
+    flag epochs -- against oracle.counters: stage = rank mod P, the stage's local layers (modular i mod P,
+    P:127; contiguous blocks), per-step transfers = the closed-form p2p call counts, shard size."""
+    from oracle import counters as oc
+    from paper_2106_02679_b200 import Config, _abi
+    flags = _abi.LGA_FLAG_CONTIGUOUS_PP if contig else 0
+    cfg = Config(layers=L, d_model=64, heads=4, seq_len=32, micro_batch=2, n_micro=N, dp=D, pp=P, precision=0,
+                 flags=flags)
+    pipeline = "contiguous" if contig else "modular"
+    for rank in range(D * P):
+        p = cfg.plan(rank)
+        assert p["stage"] == rank % P and p["replica"] == rank // P
+        mine = oc.local_layers(p["stage"], L, P, pipeline)
+        assert [p["first_layer"] + k * p["layer_stride"] for k in range(p["local_layers"])] == mine
+        ref = oc.comm_counters(oc.StepShape(layers=L, d=64, seq=32, micro_batch=2, n_micro=N, dp=D, pp=P),
+                               stage=p["stage"], pipeline=pipeline)
+        assert p["p2p_send_fwd"] + p["p2p_send_bwd"] == ref["p2p_send_calls"]
+        assert p["p2p_recv_fwd"] + p["p2p_recv_bwd"] == ref["p2p_recv_calls"]
+        assert p["p2p_send_fwd"] == p["p2p_recv_bwd"] and p["p2p_recv_fwd"] == p["p2p_send_bwd"]
+        assert p["layer_elems_padded"] == oc.padded_layer_params(64, D)
+        assert p["shard_elems"] == p["layer_elems_padded"] // D
+        assert p["chunk"] == (N if P == 1 else 1)

@@ -1,4 +1,8 @@
-"""World-size-2 gloo tests on CPU for the N > 1 host logic (no GPU):
+"""World-size-2 / 4 gloo tests on CPU (no GPU).  These are ORACLE-CONSISTENCY tests of the decompositions the
+library implements, played in Python with the fp64 oracle as the compute: they do not call liblga.  The
+library's own host logic is checked on CPU by test_abi_cpu.py::test_rank_plan_matches_closed_forms (lga_plan:
+the rank grid, local layers and pipeline flag targets lga_init uses), and its multi-rank data paths by the
+-m gpu tests of test_gpu_dist.py (which also run with all ranks sharing one GPU).
 
 * the data-parallel decomposition the library implements -- per-replica micro-batch ownership (A-10),
   unscaled sums reduced over replicas with one 1/(D N) scale (A-3), shards of the 64 D-padded layer vector
