@@ -159,6 +159,8 @@ typedef struct {
   uint32_t gemm_launches, attn_launches, adam_launches;
   double gemm_flop, attn_flop, adam_bytes;
   uint64_t kernel_launches;  /* every kernel this library launched in the step (NCCL excluded) */
+  uint64_t graph_captures;   /* step graphs captured since lga_init (a small cache keyed by the x / target
+                                pointers: alternating two input buffers captures twice, then replays) */
 } lga_timing;
 
 typedef struct lga_handle lga_handle;

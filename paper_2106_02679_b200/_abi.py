@@ -62,7 +62,7 @@ class lga_timing(C.Structure):
                                           "gemm_ms", "attn_ms", "adam_ms")]
                 + [(n, C.c_uint32) for n in ("gemm_launches", "attn_launches", "adam_launches")]
                 + [(n, C.c_double) for n in ("gemm_flop", "attn_flop", "adam_bytes")]
-                + [("kernel_launches", C.c_uint64)])
+                + [("kernel_launches", C.c_uint64), ("graph_captures", C.c_uint64)])
 
     def as_dict(self):
         return {n: float(getattr(self, n)) for n, _ in self._fields_}

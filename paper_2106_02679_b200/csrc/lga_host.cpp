@@ -272,11 +272,18 @@ struct lga_handle {
   // CUDA graph of lga_step (captured at the second call, replayed while x / target keep their pointers)
   bool capturing = false, graph_broken = false;
   int eager_steps = 0;
-  cudaGraphExec_t gexec = nullptr;
-  const float *g_x = nullptr, *g_T = nullptr;
-  lga_comm_stats g_last{};
-  int g_nwait = 0, g_nprof = 0;
-  unsigned long long g_launches = 0;
+  // a small cache keyed by the (x, target) pointers: a data loader that double-buffers its inputs replays
+  // two graphs instead of re-capturing every step
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    const float *x = nullptr, *T = nullptr;
+    lga_comm_stats last{};
+    int nwait = 0, nprof = 0;
+    unsigned long long launches = 0, used = 0;
+  };
+  static constexpr int kGraphs = 2;
+  StepGraph graphs[kGraphs];
+  unsigned long long graph_clock = 0, graph_captures = 0;
   int64_t partial_floats = 0;
   // events
   std::vector<cudaEvent_t> ev_ag, ev_slot_free;   // per slot
@@ -1467,7 +1474,8 @@ static void free_handle(lga_handle* h) {
     }
   }
   cudaGetLastError();
-  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  for (auto& gr : h->graphs)
+    if (gr.exec) cudaGraphExecDestroy(gr.exec);
   for (size_t q = 0; q < h->wbase.size(); ++q)
     if (h->wbase[q] && h->wbase[q] != h->arena.base) cudaIpcCloseMemHandle(h->wbase[q]);
   if (h->dp_comm) ncclCommDestroy(h->dp_comm);
@@ -1756,7 +1764,7 @@ static void issue_step(lga_handle* h, const float* x, const float* T, bool host_
 
 // Capture issue_step into a graph (LGA_FLAG_NO_GRAPH off, device inputs).  False on any capture failure
 // (the step then runs eagerly and capture is not retried).
-static bool capture_step(lga_handle* h, const float* x, const float* T) {
+static bool capture_step(lga_handle* h, lga_handle::StepGraph& gr, const float* x, const float* T) {
   cudaGraph_t graph = nullptr;
   if (cudaStreamBeginCapture(h->s_comp, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
     cudaGetLastError();
@@ -1777,19 +1785,19 @@ static bool capture_step(lga_handle* h, const float* x, const float* T) {
     if (graph) cudaGraphDestroy(graph);
     return false;
   }
-  e = cudaGraphInstantiateWithFlags(&h->gexec, graph, cudaGraphInstantiateFlagUseNodePriority);
+  e = cudaGraphInstantiateWithFlags(&gr.exec, graph, cudaGraphInstantiateFlagUseNodePriority);
   cudaGraphDestroy(graph);
   if (e != cudaSuccess) {
     cudaGetLastError();
-    h->gexec = nullptr;
+    gr.exec = nullptr;
     return false;
   }
-  h->g_x = x;
-  h->g_T = T;
-  h->g_last = h->last;
-  h->g_nwait = h->n_wait;
-  h->g_nprof = h->n_prof;
-  h->g_launches = launch_count() - l0;
+  gr.x = x;
+  gr.T = T;
+  gr.last = h->last;
+  gr.nwait = h->n_wait;
+  gr.nprof = h->n_prof;
+  gr.launches = launch_count() - l0;
   return true;
 }
 
@@ -1807,21 +1815,35 @@ static lga_status run_step(lga_handle* h, const float* x, const float* T, double
   // CUDA graph of the whole step: captured at the second device-input call, replayed while the input
   // pointers stay the same; the first call (lazy initialisation) and host-input calls run eagerly
   const bool graph_ok = !host_inputs && !c.graph_off && !h->graph_broken && h->eager_steps >= 1;
-  if (graph_ok && h->gexec && (x != h->g_x || T != h->g_T)) {
-    CK(cudaGraphExecDestroy(h->gexec));
-    h->gexec = nullptr;
+  lga_handle::StepGraph* gr = nullptr;
+  if (graph_ok) {
+    for (auto& e : h->graphs)
+      if (e.exec && e.x == x && e.T == T) gr = &e;
+    if (!gr) {   // capture into a free slot or over the least recently used one
+      gr = &h->graphs[0];
+      for (auto& e : h->graphs)
+        if (!e.exec || e.used < gr->used) gr = &e;
+      if (gr->exec) {
+        CK(cudaGraphExecDestroy(gr->exec));
+        gr->exec = nullptr;
+      }
+      CK(cudaEventRecord(h->ev_in, h->user));          // order the capture's stream after the caller
+      CK(cudaStreamWaitEvent(h->s_comp, h->ev_in, 0));
+      if (!capture_step(h, *gr, x, T)) {
+        h->graph_broken = true;
+        gr = nullptr;
+      } else {
+        h->graph_captures++;
+      }
+    }
   }
-  if (graph_ok && !h->gexec) {
-    CK(cudaEventRecord(h->ev_in, h->user));          // order the capture's stream after the caller
-    CK(cudaStreamWaitEvent(h->s_comp, h->ev_in, 0));
-    if (!capture_step(h, x, T)) h->graph_broken = true;
-  }
-  if (graph_ok && h->gexec) {
-    CK(cudaGraphLaunch(h->gexec, h->user));
-    h->last = h->g_last;
-    h->n_wait = h->g_nwait;
-    h->n_prof = h->g_nprof;
-    h->launches_last = h->g_launches;
+  if (gr) {
+    gr->used = ++h->graph_clock;
+    CK(cudaGraphLaunch(gr->exec, h->user));
+    h->last = gr->last;
+    h->n_wait = gr->nwait;
+    h->n_prof = gr->nprof;
+    h->launches_last = gr->launches;
   } else {
     const unsigned long long l0 = launch_count();
     CK(cudaEventRecord(h->ev_in, h->user));
@@ -1958,6 +1980,7 @@ lga_status lga_timing_last(lga_handle* h, lga_timing* out) {
     }
   }
   t.kernel_launches = h->launches_last;
+  t.graph_captures = h->graph_captures;
   *out = t;
   return LGA_OK;
   ABI_CATCH

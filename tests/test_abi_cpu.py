@@ -29,7 +29,29 @@ def test_struct_layout_matches_header():
     # lga_config: 1 uint32 + 13 int32 + 6 float + 1 int32 + 1 uint32 = 22 * 4 bytes
     assert C.sizeof(_abi.lga_config) == 22 * 4
     assert C.sizeof(_abi.lga_comm_stats) == 14 * 8   # ABI v2: + allreduce_bytes
-    assert C.sizeof(_abi.lga_timing) == 8 * 4 + 3 * 4 + 4 + 3 * 8 + 8   # incl. padding before the doubles
+    assert C.sizeof(_abi.lga_timing) == 8 * 4 + 3 * 4 + 4 + 3 * 8 + 8 + 8   # padding; ABI v3: + graph_captures
+    # and against the C compiler's view of include/lga.h: every binding struct, size and field offsets
+    import os
+    import subprocess
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    structs = {"lga_config": _abi.lga_config, "lga_comm_stats": _abi.lga_comm_stats, "lga_timing": _abi.lga_timing,
+               "lga_rank_plan": _abi.lga_rank_plan}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "lga.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    lines.append("return 0; }")
+    with tempfile.TemporaryDirectory() as td:
+        src, exe = os.path.join(td, "s.c"), os.path.join(td, "s")
+        open(src, "w").write("\n".join(lines))
+        subprocess.run(["gcc", "-I", os.path.join(root, "include"), src, "-o", exe], check=True)
+        out = dict(l.split() for l in subprocess.run([exe], capture_output=True, text=True).stdout.splitlines())
+    for name, cls in structs.items():
+        assert int(out[name]) == C.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert int(out[f"{name}.{f}"]) == getattr(cls, f).offset, (name, f)
 
 
 def test_param_count_host_only():
