@@ -439,7 +439,7 @@ def main():
         "config": {"workload": desc, "layers": shape["layers"], "d_model": d, "heads": shape["heads"], "seq_len": s,
                    "micro_batch": b, "n_micro": N, "dp": dp, "pp": pp, "global_batch": dp * N * b,
                    "tokens_per_step": tokens_per_step, "schedule": args.schedule,
-                   "chunk": cfg.chunk or ("N" if pp == 1 else 1), "parallelism": f"dp{dp}" + (f"xpp{pp}" if pp > 1 else ""),
+                   "chunk": cfg.chunk or ("N" if pp == 1 else cfg.plan(rank)["chunk"]), "parallelism": f"dp{dp}" + (f"xpp{pp}" if pp > 1 else ""),
                    "l2": f"inputs larger than L2 (x and target {in_bytes / 1e6:.0f} MB each per replica, reused)",
                    "no_comm": bool(args.no_comm), "variant": variant or "paper default (partitioned, recompute, modular); DP over NVLink peer memory"},
         "step_ms_median": statistics.median(step_ms) if step_ms else None,

@@ -122,7 +122,8 @@ typedef struct {
   int32_t precision;       /* lga_precision */
   int32_t schedule;        /* lga_schedule */
   int32_t causal;          /* 1 = causal self-attention (GPT), 0 = the paper's encoder */
-  int32_t chunk;           /* micro-batches per kernel launch, 1..N (N/P when pp>1); 0 = auto */
+  int32_t chunk;           /* micro-batches per kernel launch, 1..N (N/P when pp>1); 0 = auto: N when pp == 1,
+                              else the largest divisor of N <= N/P with chunk * b * s <= 8192 tokens */
   float lr, beta1, beta2, adam_eps, weight_decay;   /* AdamW, torch semantics (reading A-4) */
   float ln_eps;            /* LayerNorm epsilon (biased variance), 1e-5 */
   int32_t retain_grads;    /* keep each step's reduced fp32 gradient shard for lga_grads */

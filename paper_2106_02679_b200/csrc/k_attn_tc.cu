@@ -258,8 +258,8 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
         }
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // 4 independent chains
 #pragma unroll
-        for (int c = 0; c < 64; ++c) m4[c & 3] = fmaxf(m4[c & 3], sv[c]);
-        float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        for (int c = 0; c < 64; c += 2) m4[(c >> 1) & 3] = fmax3(m4[(c >> 1) & 3], sv[c], sv[c + 1]);
+        float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
         mx *= sl2;
         const float m_new = (mx > m_used + RESCALE_THRESHOLD) ? mx : m_used;
         const float moff = m_new == -INFINITY ? 0.f : -m_new;   // fully masked so far: every p is 2^-inf = 0

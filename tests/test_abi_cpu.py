@@ -133,4 +133,5 @@ def test_rank_plan_matches_closed_forms(L, P, D, N, contig):
         assert p["p2p_send_fwd"] == p["p2p_recv_bwd"] and p["p2p_recv_fwd"] == p["p2p_send_bwd"]
         assert p["layer_elems_padded"] == oc.padded_layer_params(64, D)
         assert p["shard_elems"] == p["layer_elems_padded"] // D
-        assert p["chunk"] == (N if P == 1 else 1)
+        want = N if P == 1 else max(c for c in range(1, N // P + 1) if N % c == 0 and c * 2 * 32 <= 8192)
+        assert p["chunk"] == want
