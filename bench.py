@@ -254,11 +254,18 @@ def main():
 
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    ngpu = max(1, torch.cuda.device_count())
+    shared = world > ngpu            # more ranks than GPUs: ranks share devices (peer memory over CUDA IPC)
+    local = local % ngpu
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        # NCCL refuses two ranks on one device: gloo for the harness's own barriers when ranks share GPUs
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     if world % pp:
         raise SystemExit(f"workload {args.workload} needs a multiple of {pp} GPUs")
     dp = world // pp
@@ -289,14 +296,15 @@ def main():
     def all_ranks(v: float) -> list:
         if dist is None:
             return [v]
-        out = [torch.zeros(1, device="cuda", dtype=torch.float64) for _ in range(world)]
-        dist.all_gather(out, torch.tensor([v], device="cuda", dtype=torch.float64))
+        dev = "cpu" if shared else "cuda"
+        out = [torch.zeros(1, device=dev, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(out, torch.tensor([v], device=dev, dtype=torch.float64))
         return [float(t.item()) for t in out]
 
     def max_over_ranks(v: float) -> float:
         if dist is None:
             return v
-        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        t = torch.tensor([v], device="cpu" if shared else "cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -402,16 +410,20 @@ def main():
     peaks, peak_src = measured_peaks()
     gemm_tflops = prof["gemm_flop"] / (prof["gemm_ms"] / 1000.0) / 1e12 if prof["gemm_ms"] > 0 else 0.0
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-    traffic = None
+    # measured DRAM bytes per GEMM launch from the committed launch list of this workload's step
+    # (tools/gemm_traffic.py -> profiles/gemm_traffic.json), beside the algorithmic (compulsory) bytes
+    traffic, traffic_info = None, None
     tp_path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tp_path):
         try:
-            traffic = json.load(open(tp_path)).get(args.workload)
+            traffic_info = json.load(open(tp_path)).get(args.workload)
+            traffic = traffic_info["traffic_bytes_per_launch"] if isinstance(traffic_info, dict) else None
         except Exception:
-            traffic = None
+            traffic, traffic_info = None, None
     roofline = {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05 bf16, all GEMM launches of the step)",
                 "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
                 "frac": gemm_tflops / peak if peak else None, "traffic": traffic,
+                "traffic_detail": traffic_info,
                 "peak_source": peak_src + " bf16_tflops_sustained (kernel timed inside a long step)",
                 "launches": prof["gemm_launches"],
                 "flop_per_launch": prof["gemm_flop"] / max(1, prof["gemm_launches"]),
@@ -433,7 +445,7 @@ def main():
     from oracle import counters as oc
     fpt = oc.flops_per_token_model(shape["layers"], d, s)
     line = {
-        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": min(world, ngpu), "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16" if precision == LGA_BF16 else "f32", "data": "synthetic",
         "config": {"workload": desc, "layers": shape["layers"], "d_model": d, "heads": shape["heads"], "seq_len": s,
@@ -441,7 +453,8 @@ def main():
                    "tokens_per_step": tokens_per_step, "schedule": args.schedule,
                    "chunk": cfg.chunk or ("N" if pp == 1 else cfg.plan(rank)["chunk"]), "parallelism": f"dp{dp}" + (f"xpp{pp}" if pp > 1 else ""),
                    "l2": f"inputs larger than L2 (x and target {in_bytes / 1e6:.0f} MB each per replica, reused)",
-                   "no_comm": bool(args.no_comm), "variant": variant or "paper default (partitioned, recompute, modular); DP over NVLink peer memory"},
+                   "no_comm": bool(args.no_comm), "ranks": world,
+                   "ranks_share_gpus": bool(shared), "variant": variant or "paper default (partitioned, recompute, modular); DP over NVLink peer memory"},
         "step_ms_median": statistics.median(step_ms) if step_ms else None,
         "step_ms_p90": sorted(step_ms)[min(len(step_ms) - 1, int(0.9 * len(step_ms)))] if step_ms else None,
         "exposed_comm_ms_per_step": prof["comm_wait_ms"] / args.steps,

@@ -36,6 +36,12 @@ constexpr int NT = (4 + EW_WARPS) * 32;
 #define LGA_BWD_NST_DQ128 2
 #endif
 constexpr float LOG2E = 1.4426950408889634f;
+#ifndef LGA_BWD_POLY
+#define LGA_BWD_POLY 3
+#endif
+// of every 8 exponent pairs of an unmasked tile, computed by the FMA-pipe polynomial instead of the SFU (as in
+// the forward): the element-wise phase issues 2^x for every (query, key) pair, 64 / 128 per thread per tile
+constexpr int BWD_POLY = LGA_BWD_POLY;
 
 // rowsum(dO * o) per (sequence, head, position): d_h / 8 lanes per row (8 or 16, 16-byte loads), shuffle
 // reduction within the lane group
@@ -184,7 +190,8 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* g_done = p_full + 2;            // [2]
   uint64_t* kv_empty = g_done + 2;          // K / V read by the item's last S^T / dP^T MMAs
   uint64_t* acc_free = kv_empty + 1;        // dK / dV drained from TMEM by every element-wise thread
-  constexpr int NBAR = 2 * NST + 9;
+  uint64_t* dv_done = acc_free + 1;         // [2] the dV MMAs of an iteration done (P^T read)
+  constexpr int NBAR = 2 * NST + 11;
   static_assert(NBAR * 8 + 4 <= 256, "barrier area");
   static_assert(SM::TOTAL <= 232448, "shared memory");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
@@ -281,10 +288,13 @@ __global__ void __launch_bounds__(NT, 1)
       item(t, kt, h, sq, qstart, nq);
       // S^T(g) = K Q^T, dP^T(g) = V dO^T into buffer g & 1 (global iteration g = local i of this item), once
       // the gradient MMAs of iteration g - 2 have consumed the P^T / dS^T that buffer held
+      // S^T(g) only overwrites P^T(g-2), read by the dV MMAs, and dP^T(g) only dS^T(g-2), read by the dK MMAs:
+      // S^T(g) is issued as soon as dV(g-2) is done, so it queues behind dK(g-2) on the tensor pipe instead of
+      // the pipe idling while the issuer waits for both
       auto issue_s = [&](int g, int i) {
         const int st = g % NST, b = g & 1;
-        if (g >= 2) mbar_wait(&g_done[b], ((g - 2) >> 1) & 1);
         mbar_wait(&q_full[st], (g / NST) & 1);
+        if (g >= 2) mbar_wait(&dv_done[b], ((g - 2) >> 1) & 1);
         fence_after();
         const uint64_t dq = desc_add(dQk, st * SM::QT), dg = desc_add(dGk, st * SM::QT);
         if (leader) {
@@ -292,6 +302,15 @@ __global__ void __launch_bounds__(NT, 1)
           for (int kk = 0; kk < DH / 16; ++kk) {
             const uint32_t oa = (kk >> 2) * SM::SUB128 + (kk & 3) * 32, ob = (kk >> 2) * SM::SUB64 + (kk & 3) * 32;
             umma_f16(t_st(b), desc_add(dK, oa), desc_add(dq, ob), idesc_s, kk > 0);
+          }
+        }
+        __syncwarp();
+        if (g >= 2) mbar_wait(&g_done[b], ((g - 2) >> 1) & 1);
+        fence_after();
+        if (leader) {
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk) {
+            const uint32_t oa = (kk >> 2) * SM::SUB128 + (kk & 3) * 32, ob = (kk >> 2) * SM::SUB64 + (kk & 3) * 32;
             umma_f16(t_dpt(b), desc_add(dV, oa), desc_add(dg, ob), idesc_s, kk > 0);
           }
           umma_commit(&s_full[b]);
@@ -310,12 +329,17 @@ __global__ void __launch_bounds__(NT, 1)
         const uint64_t dq = desc_add(dQm, st * SM::QT), dg = desc_add(dGm, st * SM::QT);
         if (leader) {
 #pragma unroll
-          for (int kk = 0; kk < QB / 16; ++kk) {
+          for (int kk = 0; kk < QB / 16; ++kk) {   // dV first (its completion frees P^T for S^T(g+2))
             const uint32_t ta = 32 * (kk >> 1) + 8 * (kk & 1);   // 16 queries: owner half, 8 packed columns
             const uint32_t ob = kk * 16 * 128;                   // MN-major B: 16 query rows
-            const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-            umma_f16_ts(t_dv, t_st(b) + ta, desc_add(dg, ob), idesc_g, acc);
-            umma_f16_ts(t_dk, t_dpt(b) + ta, desc_add(dq, ob), idesc_g, acc);
+            umma_f16_ts(t_dv, t_st(b) + ta, desc_add(dg, ob), idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&dv_done[b]);
+#pragma unroll
+          for (int kk = 0; kk < QB / 16; ++kk) {
+            const uint32_t ta = 32 * (kk >> 1) + 8 * (kk & 1);
+            const uint32_t ob = kk * 16 * 128;
+            umma_f16_ts(t_dk, t_dpt(b) + ta, desc_add(dq, ob), idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&g_done[b]);
           umma_commit(&q_empty[st]);
@@ -344,6 +368,7 @@ __global__ void __launch_bounds__(NT, 1)
         const float* dsm = ls + 64;
         // valid iff q < s, kj < s and (causal) kj <= q; only tiles touching the diagonal / the end mask
         const bool need_mask = kj >= s || qa + 32 > s || (a.causal && kj > qa);
+        const bool any_mask = __any_sync(0xffffffffu, need_mask);   // warp-uniform polynomial choice
         mbar_wait(&s_full[grp], (g >> 1) & 1);
         fence_after();
         mbar_wait(&q_full[st], (g / NST) & 1);   // lse / dsum of tile g landed with Q / dO
@@ -367,11 +392,15 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int c = 0; c < 16; c += 2) {
             float p[2], gg[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              p[e] = ex2(sc[c + e]);
-              gg[e] = p[e] * (__uint_as_float(rdp[c + e]) - dsm[ch * 16 + c + e]) * a.scale;
+            if (!any_mask && ((c >> 1) & 7) < BWD_POLY) {
+              ex2_poly2(f2pack(sc[c], sc[c + 1]), p[0], p[1]);
+            } else {
+              p[0] = ex2(sc[c]);
+              p[1] = ex2(sc[c + 1]);
             }
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              gg[e] = p[e] * (__uint_as_float(rdp[c + e]) - dsm[ch * 16 + c + e]) * a.scale;
             pp[c / 2] = pack_bf16x2(p[0], p[1]);
             pd[c / 2] = pack_bf16x2(gg[0], gg[1]);
           }
@@ -604,6 +633,7 @@ __global__ void __launch_bounds__(NT, 1)
         const int g = jg + j;
         const int ka = j * KB2 + cg * 32;
         const bool need_mask = q >= s || ka + 32 > s || (a.causal && ka + 31 > q0 + qd * 32);
+        const bool any_mask = __any_sync(0xffffffffu, need_mask);   // warp-uniform polynomial choice
         mbar_wait(s_full, g & 1);
         fence_after();
         uint32_t rsv[2][16], rdp[2][16];
@@ -631,8 +661,14 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int c = 0; c < 16; c += 2) {
             float gg[2];
+            if (!any_mask && ((c >> 1) & 7) < BWD_POLY) {
+              ex2_poly2(f2pack(sc[c], sc[c + 1]), gg[0], gg[1]);
+            } else {
+              gg[0] = ex2(sc[c]);
+              gg[1] = ex2(sc[c + 1]);
+            }
 #pragma unroll
-            for (int e = 0; e < 2; ++e) gg[e] = ex2(sc[c + e]) * (__uint_as_float(rdp[ch][c + e]) - Dq) * a.scale;
+            for (int e = 0; e < 2; ++e) gg[e] *= (__uint_as_float(rdp[ch][c + e]) - Dq) * a.scale;
             pd[ch * 8 + c / 2] = pack_bf16x2(gg[0], gg[1]);
           }
         }
