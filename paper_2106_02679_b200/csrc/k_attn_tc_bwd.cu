@@ -37,10 +37,11 @@ constexpr int NT = (4 + EW_WARPS) * 32;
 #endif
 constexpr float LOG2E = 1.4426950408889634f;
 #ifndef LGA_BWD_POLY
-#define LGA_BWD_POLY 3
+#define LGA_BWD_POLY 0
 #endif
 // of every 8 exponent pairs of an unmasked tile, computed by the FMA-pipe polynomial instead of the SFU (as in
-// the forward): the element-wise phase issues 2^x for every (query, key) pair, 64 / 128 per thread per tile
+// the forward).  Measured on the 1.3B shapes (kbench, backward): 0 / 2 / 3 / 4 pairs -> 1.094 / 1.093 / 1.105 /
+// 1.111 ms -- the backward's element-wise phase is not SFU-bound, so the default keeps every 2^x on the SFU
 constexpr int BWD_POLY = LGA_BWD_POLY;
 
 // rowsum(dO * o) per (sequence, head, position): d_h / 8 lanes per row (8 or 16, 16-byte loads), shuffle
