@@ -206,19 +206,19 @@ static int lnf_grid(int rows) { return std::max(1, std::min((rows + LNF_ROWS - 1
 
 // EXTRA: also the column sums of resid and of dx (partial rows 2 and 3 of each block's 4 d floats): the bias
 // gradients that are column sums of this kernel's input / output (pre-LN LN2: db2 = sum dY, db_o = sum dh1).
-template <int CPL, bool EXTRA>
-__global__ void __launch_bounds__(256, 2) ln_bwd_fused(const float* __restrict__ dout, const float* __restrict__ x,
+template <int CPL, bool EXTRA, int NW = 8>
+__global__ void __launch_bounds__(NW * 32, 2) ln_bwd_fused(const float* __restrict__ dout, const float* __restrict__ x,
                                                     const float2* __restrict__ stats, const void* gamma, DT pdt,
                                                     const float* __restrict__ resid, float* __restrict__ dx,
                                                     void* dx_e, DT edt, float* __restrict__ partial, int rows, int d) {
-  __shared__ float2 red[LNF_ROWS][8];
+  __shared__ float2 red[LNF_ROWS][NW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = warp * (32 * CPL) + lane * CPL;
   float g[CPL];
   // column accumulators: dgamma, dbeta (+ EXTRA: sum resid, sum dx).  In registers without EXTRA; with it all
   // four live in shared memory ([k][thread]: conflict-free) -- registers are full at CPL = 8 and would spill
   float dg_r[EXTRA ? 1 : CPL], db_r[EXTRA ? 1 : CPL];
-  __shared__ float acc_x[EXTRA ? 4 * CPL : 1][EXTRA ? 256 : 1];
+  __shared__ float acc_x[EXTRA ? 4 * CPL : 1][EXTRA ? NW * 32 : 1];
   auto acc = [&](int which, int k) -> float& {   // which: 0 dgamma, 1 dbeta, 2 sum resid, 3 sum dx
     if (EXTRA) return acc_x[which * CPL + k][threadIdx.x];
     return which == 0 ? dg_r[EXTRA ? 0 : k] : db_r[EXTRA ? 0 : k];
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_fused(const float* __restrict__
     for (int rr = 0; rr < LNF_ROWS; ++rr) {
       float a = 0.f, b = 0.f;
 #pragma unroll
-      for (int w = 0; w < 8; ++w) a += red[rr][w].x, b += red[rr][w].y;   // fixed warp order
+      for (int w = 0; w < NW; ++w) a += red[rr][w].x, b += red[rr][w].y;   // fixed warp order
       m1[rr] = a * inv_d;
       m2[rr] = b * sr[rr].y * inv_d;
     }
@@ -316,7 +316,8 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_fused(const float* __restrict__
 #ifdef LGA_NO_LN_FUSED
 static bool lnf_ok(int) { return false; }
 #else
-static bool lnf_ok(int d) { return d == 1024 || d == 2048; }   // d = 4096 would spill at 2 blocks / SM
+// d = 768 (6 warps x 4 columns), 1024 (8 x 4), 2048 (8 x 8); d = 4096 would spill at 2 blocks / SM
+static bool lnf_ok(int d) { return d == 768 || d == 1024 || d == 2048; }
 #endif
 
 // =============================================================== backward: dgamma / dbeta column partials
@@ -359,9 +360,10 @@ int ln_bwd(const float* dout, const float* x, const float2* stats, const void* g
   if (rows <= 0) return 0;
   if (lnf_ok(d)) {
     const int grid = lnf_grid(rows);
-#define LFU(C, X) note_launch(), ln_bwd_fused<C, X><<<grid, 256, 0, st>>>(dout, x, stats, gamma, pdt, resid, dx, dx_e, edt, partial, rows, d)
-    if (d == 1024) { if (extra) LFU(4, true); else LFU(4, false); }
-    else { if (extra) LFU(8, true); else LFU(8, false); }
+#define LFU(C, X, W) note_launch(), ln_bwd_fused<C, X, W><<<grid, (W) * 32, 0, st>>>(dout, x, stats, gamma, pdt, resid, dx, dx_e, edt, partial, rows, d)
+    if (d == 768) { if (extra) LFU(4, true, 6); else LFU(4, false, 6); }
+    else if (d == 1024) { if (extra) LFU(4, true, 8); else LFU(4, false, 8); }
+    else { if (extra) LFU(8, true, 8); else LFU(8, false, 8); }
 #undef LFU
     return grid;
   }
@@ -413,6 +415,34 @@ __global__ void __launch_bounds__(256) colsum_finish_kernel(const float* __restr
     if (acc_in) t += acc_in[c];
     st_elem(out, c, out_dt, t);
   }
+}
+
+// Several finishes over the same partial rows in ONE launch (blockIdx.y = output): the LayerNorm backward's
+// dgamma / dbeta (+ the two bias sums) -- same fixed order as colsum_finish_kernel, so the same bits.
+__global__ void __launch_bounds__(256) colsum_finish_multi_kernel(const float* __restrict__ partial, int nblk,
+                                                                  int64_t pstride, int n, FinishSet fs) {
+  __shared__ float red[8][33];
+  const FinishOut& o = fs.o[blockIdx.y];
+  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
+  const float* p = partial + o.col0;
+  float s = 0.f;
+  if (c < n)
+    for (int k = g; k < nblk; k += 8) s += p[(int64_t)k * pstride + c];
+  red[g][cl] = s;
+  __syncthreads();
+  if (g == 0 && c < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i][cl];
+    if (o.acc_in) t += o.acc_in[c];
+    st_elem(o.out, c, o.out_dt, t);
+  }
+}
+
+void colsum_finish_multi(const float* partial, int nblk, int64_t pstride, int n, const FinishSet& fs, cudaStream_t st) {
+  if (n <= 0 || fs.k <= 0) return;
+  note_launch(), colsum_finish_multi_kernel<<<dim3((n + 31) / 32, fs.k), 256, 0, st>>>(partial, nblk, pstride, n, fs);
 }
 
 void colsum_finish(const float* partial, int nblk, int64_t pstride, int n, const float* acc_in, void* out, DT out_dt,

@@ -103,6 +103,18 @@ int colsum_blocks(int rows);
 //   acc_in == nullptr: out[n] = v ; else out[n] = acc_in[n] + v ;  out stored as out_dt.
 void colsum_finish(const float* partial, int nblk, int64_t pstride, int n, const float* acc_in,
                    void* out, DT out_dt, cudaStream_t st);
+// up to 4 finishes over the same partial rows in one launch: output i sums columns col0 .. col0 + n - 1
+struct FinishOut {
+  const float* acc_in = nullptr;
+  void* out = nullptr;
+  DT out_dt = DT::F32;
+  int64_t col0 = 0;
+};
+struct FinishSet {
+  FinishOut o[4];
+  int k = 0;
+};
+void colsum_finish_multi(const float* partial, int nblk, int64_t pstride, int n, const FinishSet& fs, cudaStream_t st);
 
 // ------------------------------------------------------------------ loss
 // dY = (y - T) / numel_mb; sumsq partial per block (double).  n = total elements.

@@ -757,10 +757,12 @@ static void layer_bwd(lga_handle* h, const Ws& w, const void* W, const float* x_
                             h->partial, T, d, st, /*extra=*/true);
     KCHECK();
     const int64_t o4[4] = {c.o_ln2w, c.o_ln2b, c.o_b2, c.o_bo};
+    FinishSet fs;
     for (int k = 0; k < 4; ++k) {
       GradDst gd = dst(o4[k]);
-      colsum_finish(h->partial + k * d, nblk, 4LL * d, d, gd.acc_in, gd.out, gd.out_dt, st);
+      fs.o[fs.k++] = FinishOut{gd.acc_in, gd.out, gd.out_dt, (int64_t)k * d};
     }
+    colsum_finish_multi(h->partial, nblk, 4LL * d, d, fs, st);
     KCHECK();
   }
   const void* dh1e = c.bf16 ? (const void*)h->dh1e : (const void*)h->dh1;
@@ -791,8 +793,10 @@ static void layer_bwd(lga_handle* h, const Ws& w, const void* W, const float* x_
                             T, d, st);
     KCHECK();
     GradDst gw = dst(c.o_ln1w), gbias = dst(c.o_ln1b);
-    colsum_finish(h->partial, nblk, 2LL * d, d, gw.acc_in, gw.out, gw.out_dt, st);
-    colsum_finish(h->partial + d, nblk, 2LL * d, d, gbias.acc_in, gbias.out, gbias.out_dt, st);
+    FinishSet fs;
+    fs.o[fs.k++] = FinishOut{gw.acc_in, gw.out, gw.out_dt, 0};
+    fs.o[fs.k++] = FinishOut{gbias.acc_in, gbias.out, gbias.out_dt, (int64_t)d};
+    colsum_finish_multi(h->partial, nblk, 2LL * d, d, fs, st);
     KCHECK();
   }
 }
@@ -814,11 +818,13 @@ static void layer_bwd_post(lga_handle* h, const Ws& w, const void* W, const floa
                             h->partial, T, d, st, /*extra=*/true);
     KCHECK();
     const int64_t o4[4] = {ow, ob, -1, osum};
+    FinishSet fs;
     for (int k = 0; k < 4; ++k) {
       if (o4[k] < 0) continue;
       GradDst gd = dst(o4[k]);
-      colsum_finish(h->partial + k * d, nblk, 4LL * d, d, gd.acc_in, gd.out, gd.out_dt, st);
+      fs.o[fs.k++] = FinishOut{gd.acc_in, gd.out, gd.out_dt, (int64_t)k * d};
     }
+    colsum_finish_multi(h->partial, nblk, 4LL * d, d, fs, st);
     KCHECK();
   };
   const void* dse = c.bf16 ? (const void*)h->dh1e : (const void*)h->dh1;   // ds2, then ds1, as GEMM operand

@@ -107,8 +107,10 @@ extern "C" int lgatest_ln_bwd(const float* dout, const float* x, const float* st
                           partial, rows, d, st, extra);
   const int64_t ps = (extra ? 4LL : 2LL) * d;
   float* outs[4] = {dgamma, dbeta, sum_resid, sum_dx};
+  FinishSet fs;   // one multi-output finish launch, as the step does
   for (int k = 0; k < (extra ? 4 : 2); ++k)
-    if (outs[k]) colsum_finish(partial + k * d, nblk, ps, d, nullptr, outs[k], DT::F32, st);
+    if (outs[k]) fs.o[fs.k++] = FinishOut{nullptr, outs[k], DT::F32, (int64_t)k * d};
+  colsum_finish_multi(partial, nblk, ps, d, fs, st);
   return (int)cudaGetLastError();
 }
 
