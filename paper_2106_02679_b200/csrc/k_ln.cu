@@ -201,13 +201,23 @@ __global__ void __launch_bounds__(256) ln_bwd_block(const float* __restrict__ do
 // registers, reduces each row's two sums across the 8 warps in a fixed order through shared memory, writes
 // dx, and accumulates dgamma / dbeta for its columns in registers -- one partial per block (fixed grid,
 // fixed row order: bitwise reproducible).
-constexpr int LNF_ROWS = 4;
-static int lnf_grid(int rows) { return std::max(1, std::min((rows + LNF_ROWS - 1) / LNF_ROWS, num_sms() * 2)); }
+// rows held in registers per group and resident blocks per SM (measured at the 1.3B shape, d = 2048, fused
+// backward with the 4 column sums: 4 rows x 2 blocks 0.232 ms, 2 x 3 0.223 ms (5.41 TB/s), 2 x 4 and 3 x 3 spill)
+#ifndef LGA_LNF_ROWS
+#define LGA_LNF_ROWS 2
+#endif
+#ifndef LGA_LNF_MINB
+#define LGA_LNF_MINB 3
+#endif
+constexpr int LNF_ROWS = LGA_LNF_ROWS;
+static int lnf_grid(int rows) {
+  return std::max(1, std::min((rows + LNF_ROWS - 1) / LNF_ROWS, num_sms() * LGA_LNF_MINB));
+}
 
 // EXTRA: also the column sums of resid and of dx (partial rows 2 and 3 of each block's 4 d floats): the bias
 // gradients that are column sums of this kernel's input / output (pre-LN LN2: db2 = sum dY, db_o = sum dh1).
 template <int CPL, bool EXTRA, int NW = 8>
-__global__ void __launch_bounds__(NW * 32, 2) ln_bwd_fused(const float* __restrict__ dout, const float* __restrict__ x,
+__global__ void __launch_bounds__(NW * 32, LGA_LNF_MINB) ln_bwd_fused(const float* __restrict__ dout, const float* __restrict__ x,
                                                     const float2* __restrict__ stats, const void* gamma, DT pdt,
                                                     const float* __restrict__ resid, float* __restrict__ dx,
                                                     void* dx_e, DT edt, float* __restrict__ partial, int rows, int d) {
@@ -215,14 +225,11 @@ __global__ void __launch_bounds__(NW * 32, 2) ln_bwd_fused(const float* __restri
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = warp * (32 * CPL) + lane * CPL;
   float g[CPL];
-  // column accumulators: dgamma, dbeta (+ EXTRA: sum resid, sum dx).  In registers without EXTRA; with it all
-  // four live in shared memory ([k][thread]: conflict-free) -- registers are full at CPL = 8 and would spill
-  float dg_r[EXTRA ? 1 : CPL], db_r[EXTRA ? 1 : CPL];
-  __shared__ float acc_x[EXTRA ? 4 * CPL : 1][EXTRA ? NW * 32 : 1];
-  auto acc = [&](int which, int k) -> float& {   // which: 0 dgamma, 1 dbeta, 2 sum resid, 3 sum dx
-    if (EXTRA) return acc_x[which * CPL + k][threadIdx.x];
-    return which == 0 ? dg_r[EXTRA ? 0 : k] : db_r[EXTRA ? 0 : k];
-  };
+  // column accumulators: dgamma, dbeta (+ EXTRA: sum resid, sum dx), in shared memory ([k][thread]:
+  // conflict-free): registers hold the row group, and 3 resident blocks per SM need <= 80 registers
+  constexpr int NACC = EXTRA ? 4 : 2;
+  __shared__ float acc_x[NACC * CPL][NW * 32];
+  auto acc = [&](int which, int k) -> float& { return acc_x[which * CPL + k][threadIdx.x]; };
 #pragma unroll
   for (int k = 0; k < CPL; k += 4) {
     const float4 t = ld4(gamma, pdt, c0 + k);
@@ -303,7 +310,7 @@ __global__ void __launch_bounds__(NW * 32, 2) ln_bwd_fused(const float* __restri
       }
     }
   }
-  constexpr int NP = EXTRA ? 4 : 2;   // partial rows per block
+  constexpr int NP = NACC;   // partial rows per block
   float* pg = partial + (int64_t)blockIdx.x * NP * d + c0;
 #pragma unroll
   for (int k = 0; k < CPL; k += 4) {

@@ -94,6 +94,33 @@ def gemm(args):
         print(f"gemm {name} M={M} N={N} K={K} {kind:12s}: {ms:.3f} ms  {2.0 * M * N * K / ms / 1e9:.1f} TFLOP/s")
 
 
+def ln(args):
+    """LayerNorm forward / fused backward (with the 4 column sums) at the step's shape: DRAM GB/s."""
+    T, d = args.tokens, args.d
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    VP, I = C.c_void_p, C.c_int
+    L.lgatest_ln_fwd.argtypes = [VP, VP, VP, I, VP, I, VP, I, I, C.c_float, VP]
+    L.lgatest_ln_bwd.argtypes = [VP, VP, VP, VP, I, VP, VP, VP, I, VP, VP, VP, VP, VP, I, I, VP]
+    L.lgatest_ln_bwd_partial_floats.restype = C.c_int64
+    x = torch.randn(T, d, device="cuda")
+    g = torch.ones(d, device="cuda").bfloat16()
+    b = torch.zeros(d, device="cuda").bfloat16()
+    y = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
+    stats = torch.empty(T, 2, device="cuda")
+    fwd = lambda: L.lgatest_ln_fwd(P(x), P(g), P(b), 1, P(y), 1, P(stats), T, d, 1e-5, st)
+    ms = timeit(fwd)
+    print(f"ln fwd      T={T} d={d}: {ms:.3f} ms  {T * d * (4 + 2) / ms / 1e6:.0f} GB/s")
+    dout, res = torch.randn(T, d, device="cuda"), torch.randn(T, d, device="cuda")
+    dx = torch.empty(T, d, device="cuda")
+    dxe = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
+    v = [torch.empty(d, device="cuda") for _ in range(4)]
+    part = torch.empty(2 * int(L.lgatest_ln_bwd_partial_floats(T, d)), device="cuda")
+    bwd = lambda: L.lgatest_ln_bwd(P(dout), P(x), P(stats), P(g), 1, P(res), P(dx), P(dxe), 1, P(v[0]), P(v[1]), P(v[2]),
+                                   P(v[3]), P(part), T, d, st)
+    ms = timeit(bwd)
+    print(f"ln bwd+sums T={T} d={d}: {ms:.3f} ms  {T * d * (3 * 4 + 4 + 2) / ms / 1e6:.0f} GB/s")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("what", nargs="*", default=["attn", "gemm"])
@@ -108,3 +135,5 @@ if __name__ == "__main__":
         attn(a)
     if "gemm" in a.what:
         gemm(a)
+    if "ln" in a.what:
+        ln(a)
