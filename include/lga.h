@@ -257,6 +257,17 @@ lga_status lga_grads(lga_handle* h, float* out, uint64_t n, int32_t out_on_devic
 /* Current fp32 master parameters, same layout / size rules as lga_grads. */
 lga_status lga_params(lga_handle* h, float* out, uint64_t n, int32_t out_on_device);
 
+/* Checkpoint / resume of this rank's training state: a small header (configuration, rank, AdamW step t)
+ * followed by the fp32 master shard, Adam m and v of its stage's layers ([3][L/P][S] floats, S = padded
+ * layer / D, or the whole padded layer with LGA_FLAG_UNPARTITIONED).  lga_state_bytes gives the size;
+ * lga_save_state copies the state into `host_out` after the last step completed; lga_load_state restores it
+ * into a handle of the same configuration and rank (INVALID_ARG otherwise), refreshes the 16-bit parameter
+ * shard and sets t, so the next lga_step continues the run bit for bit (SIZE_MISMATCH if `bytes` differs).
+ * Not collective; every rank saves / loads its own shard between the same two steps. */
+lga_status lga_state_bytes(const lga_handle* h, uint64_t* bytes);
+lga_status lga_save_state(lga_handle* h, void* host_out, uint64_t bytes);
+lga_status lga_load_state(lga_handle* h, const void* host_in, uint64_t bytes);
+
 /* Counters for the last step and the running total (either may be NULL).  Host only. */
 lga_status lga_comm_bytes(const lga_handle* h, lga_comm_stats* last_step, lga_comm_stats* total);
 

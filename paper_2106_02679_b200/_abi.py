@@ -108,6 +108,9 @@ def lib():
         "lga_params": (C.c_int, [H, C.c_void_p, C.c_uint64, C.c_int32]),
         "lga_comm_bytes": (C.c_int, [H, C.POINTER(lga_comm_stats), C.POINTER(lga_comm_stats)]),
         "lga_layer_stage": (C.c_int, [H, C.POINTER(C.c_int32), C.c_int32]),
+        "lga_state_bytes": (C.c_int, [H, C.POINTER(C.c_uint64)]),
+        "lga_save_state": (C.c_int, [H, C.c_void_p, C.c_uint64]),
+        "lga_load_state": (C.c_int, [H, C.c_void_p, C.c_uint64]),
         "lga_timing_last": (C.c_int, [H, C.POINTER(lga_timing)]),
         "lga_destroy": (None, [H]),
     }
@@ -128,4 +131,5 @@ def check(status: int):
 
 EXPORTED = ["lga_abi_version", "lga_status_string", "lga_last_error", "lga_param_count", "lga_plan", "lga_nccl_unique_id",
             "lga_init", "lga_step", "lga_step_host", "lga_grads", "lga_params", "lga_comm_bytes", "lga_layer_stage",
+            "lga_state_bytes", "lga_save_state", "lga_load_state",
             "lga_timing_last", "lga_destroy"]

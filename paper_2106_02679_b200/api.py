@@ -178,6 +178,19 @@ class Trainer:
         check(lib().lga_params(self._h, C.c_void_p(out.data_ptr()), out.numel(), 1))
         return out
 
+    def save_state(self) -> bytes:
+        """lga_save_state: this rank's training state (header + fp32 master / m / v shard) as bytes."""
+        n = C.c_uint64()
+        check(lib().lga_state_bytes(self._h, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(lib().lga_save_state(self._h, buf, n.value))
+        return buf.raw
+
+    def load_state(self, state: bytes):
+        """lga_load_state: resume from save_state's bytes (same configuration and rank)."""
+        buf = C.create_string_buffer(state, len(state))
+        check(lib().lga_load_state(self._h, buf, len(state)))
+
     def comm_stats(self):
         last, tot = _abi.lga_comm_stats(), _abi.lga_comm_stats()
         check(lib().lga_comm_bytes(self._h, C.byref(last), C.byref(tot)))

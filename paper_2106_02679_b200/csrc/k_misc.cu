@@ -510,7 +510,10 @@ void world_barrier(unsigned long long* const* wflag, int world, unsigned long lo
 }
 
 // the step counter t (AdamW bias corrections, flag epochs): incremented first thing in every step
-__global__ void step_begin_kernel(long long* tstep) { *tstep += 1; }
+__global__ void step_begin_kernel(long long* tstep) {   // [0] AdamW step, [1] flag epoch
+  tstep[0] += 1;
+  tstep[1] += 1;
+}
 void step_begin(long long* tstep, cudaStream_t st) { note_launch(), step_begin_kernel<<<1, 1, 0, st>>>(tstep); }
 
 static std::atomic<unsigned long long> g_launches{0};

@@ -274,7 +274,8 @@ struct lga_handle {
   unsigned long long *next_flags = nullptr, *prev_flags = nullptr;
   unsigned long long sent_fwd = 0, sent_bwd = 0, recv_fwd = 0, recv_bwd = 0;   // this step's transfers so far
   unsigned long long k_send_fwd = 0, k_send_bwd = 0, k_recv_fwd = 0, k_recv_bwd = 0;   // per step (stage map)
-  long long* tstep = nullptr;   // device step counter t (from 1): AdamW bias corrections, flag epochs
+  long long* tstep = nullptr;   // device AdamW step t (from 1; restored by lga_load_state): bias corrections
+  long long* tepoch = nullptr;  // device count of steps run by this handle: targets of every peer / pipeline flag
   // cross-step event waits are redundant (every step starts after the previous one completed) and illegal
   // inside a stream capture: only wait on events recorded earlier in the same step
   bool rec_adam[2] = {false, false};
@@ -406,7 +407,8 @@ static void plan_arena(lga_handle* h) {
   h->xin = A.take<float>(act);
   h->tin = A.take<float>(act);
   h->flags = A.take<unsigned long long>(8);
-  h->tstep = A.take<long long>(1);
+  h->tstep = A.take<long long>(2);   // [0] AdamW step t, [1] steps run by this handle (flag epochs)
+  h->tepoch = h->tstep ? h->tstep + 1 : nullptr;
   if (h->world > 1) {
     h->wflags = A.take<unsigned long long>(16);
     h->loss_ring = A.take<double>(4 * (int64_t)h->world);
@@ -918,7 +920,7 @@ static void all_gather(lga_handle* h, int j, int slot) {
   if (c.dp_ipc) {
     // every replica's AdamW of layer j of the previous step is done (D (t-1) signals), then pull the D
     // shards over NVLink on the copy engines and tell each owner that its shard j has been read
-    wait_flag(h->dpf + DPF_PARAM * c.Lloc + j, h->tstep, (unsigned long long)c.D, 0ull, h->s_comm);
+    wait_flag(h->dpf + DPF_PARAM * c.Lloc + j, h->tepoch, (unsigned long long)c.D, 0ull, h->s_comm);
     KCHECK();
     const size_t bytes = (size_t)c.S * dt_size(c.E);
     for (int p = 0; p < c.D; ++p)
@@ -980,9 +982,9 @@ static void rs_adam_peer(lga_handle* h, int j) {
   if (!h->comm_off) {
     dp_signal(h->dp_flag_dev, c.D, DPF_GRAD * c.Lloc + j, h->s_comm);
     KCHECK();
-    wait_flag(h->dpf + DPF_GRAD * c.Lloc + j, h->tstep, D, D, h->s_comm);
+    wait_flag(h->dpf + DPF_GRAD * c.Lloc + j, h->tepoch, D, D, h->s_comm);
     KCHECK();
-    wait_flag(h->dpf + DPF_READ * c.Lloc + j, h->tstep, R * D, R * D, h->s_comm);
+    wait_flag(h->dpf + DPF_READ * c.Lloc + j, h->tepoch, R * D, R * D, h->s_comm);
     KCHECK();
   }
   const float gscale = 1.0f / ((float)c.D * (float)c.N);   // gradient of the mean loss (A-3)
@@ -1023,14 +1025,14 @@ static void allreduce_adam_peer(lga_handle* h, int j) {
     const unsigned long long D = (unsigned long long)c.D;
     dp_signal(h->dp_flag_dev, c.D, DPF_GRAD * c.Lloc + j, h->s_comm);
     KCHECK();
-    wait_flag(h->dpf + DPF_GRAD * c.Lloc + j, h->tstep, D, D, h->s_comm);
+    wait_flag(h->dpf + DPF_GRAD * c.Lloc + j, h->tepoch, D, D, h->s_comm);
     KCHECK();
     const int64_t goff = (int64_t)j * c.plpad + (int64_t)h->replica * Sr;
     peer_reduce(h->dp_gst_dev, goff, c.D, c.G, nullptr, false, eoff(gs, c.G, (int64_t)h->replica * Sr), Sr, h->s_comm);
     KCHECK();
     dp_signal(h->dp_flag_dev, c.D, DPF_RED * c.Lloc + j, h->s_comm);
     KCHECK();
-    wait_flag(h->dpf + DPF_RED * c.Lloc + j, h->tstep, D, D, h->s_comm);
+    wait_flag(h->dpf + DPF_RED * c.Lloc + j, h->tepoch, D, D, h->s_comm);
     KCHECK();
     for (int p = 0; p < c.D; ++p) {
       if (p == h->replica) continue;
@@ -1058,7 +1060,7 @@ static void rs_acc_peer(lga_handle* h, int j, int m) {
   if (!h->comm_off) {
     dp_signal(h->dp_flag_dev, c.D, DPF_GRAD * c.Lloc + j, h->s_comm);
     KCHECK();
-    wait_flag(h->dpf + DPF_GRAD * c.Lloc + j, h->tstep, D * N, D * (unsigned long long)(m + 1), h->s_comm);
+    wait_flag(h->dpf + DPF_GRAD * c.Lloc + j, h->tepoch, D * N, D * (unsigned long long)(m + 1), h->s_comm);
     KCHECK();
     peer_reduce(h->dp_gst_dev, (int64_t)j * c.plpad + (int64_t)h->replica * c.S, c.D, c.G, acc, m == 0, nullptr, c.S,
                 h->s_comm);
@@ -1071,7 +1073,7 @@ static void rs_acc_peer(lga_handle* h, int j, int m) {
   }
   if (m == c.N - 1) {
     if (!h->comm_off) {
-      wait_flag(h->dpf + DPF_READ * c.Lloc + j, h->tstep, 2 * N * D, 2 * N * D, h->s_comm);
+      wait_flag(h->dpf + DPF_READ * c.Lloc + j, h->tepoch, 2 * N * D, 2 * N * D, h->s_comm);
       KCHECK();
     }
     adam_layer(h, j, acc, DT::F32);
@@ -1167,7 +1169,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
           h->last.p2p_recv_bytes += (uint64_t)cw * mb * 4;
           if (!h->comm_off) {
             count_wait(h, nullptr, 1);
-            wait_flag(h->flags + 0, h->tstep, h->k_recv_fwd, h->recv_fwd, h->s_comp);
+            wait_flag(h->flags + 0, h->tepoch, h->k_recv_fwd, h->recv_fwd, h->s_comp);
             KCHECK();
             count_wait_end(h);
           }
@@ -1189,7 +1191,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
         h->last.p2p_send_calls += cw;
         h->last.p2p_send_bytes += (uint64_t)cw * mb * 4;
         if (!h->comm_off) {
-          set_flag(h->next_flags + 0, h->tstep, h->k_send_fwd, h->sent_fwd, h->s_comp);
+          set_flag(h->next_flags + 0, h->tepoch, h->k_send_fwd, h->sent_fwd, h->s_comp);
           KCHECK();
         }
       }
@@ -1233,7 +1235,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
     }
     if (c.dp_ipc && c.unpart && !h->comm_off) {   // every replica read last step's reduced slices of staging j
       count_wait(h, nullptr, 0);
-      wait_flag(h->dpf + DPF_READ * c.Lloc + j, h->tstep, (unsigned long long)c.D, 0ull, h->s_comp);
+      wait_flag(h->dpf + DPF_READ * c.Lloc + j, h->tepoch, (unsigned long long)c.D, 0ull, h->s_comp);
       KCHECK();
       count_wait_end(h);
     }
@@ -1254,7 +1256,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
         h->last.p2p_recv_bytes += (uint64_t)c.c * mb * 4;
         if (!h->comm_off) {
           count_wait(h, nullptr, 1);
-          wait_flag(h->flags + 1, h->tstep, h->k_recv_bwd, h->recv_bwd, h->s_comp);
+          wait_flag(h->flags + 1, h->tepoch, h->k_recv_bwd, h->recv_bwd, h->s_comp);
           KCHECK();
           count_wait_end(h);
         }
@@ -1275,7 +1277,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
         h->last.p2p_send_calls += c.c;
         h->last.p2p_send_bytes += (uint64_t)c.c * mb * 4;
         if (!h->comm_off) {
-          set_flag(h->prev_flags + 1, h->tstep, h->k_send_bwd, h->sent_bwd, h->s_comp);
+          set_flag(h->prev_flags + 1, h->tepoch, h->k_send_bwd, h->sent_bwd, h->s_comp);
           KCHECK();
         }
       }
@@ -1352,7 +1354,7 @@ static void step_standard(lga_handle* h, const float* x, const float* T) {
       }
       if (c.dp_ipc && !h->comm_off) {   // every replica read its slice of the previous micro-batch's staging j
         count_wait(h, nullptr, 0);
-        wait_flag(h->dpf + DPF_GREAD * c.Lloc + j, h->tstep, (unsigned long long)c.D * c.N, (unsigned long long)c.D * m,
+        wait_flag(h->dpf + DPF_GREAD * c.Lloc + j, h->tepoch, (unsigned long long)c.D * c.N, (unsigned long long)c.D * m,
                   h->s_comp);
         KCHECK();
         count_wait_end(h);
@@ -1725,7 +1727,7 @@ static void issue_step(lga_handle* h, const float* x, const float* T, bool host_
   h->x_split = false;
   h->rec_adam[0] = h->rec_adam[1] = false;
   std::fill(h->rec_slot.begin(), h->rec_slot.end(), 0);
-  step_begin(h->tstep, h->s_comp);   // t += 1 before anything reads it
+  step_begin(h->tstep, h->s_comp);   // t += 1 and epoch += 1 before anything reads them
   KCHECK();
   CK(cudaEventRecord(h->ev_in, h->s_comp));
   CK(cudaStreamWaitEvent(h->s_comm, h->ev_in, 0));
@@ -1766,7 +1768,7 @@ static void issue_step(lga_handle* h, const float* x, const float* T, bool host_
   h->last.allreduce_calls += 1;   // the loss (plus, unpartitioned, the per-layer gradient all-reduces)
   if (h->world > 1 && !h->comm_off) {   // over peer memory (every rank gets the same rank-order sum)
     count_wait(h, nullptr, 0);          // the kernel waits for the peers' losses: an exposed wait
-    loss_allreduce_peer(h->loss_dev, h->w_loss_dev, h->w_flag_dev, h->rank, h->world, h->tstep, h->wflags + 0,
+    loss_allreduce_peer(h->loss_dev, h->w_loss_dev, h->w_flag_dev, h->rank, h->world, h->tepoch, h->wflags + 0,
                         h->loss_ring, h->s_comp);
     KCHECK();
     count_wait_end(h);
@@ -1956,6 +1958,92 @@ lga_status lga_grads(lga_handle* h, float* out, uint64_t n, int32_t out_on_devic
 lga_status lga_params(lga_handle* h, float* out, uint64_t n, int32_t out_on_device) {
   return gather_state(h, h ? h->master : nullptr, h && h->connected ? h->peers[h->rank].off_master : 0, out, n,
                       out_on_device);
+}
+
+// ------------------------------------------------------------------ checkpoint / resume of the training state
+struct StateHeader {
+  uint64_t magic;    // "LGASTATE"
+  uint32_t abi, rank;
+  int32_t L, d, D, P, Lloc, precision;
+  int64_t S, t;
+  uint64_t flags;
+};
+static constexpr uint64_t kStateMagic = 0x4554415453414c47ull;   // little-endian "LGASTATE"
+
+lga_status lga_state_bytes(const lga_handle* h, uint64_t* bytes) {
+  if (!h || !bytes) return ERR(LGA_ERR_INVALID_ARG, "NULL argument");
+  *bytes = sizeof(StateHeader) + 3ull * h->c.Lloc * h->c.S * sizeof(float);
+  return LGA_OK;
+}
+
+static void fill_header(const lga_handle* h, StateHeader* hd, int64_t t) {
+  const Cfg& c = h->c;
+  *hd = StateHeader{};
+  hd->magic = kStateMagic;
+  hd->abi = LGA_ABI_VERSION;
+  hd->rank = (uint32_t)h->rank;
+  hd->L = c.L; hd->d = c.d; hd->D = c.D; hd->P = c.P; hd->Lloc = c.Lloc; hd->precision = c.bf16 ? 1 : 0;
+  hd->S = c.S;
+  hd->t = t;
+  hd->flags = (c.unpart ? 1u : 0u) | (c.contig ? 2u : 0u);
+}
+
+lga_status lga_save_state(lga_handle* h, void* host_out, uint64_t bytes) {
+  if (!h || !host_out) return ERR(LGA_ERR_INVALID_ARG, "NULL argument");
+  if (h->bad) return ERR(LGA_ERR_BAD_STATE, "handle latched");
+  uint64_t need = 0;
+  lga_state_bytes(h, &need);
+  if (bytes != need) return ERR(LGA_ERR_SIZE_MISMATCH, "bytes = %llu, expected %llu", (unsigned long long)bytes,
+                                (unsigned long long)need);
+  ABI_TRY
+  CK(cudaSetDevice(h->dev));
+  if (h->stepped) CK(cudaEventSynchronize(h->ev_t1));
+  CK(cudaStreamSynchronize(h->s_comp));
+  CK(cudaStreamSynchronize(h->s_comm));
+  StateHeader hd;
+  fill_header(h, &hd, h->t);
+  char* out = static_cast<char*>(host_out);
+  memcpy(out, &hd, sizeof(hd));
+  const size_t n = (size_t)h->c.Lloc * h->c.S * sizeof(float);
+  CK(cudaMemcpy(out + sizeof(hd), h->master, n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out + sizeof(hd) + n, h->mom, n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out + sizeof(hd) + 2 * n, h->var, n, cudaMemcpyDeviceToHost));
+  return LGA_OK;
+  ABI_CATCH
+}
+
+lga_status lga_load_state(lga_handle* h, const void* host_in, uint64_t bytes) {
+  if (!h || !host_in) return ERR(LGA_ERR_INVALID_ARG, "NULL argument");
+  if (h->bad) return ERR(LGA_ERR_BAD_STATE, "handle latched");
+  uint64_t need = 0;
+  lga_state_bytes(h, &need);
+  if (bytes != need) return ERR(LGA_ERR_SIZE_MISMATCH, "bytes = %llu, expected %llu", (unsigned long long)bytes,
+                                (unsigned long long)need);
+  StateHeader hd, mine;
+  memcpy(&hd, host_in, sizeof(hd));
+  fill_header(h, &mine, hd.t);
+  if (memcmp(&hd, &mine, sizeof(hd)) != 0 || hd.t < 0)
+    return ERR(LGA_ERR_INVALID_ARG, "state of another configuration or rank (L %d d %d D %d P %d rank %u)", hd.L, hd.d,
+               hd.D, hd.P, hd.rank);
+  ABI_TRY
+  CK(cudaSetDevice(h->dev));
+  if (h->stepped) CK(cudaEventSynchronize(h->ev_t1));
+  CK(cudaStreamSynchronize(h->s_comp));
+  CK(cudaStreamSynchronize(h->s_comm));
+  const char* in = static_cast<const char*>(host_in);
+  const size_t n = (size_t)h->c.Lloc * h->c.S * sizeof(float);
+  CK(cudaMemcpy(h->master, in + sizeof(hd), n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->mom, in + sizeof(hd) + n, n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->var, in + sizeof(hd) + 2 * n, n, cudaMemcpyHostToDevice));
+  // the 16-bit parameter shard the next all-gather reads, and the AdamW step (flag epochs stay this handle's)
+  cast_f32(h->master, h->pshard, h->c.E, (int64_t)h->c.Lloc * h->c.S, h->s_comp);
+  KCHECK();
+  const long long t = hd.t;
+  CK(cudaMemcpyAsync(h->tstep, &t, sizeof(t), cudaMemcpyHostToDevice, h->s_comp));
+  CK(cudaStreamSynchronize(h->s_comp));
+  h->t = t;
+  return LGA_OK;
+  ABI_CATCH
 }
 
 lga_status lga_comm_bytes(const lga_handle* h, lga_comm_stats* last_step, lga_comm_stats* total) {

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--flags", type=int, default=0)   # LGA_FLAG_* variants
+    ap.add_argument("--resume-at", type=int, default=0)   # save the state after this many steps, resume in a new handle
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -40,6 +41,11 @@ def main():
     tr = Trainer(cfg, rank=rank, world=world, device=local, init_params=init)
     losses = []
     for k in range(a.steps):
+        if a.resume_at and k == a.resume_at:   # checkpoint / resume: a fresh handle continues from the saved state
+            state = tr.save_state()
+            tr.close()
+            tr = Trainer(cfg, rank=rank, world=world, device=local, init_params=init)
+            tr.load_state(state)
         X, T = synth.batch(sh, step=k)
         r = tr.replica
         x = torch.from_numpy(X[r]).cuda()

@@ -263,3 +263,37 @@ def test_step_host_equals_step(precision):
         tr.close()
     assert np.array_equal(outs[0][0], outs[1][0])
     assert outs[0][1] == outs[1][1] and outs[0][2] == outs[1][2]
+
+
+@pytest.mark.parametrize("precision", [LGA_FP32, LGA_BF16])
+def test_checkpoint_resume_is_bitwise(precision):
+    """lga_save_state after step 2, a fresh handle, lga_load_state, step 3: the same parameters and loss bit for bit
+    as three uninterrupted steps (the AdamW step t travels with the state; flag epochs stay per handle); a state
+    of another configuration is refused."""
+    sh = C1 if precision == LGA_FP32 else synth.Shape(layers=2, d=256, heads=2, seq=128, micro_batch=1, n_micro=4)
+    init = synth.init_params(sh, style="parity")
+    cfg = Config(layers=sh.layers, d_model=sh.d, heads=sh.heads, seq_len=sh.seq, micro_batch=sh.micro_batch,
+                 n_micro=sh.n_micro, precision=precision, lr=1e-3, weight_decay=0.1, retain_grads=1)
+    batches = [synth.batch(sh, step=k) for k in range(3)]
+    dev = [(torch.from_numpy(X[0]).cuda(), torch.from_numpy(T[0]).cuda()) for X, T in batches]
+    a = Trainer(cfg, rank=0, world=1, device=0, init_params=init)
+    la = [a.step(x, t) for x, t in dev]
+    pa = a.params()
+    a.close()
+    b = Trainer(cfg, rank=0, world=1, device=0, init_params=init)
+    lb = [b.step(x, t) for x, t in dev[:2]]
+    state = b.save_state()
+    b.close()
+    other = synth.init_params(sh, seed=99, style="parity")   # the loaded state must win over the init
+    c = Trainer(cfg, rank=0, world=1, device=0, init_params=other)
+    c.load_state(state)
+    lb.append(c.step(*dev[2]))
+    pc = c.params()
+    c.close()
+    assert lb == la and np.array_equal(pa, pc)
+    from paper_2106_02679_b200._abi import LgaError
+    cfg2 = Config(**{**cfg.__dict__, "layers": sh.layers * 2})
+    d2 = Trainer(cfg2, rank=0, world=1, device=0, init_params=np.concatenate([init, init]))
+    with pytest.raises(LgaError):
+        d2.load_state(state)
+    d2.close()
