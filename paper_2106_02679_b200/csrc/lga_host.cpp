@@ -14,6 +14,7 @@
 #include "kernels.cuh"
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -503,6 +504,30 @@ static bool trace_on() {
   }
   return t == 1;
 }
+// NVTX ranges (env LGA_NVTX=1): "lga step t", "fwd layer i", "bwd layer i" around the host-side issue of each
+// pass, so that ncu --nvtx-include / an NVTX-aware profiler can select one layer's kernels (eager steps; a
+// replayed graph launches under the "lga step" range only)
+static bool nvtx_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LGA_NVTX");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+struct NvtxRange {
+  bool on;
+  NvtxRange(const char* what, long long idx) : on(nvtx_on()) {
+    if (!on) return;
+    char buf[64];
+    snprintf(buf, sizeof(buf), "%s %lld", what, idx);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() {
+    if (on) nvtxRangePop();
+  }
+};
+
 static void trace(lga_handle* h, const char* what, int64_t layer) {
   if (!trace_on()) return;
   fprintf(stderr, "[lga rank %d stage %d] %s layer %lld issued\n", h->rank, h->stage, what, (long long)layer);
@@ -1140,6 +1165,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
   for (int j = 0; j < c.Lloc; ++j, ++agk) {
     const int sl = slot_of(j, agk);
     const int64_t i = local_to_global(h, j);
+    NvtxRange nvtx_layer("fwd layer", i);
     if (dp_gather && j + 1 < c.Lloc) {  // prefetch Restore(next local layer) while computing layer i
       const int sn = slot_of(j + 1, agk + 1);
       if (h->rec_slot[sn]) CK(cudaStreamWaitEvent(h->s_comm, h->ev_slot_free[sn], 0));
@@ -1217,6 +1243,7 @@ static void step_layered(lga_handle* h, const float* x, const float* T) {
     CK(cudaEventRecord(h->ev_ag[agk % 2], h->s_comm));
   }
   for (int j = c.Lloc - 1; j >= 0; --j, ++agk) {
+    NvtxRange nvtx_layer("bwd layer", local_to_global(h, j));
     const int sl = slot_of(j, agk);
     const int64_t i = local_to_global(h, j);
     const int gb = j % 2;
@@ -1828,6 +1855,7 @@ static lga_status run_step(lga_handle* h, const float* x, const float* T, double
   ABI_TRY
   CK(cudaSetDevice(h->dev));
   h->t += 1;
+  NvtxRange nvtx_step("lga step", h->t);
   h->comm_off = c.no_comm && h->t > 1;
   CK(cudaEventRecord(h->ev_t0, h->user));
   // CUDA graph of the whole step: captured at the second device-input call, replayed while the input
