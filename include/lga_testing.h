@@ -36,9 +36,12 @@ int lgatest_gemm_ws(int M, int N, int K, const void* A, int64_t lda, int a_kmajo
 int lgatest_attn_fwd(int path, int nseq, int seq, int heads, int dh, int causal, const void* qkv, void* o, float* lse,
                      uintptr_t stream);
 int lgatest_attn_bwd(int path, int nseq, int seq, int heads, int dh, int causal, const void* qkv, const void* o,
-                     const float* lse, const void* dO, float* dsum, void* dqkv, float* colsum, uintptr_t stream);
+                     const float* lse, const void* dO, float* dsum, void* dqkv, float* colsum, void* ds_ws,
+                     uintptr_t stream);
 /* colsum (path 1, may be NULL): column sums of dqkv per (sequence, 128-row tile, 32-row quadrant),
- * [nseq * ceil(seq/128) * 4][3 d] fp32. */
+ * [nseq * ceil(seq/128) * 4][3 d] fp32.  ds_ws (path 1, may be NULL): dS workspace of
+ * nseq * heads * s128 * s128 bf16 (s128 = seq rounded up to 128) -- dQ from the stored dS (5-matmul backward);
+ * NULL = the dQ kernel that recomputes S and dP (7 matmuls). */
 
 /* LayerNorm forward (reading A-1): y = (x - mu) rstd gamma + beta over rows of d; x fp32, gamma / beta in
  * p_dt, y in y_dt, stats[r] = (mu, rstd) as float2. */

@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int r = qd * 32 + lane;
     const uint32_t lrow = (uint32_t)(qd * 32) << 16;
     const float sl2 = a.scale * LOG2E;
+    const int64_t s128 = (int64_t)nkt * KB;
     int gi = 0;
     for (int t = blockIdx.x; t < n_items; t += gridDim.x) {
       int kt, h, sq, qstart, nq;
@@ -370,6 +371,9 @@ __global__ void __launch_bounds__(NT, 1)
         // valid iff q < s, kj < s and (causal) kj <= q; only tiles touching the diagonal / the end mask
         const bool need_mask = kj >= s || qa + 32 > s || (a.causal && kj > qa);
         const bool any_mask = __any_sync(0xffffffffu, need_mask);   // warp-uniform polynomial choice
+        // dS^T [key][query] of this (sequence, head), rows / columns padded to s128 (a.dsT: dQ from dS, 5 matmuls)
+        __nv_bfloat16* dst_row =
+            a.dsT ? static_cast<__nv_bfloat16*>(a.dsT) + (((int64_t)sq * a.heads + h) * s128 + kj) * s128 : nullptr;
         mbar_wait(&s_full[grp], (g >> 1) & 1);
         fence_after();
         mbar_wait(&q_full[st], (g / NST) & 1);   // lse / dsum of tile g landed with Q / dO
@@ -408,6 +412,11 @@ __global__ void __launch_bounds__(NT, 1)
           // packed columns 32h + 8ch .. +7 lie inside chunk 0's range, already read by this thread
           tmem_st8_nowait(t_st(grp) + lrow + hf * 32 + ch * 8, pp);
           tmem_st8_nowait(t_dpt(grp) + lrow + hf * 32 + ch * 8, pd);
+          if (dst_row) {   // dS^T row segment for the dQ kernel (masked entries are 0): one full 32-byte sector
+            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst_row + qa + ch * 16),
+                         "r"(pd[0]), "r"(pd[1]), "r"(pd[2]), "r"(pd[3]), "r"(pd[4]), "r"(pd[5]), "r"(pd[6]), "r"(pd[7])
+                         : "memory");
+          }
         }
         tmem_wait_st();
         fence_before();
@@ -703,6 +712,152 @@ __global__ void __launch_bounds__(NT, 1)
   }
 }
 
+// =============================================================================== dQ from dS (5-matmul backward)
+// With a dS workspace (AttnArgs::dsT) the dK/dV kernel stores dS^T next to its P^T / dS^T TMEM writes, and dQ is a
+// plain batched, causally blocked GEMM: dQ[q] = sum_key dS[q][key] K[key] -- no second S / dP recompute, no exp.
+// Per item (128-query tile, head, sequence): k-blocks of 64 keys; A = dS^T tile [64 keys][128 queries] read
+// MN-major, B = K rows [64 keys][d_h] read MN-major; fp32 accumulator in TMEM, two stages so the drain of one
+// item overlaps the next item's MMAs; persistent, heaviest tiles first.  Warps: 0 TMA, 1 MMA, 2 TMEM,
+// 4..11 epilogue (two per TMEM lane quadrant, half the columns each).
+constexpr int DQS_STAGES = 6;
+constexpr int DQS_EPI0 = 4, DQS_EPI = 8;
+constexpr int DQS_NT = (DQS_EPI0 + DQS_EPI) * 32;
+
+template <int DH>
+struct DqsSmem {
+  static constexpr int A_BYTES = 128 * 64 * 2;        // two [64 keys][64 queries] sub-tiles
+  static constexpr int B_BYTES = DH * 64 * 2;         // DH/64 [64 keys][64 dh] sub-tiles
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = DQS_STAGES * STAGE;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+  static_assert(TOTAL <= 232448, "shared memory");
+};
+
+template <int DH>
+__global__ void __launch_bounds__(DQS_NT, 1)
+    dq_from_ds_kernel(const __grid_constant__ CUtensorMap tm_ds, const __grid_constant__ CUtensorMap tm_k,
+                      const AttnArgs a) {
+  using SM = DqsSmem<DH>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::BAR_OFF);
+  uint64_t* empty = full + DQS_STAGES;
+  uint64_t* tfull = empty + DQS_STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;           // [2] (epilogue threads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  constexpr int EPI_ALL = DQS_EPI * 32;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = a.seq, d = a.d;
+  const int nqt = (s + QB2 - 1) / QB2;
+  const int s128 = nqt * QB2;
+  const int pairs = a.heads * a.nseq;
+  const int n_items = nqt * pairs;
+  auto item = [&](int t, int& qt, int& h, int& sq, int& nkb) {
+    const int chunk = t / (DQ_G * nqt), w = t % (DQ_G * nqt);
+    const int np = min(DQ_G, pairs - chunk * DQ_G);
+    const int qi = w / np, pair = chunk * DQ_G + w % np;
+    qt = a.causal ? nqt - 1 - qi : qi;
+    h = pair % a.heads;
+    sq = pair / a.heads;
+    const int kend = a.causal ? min(s, qt * QB2 + QB2) : s;
+    nkb = (kend + 63) / 64;   // 64-key blocks
+  };
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < DQS_STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], EPI_ALL); }
+    mbar_fence_init();
+    prefetch_tmap(&tm_ds);
+    prefetch_tmap(&tm_k);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 256);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tb = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ===== TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < n_items; t += gridDim.x) {
+        int qt, h, sq, nkb;
+        item(t, qt, h, sq, nkb);
+        const int row0 = (sq * a.heads + h) * s128;   // this (sequence, head)'s dS^T rows
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * SM::STAGE;
+          uint8_t* sb = sa + SM::A_BYTES;
+          mbar_expect_tx(&full[stage], SM::STAGE);
+#pragma unroll
+          for (int i = 0; i < 2; ++i)   // queries [qt*128 + 64 i, +64) of keys [kb*64, +64)
+            tma_load_2d(sa + i * 64 * 128, &tm_ds, &full[stage], qt * QB2 + 64 * i, row0 + kb * 64);
+#pragma unroll
+          for (int i = 0; i < DH / 64; ++i)   // K[kb*64 .., h*dh + 64 i ..]
+            tma_load_3d(sb + i * 64 * 128, &tm_k, &full[stage], d + h * DH + 64 * i, kb * 64, sq);
+          if (++stage == DQS_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {  // ===== MMA issuer (whole warp, one elected lane)
+    constexpr uint32_t idesc = make_idesc(128, DH, true, true);
+    const bool leader = elect_one();
+    const uint64_t ad0 = make_desc(smem_u32(smem), 64 * 128, 1024);
+    const uint64_t bd0 = make_desc(smem_u32(smem) + SM::A_BYTES, 64 * 128, 1024);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < n_items; t += gridDim.x, ++it) {
+      int qt, h, sq, nkb;
+      item(t, qt, h, sq, nkb);
+      const int as = it & 1;
+      mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
+      fence_after();
+      const uint32_t dtm = tb + as * 128;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        fence_after();
+        const uint64_t ad = desc_add(ad0, stage * SM::STAGE), bd = desc_add(bd0, stage * SM::STAGE);
+        if (leader) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)   // 16 keys = 16 MN-major rows (2048 B)
+            umma_f16(dtm, desc_add(ad, k * 2048), desc_add(bd, k * 2048), idesc, (kb | k) != 0 ? 1u : 0u);
+          umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == DQS_STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (leader) umma_commit(&tfull[as]);
+      __syncwarp();
+    }
+  } else if (warp >= DQS_EPI0) {  // ===== epilogue: TMEM -> bf16 dQ (+ the qkv bias-gradient partials)
+    const int qd = warp & 3, half = (warp - DQS_EPI0) >> 2;
+    const uint32_t lrow = (uint32_t)(qd * 32) << 16;
+    int it = 0;
+    for (int t = blockIdx.x; t < n_items; t += gridDim.x, ++it) {
+      int qt, h, sq, nkb;
+      item(t, qt, h, sq, nkb);
+      const int as = it & 1;
+      mbar_wait(&tfull[as], (it >> 1) & 1);
+      fence_after();
+      const int q = qt * QB2 + qd * 32 + lane;
+      constexpr int OC = DH / 2;
+      __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + q) * 3 * d + h * DH + half * OC;
+      float* cs = a.colsum ? a.colsum + ((int64_t)(sq * nqt + qt) * 4 + qd) * 3 * d + h * DH + half * OC : nullptr;
+      store_row_bf16_global(out, tb + as * 128 + lrow + half * OC, OC, 1.f, q < s, cs);
+      fence_before();
+      mbar_arrive(&tempty[as]);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    tmem_dealloc(tb, 256);
+  }
+}
+
 template <int DH>
 static cudaError_t run(const AttnArgs& a, cudaStream_t st) {
   const int64_t rows = (int64_t)a.nseq * a.seq * a.heads;
@@ -727,6 +882,21 @@ static cudaError_t run(const AttnArgs& a, cudaStream_t st) {
   const int dkv_items = ((a.seq + KB - 1) / KB) * a.heads * a.nseq;
   note_launch(), dkdv_kernel<DH><<<std::min(dkv_items, num_sms()), NT, DkvSmem<DH>::TOTAL, st>>>(kv128, q64, g64, a);
   const int dq_items = ((a.seq + QB2 - 1) / QB2) * a.heads * a.nseq;
+  if (a.dsT) {   // dQ from the dS^T the dK/dV kernel stored (5-matmul backward)
+    static bool set2 = false;
+    if (!set2) {
+      if ((e = cudaFuncSetAttribute(dq_from_ds_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    DqsSmem<DH>::TOTAL)))
+        return e;
+      set2 = true;
+    }
+    const uint64_t s128 = (uint64_t)((a.seq + QB2 - 1) / QB2) * QB2;
+    CUtensorMap ds, k64;
+    if ((e = map2d_bf16(&ds, a.dsT, s128, s128 * a.heads * a.nseq, s128, 64, 64)) != cudaSuccess) return e;
+    if ((e = map3d_bf16(&k64, a.qkv, ld, a.seq, a.nseq, 64)) != cudaSuccess) return e;
+    note_launch(), dq_from_ds_kernel<DH><<<std::min(dq_items, num_sms()), DQS_NT, DqsSmem<DH>::TOTAL, st>>>(ds, k64, a);
+    return cudaGetLastError();
+  }
   note_launch(), dq_kernel<DH><<<std::min(dq_items, num_sms()), NT, DqSmem<DH>::TOTAL, st>>>(q128, g128, kv128, a);
   return cudaGetLastError();
 }

@@ -72,6 +72,9 @@ struct AttnArgs {
   // backward (tensor-core path): also the column sums of dqkv (the qkv bias gradient) per (sequence, 128-row
   // tile, 32-row quadrant): colsum[((sq * ceil(seq/128) + tile) * 4 + quadrant) * 3d + col], fp32
   float* colsum = nullptr;
+  // backward (tensor-core path): optional dS workspace [nseq][heads][s128][s128] bf16 (s128 = seq rounded up to
+  // 128): the dK/dV kernel stores dS^T there and dQ becomes a GEMM over it (5 matmuls per block instead of 7)
+  void* dsT = nullptr;
 };
 void attn_fwd_f32(const AttnArgs& a, cudaStream_t st);
 void attn_bwd_f32(const AttnArgs& a, cudaStream_t st);

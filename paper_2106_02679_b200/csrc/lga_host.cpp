@@ -266,6 +266,7 @@ struct lga_handle {
   void *dYe = nullptr, *dh1e = nullptr, *dO = nullptr, *dqkv = nullptr;
   float *dC = nullptr, *dh1 = nullptr, *dsum = nullptr, *partial = nullptr;
   float* splitk_ws = nullptr;   // split-K partial sums of tile-starved GEMMs (small-d weight gradients)
+  void* attn_ds = nullptr;      // dS^T of one chunk's attention backward (dQ from dS: 5 matmuls per block)
   int64_t splitk_floats = 0;
   double *mse_partial = nullptr, *loss_dev = nullptr, *loss_host = nullptr;
   float *xin = nullptr, *tin = nullptr;  // device copies for lga_step_host
@@ -403,6 +404,12 @@ static void plan_arena(lga_handle* h) {
   h->partial = A.take<float>(h->partial_floats);
   h->splitk_floats = c.bf16 ? std::min<int64_t>(16LL * 4 * d * d, (int64_t)1 << 25) : 0;
   h->splitk_ws = c.bf16 ? A.take<float>(h->splitk_floats) : nullptr;
+  {   // bf16: [c b][heads][s128][s128] bf16 (LGA_ATTN_BWD=7 keeps the 7-matmul dQ kernel, no workspace)
+    const char* v = getenv("LGA_ATTN_BWD");
+    const bool seven = v && v[0] == '7';
+    const int64_t s128 = (int64_t)(c.s + 127) / 128 * 128;
+    h->attn_ds = (c.bf16 && !seven) ? A.take_bytes((size_t)c.c * c.b * c.H * s128 * s128 * 2) : nullptr;
+  }
   h->mse_partial = A.take<double>(mse_blocks(act) + 64);
   h->loss_dev = A.take<double>(c.N + 8);
   h->xin = A.take<float>(act);
@@ -720,6 +727,7 @@ static void attn_bwd_and_bias(lga_handle* h, const Ws& w, int T, const GradDst& 
   a.scale = 1.0f / sqrtf((float)c.dh);
   a.qkv = w.qkv; a.o = w.o; a.lse = w.lse; a.dO = h->dO; a.dsum = h->dsum; a.dqkv = h->dqkv;
   a.colsum = c.bf16 ? h->partial : nullptr;
+  a.dsT = h->attn_ds;
   const int p = prof_begin(h, st);
   if (c.bf16) CK(attn_bwd_bf16(a, st)); else attn_bwd_f32(a, st);
   KCHECK();

@@ -73,10 +73,11 @@ extern "C" int lgatest_attn_fwd(int path, int nseq, int seq, int heads, int dh, 
 
 extern "C" int lgatest_attn_bwd(int path, int nseq, int seq, int heads, int dh, int causal, const void* qkv,
                                 const void* o, const float* lse, const void* dO, float* dsum, void* dqkv,
-                                float* colsum, uintptr_t stream) {
+                                float* colsum, void* ds_ws, uintptr_t stream) {
   AttnArgs a = mk(nseq, seq, heads, dh, causal);
   a.qkv = qkv; a.o = (void*)o; a.lse = (float*)lse; a.dO = dO; a.dsum = dsum; a.dqkv = dqkv;
   a.colsum = colsum;
+  a.dsT = ds_ws;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (path == 0) {
     attn_bwd_f32(a, st);

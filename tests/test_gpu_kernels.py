@@ -21,7 +21,7 @@ L.lgatest_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_i
 L.lgatest_attn_fwd.restype = C.c_int
 L.lgatest_attn_fwd.argtypes = [C.c_int] * 6 + [C.c_void_p] * 3 + [C.c_void_p]
 L.lgatest_attn_bwd.restype = C.c_int
-L.lgatest_attn_bwd.argtypes = [C.c_int] * 6 + [C.c_void_p] * 7 + [C.c_void_p]
+L.lgatest_attn_bwd.argtypes = [C.c_int] * 6 + [C.c_void_p] * 8 + [C.c_void_p]
 
 
 def P(t):
@@ -169,7 +169,7 @@ def _attn_ref(qkv, nseq, s, H, dh, causal):
                                                   (1, 128, 200, 1, 1), (1, 64, 300, 0, 1), (1, 128, 512, 0, 1),
                                                   (1, 64, 1024, 1, 1),
                                                   (1, 128, 1024, 1, 6), (1, 64, 700, 0, 6), (0, 32, 300, 1, 6)])
-def test_attention_fwd_bwd(path, dh, s, causal, mag, nseq=2, H=3):
+def test_attention_fwd_bwd(path, dh, s, causal, mag, nseq=2, H=3, ds_path=None):
     d = H * dh
     dt = torch.float32 if path == 0 else torch.bfloat16
     g = torch.Generator(device="cuda").manual_seed(3)
@@ -195,8 +195,11 @@ def test_attention_fwd_bwd(path, dh, s, causal, mag, nseq=2, H=3):
     dqkv = torch.full((nseq * s, 3 * d), float("nan"), device="cuda", dtype=dt)
     nt = (s + 127) // 128
     cs = torch.full((nseq * nt * 4, 3 * d), float("nan"), device="cuda") if path == 1 else None
+    ds = None
+    if path == 1 and ds_path != 7:   # the 5-matmul backward (dQ from the stored dS^T); 7: dQ recomputes S, dP
+        ds = torch.full((nseq * H * nt * 128 * nt * 128,), float("nan"), device="cuda", dtype=torch.bfloat16)
     assert L.lgatest_attn_bwd(path, nseq, s, H, dh, causal, P(qkv), P(o), P(lse), P(dO), P(dsum), P(dqkv), P(cs),
-                              stream()) == 0
+                              P(ds), stream()) == 0
     torch.cuda.synchronize()
     gq, gk, gv = torch.autograd.grad(ref, (q, k, v), dO.float().view(nseq, s, H, dh).permute(0, 2, 1, 3))
     pack = lambda t: t.permute(0, 2, 1, 3).reshape(nseq * s, d)
@@ -210,6 +213,12 @@ def test_attention_fwd_bwd(path, dh, s, causal, mag, nseq=2, H=3):
         assert relerr(cs[:, :d], full[:, :d]) < 2e-2 and relerr(cs[:, 2 * d:], full[:, 2 * d:]) < 2e-2
         # dL/db_K = sum over keys of dK is 0 (softmax shift invariance, pin P4): only rounding noise survives
         assert cs[:, d:2 * d].sum(0).norm() < 2e-2 * full[:, :d].sum(0).norm()
+
+
+@pytest.mark.parametrize("dh,s,causal", [(128, 256, 1), (64, 300, 0), (128, 200, 1)])
+def test_attention_bwd_seven_matmul_path(dh, s, causal):
+    """The dQ kernel that recomputes S and dP (no dS workspace) stays correct."""
+    test_attention_fwd_bwd(1, dh, s, causal, 1, ds_path=7)
 
 
 @pytest.mark.parametrize("dh,s,causal,mag", [(128, 512, 1, 1), (64, 512, 1, 6), (128, 384, 0, 1)])

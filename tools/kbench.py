@@ -23,7 +23,7 @@ L.lgatest_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_i
 L.lgatest_attn_fwd.restype = C.c_int
 L.lgatest_attn_fwd.argtypes = [C.c_int] * 6 + [C.c_void_p] * 3 + [C.c_void_p]
 L.lgatest_attn_bwd.restype = C.c_int
-L.lgatest_attn_bwd.argtypes = [C.c_int] * 6 + [C.c_void_p] * 7 + [C.c_void_p]
+L.lgatest_attn_bwd.argtypes = [C.c_int] * 6 + [C.c_void_p] * 8 + [C.c_void_p]
 
 
 def P(t):
@@ -58,8 +58,12 @@ def attn(args):
         ms = timeit(lambda: L.lgatest_attn_fwd(path, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), st))
         print(f"attn {name:14s} nseq={nseq} s={s} H={H} dh={dh}: {ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s")
     L.lgatest_attn_fwd(1, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), st)
-    ms = timeit(lambda: L.lgatest_attn_bwd(1, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), P(dO), P(dsum), P(dqkv), None, st))
-    print(f"attn {'bwd':14s} nseq={nseq} s={s} H={H} dh={dh}: {ms:.3f} ms  {2 * flops / ms / 1e9:.1f} TFLOP/s (algorithmic 2x fwd)")
+    s128 = (s + 127) // 128 * 128
+    ds = torch.empty(nseq * H * s128 * s128, device="cuda", dtype=torch.bfloat16)
+    for name, ws in (("bwd 5-mm", ds), ("bwd 7-mm", None)):
+        ms = timeit(lambda: L.lgatest_attn_bwd(1, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), P(dO), P(dsum), P(dqkv), None,
+                                               P(ws), st))
+        print(f"attn {name:14s} nseq={nseq} s={s} H={H} dh={dh}: {ms:.3f} ms  {2 * flops / ms / 1e9:.1f} TFLOP/s (algorithmic 2x fwd)")
 
 
 def gemm(args):
