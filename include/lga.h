@@ -263,7 +263,9 @@ lga_status lga_params(lga_handle* h, float* out, uint64_t n, int32_t out_on_devi
  * lga_save_state copies the state into `host_out` after the last step completed; lga_load_state restores it
  * into a handle of the same configuration and rank (INVALID_ARG otherwise), refreshes the 16-bit parameter
  * shard and sets t, so the next lga_step continues the run bit for bit (SIZE_MISMATCH if `bytes` differs).
- * Not collective; every rank saves / loads its own shard between the same two steps. */
+ * Every rank saves / loads its own shard between the same two steps.  lga_save_state is local;
+ * lga_load_state is collective for world > 1: it returns after every rank has restored its shard (the
+ * next step's all-gathers read peers' shards), LGA_ERR_CUDA if a peer does not arrive within 600 s. */
 lga_status lga_state_bytes(const lga_handle* h, uint64_t* bytes);
 lga_status lga_save_state(lga_handle* h, void* host_out, uint64_t bytes);
 lga_status lga_load_state(lga_handle* h, const void* host_in, uint64_t bytes);

@@ -2078,6 +2078,12 @@ lga_status lga_load_state(lga_handle* h, const void* host_in, uint64_t bytes) {
   CK(cudaMemcpyAsync(h->tstep, &t, sizeof(t), cudaMemcpyHostToDevice, h->s_comp));
   CK(cudaStreamSynchronize(h->s_comp));
   h->t = t;
+  // a peer's next step all-gathers this rank's parameter shard as soon as it starts: return only when every
+  // rank has restored its own (a fresh handle's flag epochs give its first gather nothing to wait for)
+  if (!world_sync(h, 600.0)) {
+    ERR(LGA_ERR_CUDA, "world barrier timed out (a peer did not call lga_load_state)");
+    throw StatusError{LGA_ERR_CUDA};
+  }
   return LGA_OK;
   ABI_CATCH
 }
