@@ -11,7 +11,10 @@
 // The result is the same definition (O3): o = sum_j P_j V_j / l, lse = m + log2(l) (natural log saved).
 // P never touches shared memory: the softmax thread writes it (bf16) into TMEM over the S columns it has
 // just read, and the PV MMA takes its A operand from TMEM.
-// Warp roles: 0 TMA (Q, K), 1 MMA issuer, 2 TMEM allocator, 3 TMA (V), 4..11 softmax + epilogue.
+// Warp roles: 0 TMA (Q, K), 1 MMA issuer, 2 TMEM allocator, 3 TMA (V), 4..11 softmax, 12..15 epilogue.
+// The epilogue warps take each finished item's O from TMEM (combining the two key halves), free the
+// accumulators for the next item's first PV and store O through a swizzled staging tile with TMA, while the
+// softmax warps already work on the next item (the per-item epilogue is off the softmax critical path).
 #include "kernels.cuh"
 #include "tc_common.cuh"
 
@@ -27,8 +30,10 @@ using namespace tcu;
 
 constexpr int BQ = 128, BKV = 128;
 constexpr int SM_WARPS = 8;                    // softmax warps: 2 per TMEM lane quadrant, 64 key columns each
-constexpr int NT = (4 + SM_WARPS) * 32;
+constexpr int EPI_WARPS = 4;                   // one per TMEM lane quadrant
+constexpr int NT = (4 + SM_WARPS + EPI_WARPS) * 32;
 constexpr int SM_THREADS = SM_WARPS * 32;
+constexpr int EPI_THREADS = EPI_WARPS * 32;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_THRESHOLD = 8.0f;   // log2 units
 #ifndef LGA_POLY_PAIRS
@@ -39,10 +44,20 @@ constexpr int POLY_PAIRS = LGA_POLY_PAIRS;  // of every 8 exponent pairs, comput
 #ifdef LGA_FWD_TRACE
 // Timing-only instrumentation (development builds): clock64() at pipeline events of CTA 0's first item.
 __device__ long long g_fwd_trace[40][8];
+__device__ long long g_fwd_items[64][4];   // CTA 0 per item: MMA item start, last PV issued, epilogue start / end
+__device__ long long g_fwd_cta[256][2];    // %globaltimer (ns) at each CTA's start and end
+__device__ __forceinline__ long long globaltimer_ns() {
+  long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
 #define FTR(j, k) \
   if (blockIdx.x == 0 && t == 0 && (j) < 40) g_fwd_trace[j][k] = clock64()
+#define FIT(i, k) \
+  if (blockIdx.x == 0 && (i) < 64) g_fwd_items[i][k] = clock64()
 #else
 #define FTR(j, k)
+#define FIT(i, k)
 #endif
 
 template <int DH>
@@ -53,14 +68,16 @@ struct FwdSmem {
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = Q_OFF + TILE;        // [NK]
   static constexpr int V_OFF = K_OFF + NK * TILE;   // [NV]
-  static constexpr int RED_OFF = V_OFF + NV * TILE; // [2 halves][128 rows] maxima, then [2][128] sums
-  static constexpr int BAR_OFF = RED_OFF + 4 * 128 * 4;
+  static constexpr int STG_OFF = V_OFF + NV * TILE; // O staging: [128 rows][64 cols] bf16, 128B-swizzled (TMA store)
+  static constexpr int RED_OFF = STG_OFF + SUB;     // [2 items][2 halves][128 rows] maxima, then [2][128] sums
+  static constexpr int BAR_OFF = RED_OFF + 2 * 4 * 128 * 4;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
   static_assert(TOTAL <= 232448, "shared memory");
 };
 
 template <int DH>
-__global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUtensorMap tm, const AttnArgs a) {
+__global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUtensorMap tm,
+                                                     const __grid_constant__ CUtensorMap tmo, const AttnArgs a) {
   using SM = FwdSmem<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps shared provenance
@@ -78,13 +95,18 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
                                        // issued before P(g) is awaited)
   uint64_t* o_done = p_full + 4;       // [2 halves]
   uint64_t* q_empty = o_done + 2;      // Q buffer free (all S MMAs of an item done)
-  uint64_t* o_free = q_empty + 1;      // O accumulators read by the epilogue (SM_THREADS arrivals)
+  uint64_t* o_free = q_empty + 1;      // O accumulators read by the epilogue (EPI_THREADS arrivals)
   uint64_t* p_free = o_free + 1;       // [2] per S / P TMEM buffer: PV of the tile in it done
-  constexpr int NBAR = 1 + 2 * NK + 2 * NV + 12;
+  uint64_t* ml_full = p_free + 2;      // [2 items] row maxima / sums of an item in red (SM_THREADS arrivals)
+  uint64_t* ml_empty = ml_full + 2;    // [2 items] red read by the epilogue (EPI_THREADS arrivals)
+  constexpr int NBAR = 1 + 2 * NK + 2 * NV + 16;
   static_assert(NBAR * 8 + 4 <= 256, "barrier area");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef LGA_FWD_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 256) g_fwd_cta[blockIdx.x][0] = globaltimer_ns();
+#endif
   const int s = a.seq, d = a.d;
   const int nqt = (s + BQ - 1) / BQ;
   const int per_q = a.heads * a.nseq;
@@ -107,7 +129,8 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < NBAR; ++i) {
       uint32_t cnt = 1;
-      if (&bars[i] == o_free) cnt = SM_THREADS;
+      if (&bars[i] == o_free || &bars[i] == ml_empty || &bars[i] == ml_empty + 1) cnt = EPI_THREADS;
+      if (&bars[i] == ml_full || &bars[i] == ml_full + 1) cnt = SM_THREADS;
       if (&bars[i] >= p_full && &bars[i] < p_full + 4) cnt = SM_THREADS / 2;
       mbar_init(&bars[i], cnt);   // softmax threads arrive individually
     }
@@ -173,13 +196,13 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
       int qt, h, sq, nkv;
       item(t, qt, h, sq, nkv);
       mbar_wait(q_full, it & 1);
+      if (lane == 0) FIT(it, 0);
       const int j0 = js;   // global index of this item's first tile
       for (int j = 0; j <= nkv; ++j) {
         if (j < nkv) {
           const int g = j0 + j, st = g % NK, b = g & 1;
           mbar_wait(&k_full[st], (g / NK) & 1);
           if (g >= 2) mbar_wait(&p_free[b], ((g - 2) >> 1) & 1);   // buffer b holds P(g-2) until PV(g-2) read it
-          FTR(j, 0);
           fence_after();
           const uint64_t dk = desc_add(dK, st * SM::TILE);
           if (leader) {
@@ -189,24 +212,23 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
               umma_f16(tbase + 128 * b, desc_add(dQ, off), desc_add(dk, off), idesc_s, kk > 0);
             }
             umma_commit(&s_full[b]);
-            umma_commit(&k_empty[st]);                // K tile consumed
-            if (j == nkv - 1) umma_commit(q_empty);   // Q no longer needed by this item
+            umma_commit(&k_empty[st]);
+            if (j == nkv - 1) umma_commit(q_empty);
           }
           __syncwarp();
         }
         if (j >= 1) {
           const int jj = j - 1, g = j0 + jj, st = g % NV, pb = g & 1;
-          if (jj == 0) mbar_wait(o_free, (it & 1) ^ 1);   // previous item's epilogue has read O
+          if (jj == 0) mbar_wait(o_free, (it & 1) ^ 1);
           mbar_wait(&v_full[st], (g / NV) & 1);
           const uint64_t dv = desc_add(dVm, st * SM::TILE);
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {   // O_h += P_h V_h over keys 64h .. 64h+63
+          for (int hh = 0; hh < 2; ++hh) {
             mbar_wait(&p_full[pb * 2 + hh], (g >> 1) & 1);
-            FTR(jj, 1 + hh);
             fence_after();
             if (leader) {
 #pragma unroll
-              for (int kk = 4 * hh; kk < 4 * hh + 4; ++kk)   // A = P_h from TMEM: 16 keys = 8 packed columns
+              for (int kk = 4 * hh; kk < 4 * hh + 4; ++kk)
                 umma_f16_ts(t_o[hh], tbase + 128 * pb + 64 * hh + 8 * (kk & 3), desc_add(dv, kk * 16 * 128), idesc_o,
                             (jj > 0 || kk > 4 * hh) ? 1u : 0u);
               umma_commit(&o_done[hh]);
@@ -216,13 +238,14 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
           if (leader) {
             umma_commit(&v_empty[st]);
             umma_commit(&p_free[pb]);
+            if (jj == nkv - 1) FIT(it, 1);
           }
           __syncwarp();
         }
       }
       js += nkv;
     }
-  } else if (warp >= 4) {  // ===== softmax + epilogue: one query row and one key half per thread
+  } else if (warp >= 4 && warp < 4 + SM_WARPS) {  // ===== softmax: one query row and one key half per thread
     const int qd = warp & 3;
     const int hf = (warp - 4) >> 2;            // key half of every tile this warp owns
     const int r = qd * 32 + lane;
@@ -230,7 +253,8 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
     const float sl2 = a.scale * LOG2E;
     float* red = reinterpret_cast<float*>(smem + SM::RED_OFF);
     int gt = 0;   // global tile counter
-    for (int t = blockIdx.x; t < n_items; t += gridDim.x) {
+    int its = 0;  // item counter
+    for (int t = blockIdx.x; t < n_items; t += gridDim.x, ++its) {
       int qt, h, sq, nkv;
       item(t, qt, h, sq, nkv);
       const int q0 = qt * BQ, q = q0 + r;
@@ -240,11 +264,23 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
         mbar_wait(&s_full[b], (gt >> 1) & 1);
         if (warp == 4 && lane == 0) FTR(j, 3);
         fence_after();
+        const int k0 = j * BKV + hf * 64;
+        if ((k0 >= s) || (a.causal && k0 > q0 + qd * 32 + 31)) {
+          // (warp-uniform) every key of this half is past the sequence end or after the warp's 32 queries --
+          // on the causal diagonal half of the warps: P = 0, max and sum unchanged
+          uint32_t z[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) z[c] = 0u;
+          tmem_st32_u(tbase + 128 * b + lane_off + hf * 64, z);
+          tmem_wait_st();
+          fence_before();
+          mbar_arrive(&p_full[b * 2 + hf]);
+          continue;
+        }
         uint32_t raw[2][32];
         tmem_ld32_nowait(tbase + 128 * b + lane_off + hf * 64, raw[0]);
         tmem_ld32_nowait(tbase + 128 * b + lane_off + hf * 64 + 32, raw[1]);
         tmem_wait_ld();
-        const int k0 = j * BKV + hf * 64;
         // masking only where a key can be past the sequence end or after the query (uniform per warp)
         const bool need_mask = (k0 + 64 > s) || (a.causal && k0 + 63 > q0 + qd * 32);
         float sv[64];
@@ -319,50 +355,89 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
         if (warp == 8 && lane == 0) FTR(j, 7);
         mbar_arrive(&p_full[b * 2 + hf]);
       }
-      // epilogue: combine the halves, o = (2^(m0-m) O_0 + 2^(m1-m) O_1) / (2^(m0-m) l_0 + 2^(m1-m) l_1)
-      // every PV of the item done: O final.  s_full(gt-1) only implies PV(gt-3), so o_done may be anywhere
-      // from PV(gt-3) to PV(gt-1) -- three states a parity wait cannot tell apart (a wait for (gt-1) would
-      // pass at once two completions short).  First PV(gt-2) through its buffer's p_free, which is either
-      // at PV(gt-4) or PV(gt-2) (PV(gt) needs this thread's o_free), then o_done is one phase from PV(gt-1).
+      // hand the row's (max, sum) of this half to the epilogue warps (double-buffered by item)
+      const int ib = its & 1;
+      mbar_wait(&ml_empty[ib], ((its >> 1) & 1) ^ 1);
+      red[ib * 512 + hf * 128 + r] = m_used;
+      red[ib * 512 + 256 + hf * 128 + r] = l;
+      mbar_arrive(&ml_full[ib]);
+    }
+  } else if (warp >= 4 + SM_WARPS) {  // ===== epilogue: o = (2^(m0-m) O_0 + 2^(m1-m) O_1) / (2^(m0-m) l_0 + 2^(m1-m) l_1), one row per thread
+    const int qd = warp & 3;
+    const int r = qd * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    const float* red = reinterpret_cast<const float*>(smem + SM::RED_OFF);
+    uint8_t* stg = smem + SM::STG_OFF;
+    const bool issuer = warp == 4 + SM_WARPS && lane == 0;
+    int gt = 0, it = 0;
+    for (int t = blockIdx.x; t < n_items; t += gridDim.x, ++it) {
+      int qt, h, sq, nkv;
+      item(t, qt, h, sq, nkv);
+      gt += nkv;
+      const int q0 = qt * BQ, q = q0 + r;
+      const int ib = it & 1;
+      mbar_wait(&ml_full[ib], (it >> 1) & 1);
+      if (issuer) FIT(it, 2);
+      const float m0 = red[ib * 512 + r], m1 = red[ib * 512 + 128 + r];
+      const float l0 = red[ib * 512 + 256 + r], l1 = red[ib * 512 + 384 + r];
+      mbar_arrive(&ml_empty[ib]);
+      // every PV of the item done: O final.  ml_full implies S(gt-1), issued after PV(gt-3) completed, so
+      // o_done may be anywhere from PV(gt-3) to PV(gt-1) -- three states a parity wait cannot tell apart.  First
+      // PV(gt-2) through its buffer's p_free (at PV(gt-4) or PV(gt-2); PV(gt) needs this item's o_free), then
+      // o_done is at most one phase from PV(gt-1).
       if (gt >= 2) mbar_wait(&p_free[gt & 1], ((gt - 2) >> 1) & 1);
       mbar_wait(&o_done[0], (gt - 1) & 1);
       mbar_wait(&o_done[1], (gt - 1) & 1);
       fence_after();
-      red[hf * 128 + r] = m_used;
-      red[256 + hf * 128 + r] = l;
-      asm volatile("bar.sync 1, %0;" ::"n"(SM_THREADS) : "memory");
-      const float m_o = red[(hf ^ 1) * 128 + r], l_o = red[256 + (hf ^ 1) * 128 + r];
-      asm volatile("bar.sync 1, %0;" ::"n"(SM_THREADS) : "memory");   // red reusable by the next item
-      const float m0 = hf == 0 ? m_used : m_o, m1 = hf == 0 ? m_o : m_used;
-      const float l0 = hf == 0 ? l : l_o, l1 = hf == 0 ? l_o : l;
       const float mm = fmaxf(m0, m1);
       const float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - mm), f1 = m1 == -INFINITY ? 0.f : ex2(m1 - mm);
       const float lt = f0 * l0 + f1 * l1;
       const float inv = lt > 0.f ? 1.f / lt : 0.f;
-      __nv_bfloat16* og = static_cast<__nv_bfloat16*>(a.o) + ((int64_t)sq * s + q) * d + h * DH;
-#pragma unroll 1
-      for (int c = hf * (DH / 64); c < (hf + 1) * (DH / 64); ++c) {   // this thread's half of the O columns
-        float t0[32], t1[32];
-        tmem_ld32(t_o[0] + lane_off + c * 32, t0);
-        tmem_ld32(t_o[1] + lane_off + c * 32, t1);
-        if (q < s) {
-          float tt[32];
+      const float g0 = f0 * inv, g1 = f1 * inv;
+      // O through the swizzled [128][64] staging tile, one 64-column half at a time (TMA clips rows past s);
+      // the accumulators are released after the last half's TMEM loads
 #pragma unroll
-          for (int i = 0; i < 32; ++i) tt[i] = (f0 * t0[i] + f1 * t1[i]) * inv;
-          uint4* dst = reinterpret_cast<uint4*>(og + c * 32);
+      for (int hh = 0; hh < DH / 64; ++hh) {
+        uint32_t pk[32];   // 64 columns of the row, bf16 pairs
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = make_uint4(pack_bf16x2(tt[8 * i], tt[8 * i + 1]), pack_bf16x2(tt[8 * i + 2], tt[8 * i + 3]),
-                                pack_bf16x2(tt[8 * i + 4], tt[8 * i + 5]), pack_bf16x2(tt[8 * i + 6], tt[8 * i + 7]));
+        for (int c = 0; c < 4; ++c) {
+          uint32_t u0[16], u1[16];
+          tmem_ld16_nowait(t_o[0] + lane_off + hh * 64 + c * 16, u0);
+          tmem_ld16_nowait(t_o[1] + lane_off + hh * 64 + c * 16, u1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            pk[c * 8 + i] = pack_bf16x2(g0 * __uint_as_float(u0[2 * i]) + g1 * __uint_as_float(u1[2 * i]),
+                                        g0 * __uint_as_float(u0[2 * i + 1]) + g1 * __uint_as_float(u1[2 * i + 1]));
+        }
+        if (hh == DH / 64 - 1) {
+          fence_before();
+          mbar_arrive(o_free);   // the next item's first PV may overwrite the accumulators
+        }
+        if (issuer) bulk_wait_read0();   // the previous store has read the staging tile
+        asm volatile("bar.sync 2, %0;" ::"n"(EPI_THREADS) : "memory");
+        uint8_t* row = stg + r * 128;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          *reinterpret_cast<uint4*>(row + ((k ^ (r & 7)) << 4)) =
+              make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+        fence_proxy_async();
+        asm volatile("bar.sync 2, %0;" ::"n"(EPI_THREADS) : "memory");
+        if (issuer) {
+          tma_store_3d(&tmo, stg, h * DH + 64 * hh, q0, sq);
+          bulk_commit();
         }
       }
-      if (q < s && hf == 0) a.lse[((int64_t)sq * a.heads + h) * s + q] = (mm + log2f(lt)) * 0.6931471805599453f;
-      fence_before();
-      mbar_arrive(o_free);
+      if (q < s) a.lse[((int64_t)sq * a.heads + h) * s + q] = (mm + log2f(lt)) * 0.6931471805599453f;
+      if (issuer) FIT(it, 3);
     }
+    if (issuer) bulk_wait0();
   }
   fence_before();
   __syncthreads();
+#ifdef LGA_FWD_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 256) g_fwd_cta[blockIdx.x][1] = globaltimer_ns();
+#endif
   if (warp == 2) {
     fence_after();
     tmem_dealloc(tbase, 512);
@@ -371,8 +446,10 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
 
 template <int DH>
 static cudaError_t run_fwd(const AttnArgs& a, cudaStream_t st) {
-  CUtensorMap tm;
+  CUtensorMap tm, tmo;
   cudaError_t e = map3d_bf16(&tm, a.qkv, 3ull * a.d, a.seq, a.nseq, 128);
+  if (e != cudaSuccess) return e;
+  e = map3d_bf16(&tmo, a.o, a.d, a.seq, a.nseq, 128);
   if (e != cudaSuccess) return e;
   static bool set = false;
   if (!set) {
@@ -381,7 +458,7 @@ static cudaError_t run_fwd(const AttnArgs& a, cudaStream_t st) {
     set = true;
   }
   const int items = ((a.seq + BQ - 1) / BQ) * a.heads * a.nseq;
-  note_launch(), fwd_kernel<DH><<<std::min(items, num_sms()), NT, FwdSmem<DH>::TOTAL, st>>>(tm, a);
+  note_launch(), fwd_kernel<DH><<<std::min(items, num_sms()), NT, FwdSmem<DH>::TOTAL, st>>>(tm, tmo, a);
   return cudaGetLastError();
 }
 
@@ -390,6 +467,11 @@ static cudaError_t run_fwd(const AttnArgs& a, cudaStream_t st) {
 #ifdef LGA_FWD_TRACE
 extern "C" int lgatest_fwd_trace(long long* out) {
   return (int)cudaMemcpyFromSymbol(out, fat::g_fwd_trace, sizeof(fat::g_fwd_trace));
+}
+extern "C" int lgatest_fwd_trace_items(long long* items, long long* cta) {
+  cudaError_t e = cudaMemcpyFromSymbol(items, fat::g_fwd_items, sizeof(fat::g_fwd_items));
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(cta, fat::g_fwd_cta, sizeof(fat::g_fwd_cta));
+  return (int)e;
 }
 #endif
 

@@ -31,3 +31,27 @@ for j in range(16):
     it = r[0] - prev if prev is not None else 0
     prev = r[0]
     print(f"{j:2d} {r[0]:9d} {r[1]:8d} {r[2]:8d} | {r[3]:10d} {r[4]:10d} {r[5]:10d} {r[6]:10d} {r[7]:10d} | {r[4] - r[3]:7d} {it:5d}")
+
+# per item of CTA 0 (MMA start, last PV issued, epilogue start / end) and the CTAs' start / end spread
+items = np.zeros((64, 4), dtype=np.int64)
+cta = np.zeros((256, 2), dtype=np.int64)
+L.lgatest_fwd_trace_items.argtypes = [C.c_void_p, C.c_void_p]
+assert L.lgatest_fwd_trace_items(items.ctypes.data, cta.ctypes.data) == 0
+n_items = (s // 128) * H * nseq
+per = [len(range(i, n_items, 148)) for i in range(1)][0]
+nqt = s // 128
+print("\nCTA 0 items: it  qt  tiles  mma_start  last_pv  epi_start  epi_end | span  cycles/tile  gap_to_next")
+G = 16
+for it in range(min(per, 64)):
+    t = it * 148
+    chunk, w = t // (G * nqt), t % (G * nqt)
+    np_ = min(G, H * nseq - chunk * G)
+    qt = nqt - 1 - w // np_
+    r = items[it] - items[0, 0]
+    nxt = items[it + 1, 0] - items[0, 0] if it + 1 < per else r[3]
+    span = r[3] - r[0]
+    print(f"  {it:3d} {qt:3d} {qt + 1:6d} {r[0]:10d} {r[1]:8d} {r[2]:9d} {r[3]:8d} | {span:6d} {span / (qt + 1):9.0f} {nxt - r[0]:9d}")
+g = cta[:148]
+t0 = g[:, 0].min()
+st, en = (g[:, 0] - t0) / 1e3, (g[:, 1] - t0) / 1e3
+print(f"\nCTA start spread {st.max():.1f} us; end min/median/max {en.min():.1f} / {np.median(en):.1f} / {en.max():.1f} us")
