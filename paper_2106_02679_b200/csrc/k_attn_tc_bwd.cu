@@ -90,14 +90,14 @@ __device__ __forceinline__ void store_row_bf16_global(__nv_bfloat16* dst, uint32
       if (lane < 16) csum[c + lane] = cs;
     }
     if (!valid) continue;
-    float t[16];
+    uint32_t pk[8];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) t[i] = __uint_as_float(r[i]) * scale;
-    uint4* p = reinterpret_cast<uint4*>(dst + c);
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-      p[i] = make_uint4(pack_bf16x2(t[8 * i], t[8 * i + 1]), pack_bf16x2(t[8 * i + 2], t[8 * i + 3]),
-                        pack_bf16x2(t[8 * i + 4], t[8 * i + 5]), pack_bf16x2(t[8 * i + 6], t[8 * i + 7]));
+    for (int i = 0; i < 8; ++i) pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]) * scale, __uint_as_float(r[2 * i + 1]) * scale);
+    // 16 columns = one full 32-byte sector per lane (rows are one per lane: a 16-byte store would cost the
+    // same number of L1 wavefronts for half the bytes); dst + c is 32-byte aligned
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + c), "r"(pk[0]), "r"(pk[1]),
+                 "r"(pk[2]), "r"(pk[3]), "r"(pk[4]), "r"(pk[5]), "r"(pk[6]), "r"(pk[7])
+                 : "memory");
   }
 }
 

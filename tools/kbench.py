@@ -60,9 +60,11 @@ def attn(args):
     L.lgatest_attn_fwd(1, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), st)
     s128 = (s + 127) // 128 * 128
     ds = torch.empty(nseq * H * s128 * s128, device="cuda", dtype=torch.bfloat16)
-    for name, ws in (("bwd 5-mm", ds), ("bwd 7-mm", None)):
-        ms = timeit(lambda: L.lgatest_attn_bwd(1, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), P(dO), P(dsum), P(dqkv), None,
-                                               P(ws), st))
+    # the step passes the qkv-bias column partials (one row per (sequence, key tile, lane quadrant))
+    cs = torch.empty(nseq * (s128 // 128) * 4 * 3 * d, device="cuda")
+    for name, ws, csum in (("bwd 5-mm", ds, cs), ("bwd 5-mm nocs", ds, None), ("bwd 7-mm", None, cs)):
+        ms = timeit(lambda: L.lgatest_attn_bwd(1, nseq, s, H, dh, 1, P(qkv), P(o), P(lse), P(dO), P(dsum), P(dqkv),
+                                               P(csum), P(ws), st))
         print(f"attn {name:14s} nseq={nseq} s={s} H={H} dh={dh}: {ms:.3f} ms  {2 * flops / ms / 1e9:.1f} TFLOP/s (algorithmic 2x fwd)")
 
 
