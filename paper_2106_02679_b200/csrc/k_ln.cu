@@ -402,23 +402,26 @@ int ln_bwd(const float* dout, const float* x, const float2* stats, const void* g
 }
 
 // =============================================================== fixed-order finisher
-// out[n] = (acc_in ? acc_in[n] : 0) + sum_k partial[k*pstride + n].  Block = 8 row groups x 32 columns;
-// row group g sums partial rows g, g+8, ... in order; the 8 group sums are added in order g = 0..7.
-__global__ void __launch_bounds__(256) colsum_finish_kernel(const float* __restrict__ partial, int nblk,
-                                                            int64_t pstride, int n, const float* acc_in, void* out,
-                                                            DT out_dt) {
-  __shared__ float red[8][33];
+// out[n] = (acc_in ? acc_in[n] : 0) + sum_k partial[k*pstride + n].  Block = FG row groups x 32 columns (each
+// warp reads one 128-byte row segment per step); row group g sums partial rows g, g+FG, ... in order, and the
+// FG group sums are added in order g = 0..FG-1.  FG = 32 keeps ~1k loads in flight per block: the finish is a
+// short pass over a few tens of MB, latency-bound at 8 groups.
+constexpr int FG = 32;
+__global__ void __launch_bounds__(32 * FG) colsum_finish_kernel(const float* __restrict__ partial, int nblk,
+                                                                int64_t pstride, int n, const float* acc_in, void* out,
+                                                                DT out_dt) {
+  __shared__ float red[FG][33];
   const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
   float s = 0.f;
   if (c < n)
-    for (int k = g; k < nblk; k += 8) s += partial[(int64_t)k * pstride + c];
+    for (int k = g; k < nblk; k += FG) s += partial[(int64_t)k * pstride + c];
   red[g][cl] = s;
   __syncthreads();
   if (g == 0 && c < n) {
     float t = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t += red[i][cl];
+    for (int i = 0; i < FG; ++i) t += red[i][cl];
     if (acc_in) t += acc_in[c];
     st_elem(out, c, out_dt, t);
   }
@@ -426,22 +429,22 @@ __global__ void __launch_bounds__(256) colsum_finish_kernel(const float* __restr
 
 // Several finishes over the same partial rows in ONE launch (blockIdx.y = output): the LayerNorm backward's
 // dgamma / dbeta (+ the two bias sums) -- same fixed order as colsum_finish_kernel, so the same bits.
-__global__ void __launch_bounds__(256) colsum_finish_multi_kernel(const float* __restrict__ partial, int nblk,
-                                                                  int64_t pstride, int n, FinishSet fs) {
-  __shared__ float red[8][33];
+__global__ void __launch_bounds__(32 * FG) colsum_finish_multi_kernel(const float* __restrict__ partial, int nblk,
+                                                                      int64_t pstride, int n, FinishSet fs) {
+  __shared__ float red[FG][33];
   const FinishOut& o = fs.o[blockIdx.y];
   const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
   const float* p = partial + o.col0;
   float s = 0.f;
   if (c < n)
-    for (int k = g; k < nblk; k += 8) s += p[(int64_t)k * pstride + c];
+    for (int k = g; k < nblk; k += FG) s += p[(int64_t)k * pstride + c];
   red[g][cl] = s;
   __syncthreads();
   if (g == 0 && c < n) {
     float t = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t += red[i][cl];
+    for (int i = 0; i < FG; ++i) t += red[i][cl];
     if (o.acc_in) t += o.acc_in[c];
     st_elem(o.out, c, o.out_dt, t);
   }
@@ -449,13 +452,13 @@ __global__ void __launch_bounds__(256) colsum_finish_multi_kernel(const float* _
 
 void colsum_finish_multi(const float* partial, int nblk, int64_t pstride, int n, const FinishSet& fs, cudaStream_t st) {
   if (n <= 0 || fs.k <= 0) return;
-  note_launch(), colsum_finish_multi_kernel<<<dim3((n + 31) / 32, fs.k), 256, 0, st>>>(partial, nblk, pstride, n, fs);
+  note_launch(), colsum_finish_multi_kernel<<<dim3((n + 31) / 32, fs.k), 32 * FG, 0, st>>>(partial, nblk, pstride, n, fs);
 }
 
 void colsum_finish(const float* partial, int nblk, int64_t pstride, int n, const float* acc_in, void* out, DT out_dt,
                    cudaStream_t st) {
   if (n <= 0) return;
-  note_launch(), colsum_finish_kernel<<<(n + 31) / 32, 256, 0, st>>>(partial, nblk, pstride, n, acc_in, out, out_dt);
+  note_launch(), colsum_finish_kernel<<<(n + 31) / 32, 32 * FG, 0, st>>>(partial, nblk, pstride, n, acc_in, out, out_dt);
 }
 
 }  // namespace lga
