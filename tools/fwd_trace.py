@@ -55,3 +55,15 @@ g = cta[:148]
 t0 = g[:, 0].min()
 st, en = (g[:, 0] - t0) / 1e3, (g[:, 1] - t0) / 1e3
 print(f"\nCTA start spread {st.max():.1f} us; end min/median/max {en.min():.1f} / {np.median(en):.1f} / {en.max():.1f} us")
+
+# item boundaries of CTA 0: when the MMA warp starts / ends waiting for the epilogue's o_free before the next
+# item's first PV, and when the epilogue saw the item's PVs done / released the accumulators
+if hasattr(L, "lgatest_fwd_trace_items2"):
+    it2 = np.zeros((64, 4), dtype=np.int64)
+    L.lgatest_fwd_trace_items2.argtypes = [C.c_void_p]
+    assert L.lgatest_fwd_trace_items2(it2.ctypes.data) == 0
+    print("\nit  o_free wait (MMA, next item)   epi: PV done  o_free arrive | MMA wait  epi PV->free")
+    for it in range(1, min(per, 64)):
+        a = it2[it] - items[0, 0]
+        e = it2[it - 1] - items[0, 0]
+        print(f"{it:3d} {a[0]:10d} {a[1]:10d} | {e[2]:10d} {e[3]:10d} | {a[1] - a[0]:8d} {e[3] - e[2]:8d}")
