@@ -24,7 +24,7 @@ __device__ __forceinline__ void epi_store(const Epi& e, int64_t m, int64_t n, fl
     st_elem(e.out, m * e.ldo + n, e.out_dt, v);
   } else if (e.kind == EPI_GELU_FWD) {
     const float u = v + ld_elem(e.bias, n, e.bias_dt);
-    st_elem(e.aux, m * e.ldaux + n, e.aux_dt, u);
+    if (e.aux) st_elem(e.aux, m * e.ldaux + n, e.aux_dt, u);   // aux == nullptr: the pre-activation is not kept
     st_elem(e.out, m * e.ldo + n, e.out_dt, gelu_f(u));
   } else {  // EPI_GELU_BWD
     const float u = ld_elem(e.aux, m * e.ldaux + n, e.aux_dt);

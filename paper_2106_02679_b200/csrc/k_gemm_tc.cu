@@ -95,7 +95,7 @@ __device__ __forceinline__ void epi_chunk_direct(const Epi& e, int64_t m, int64_
     if (e.res) vec = vec && aligned16(e.res + m * e.ldr + n0);
     if (e.acc_in) vec = vec && aligned16(e.acc_in + m * e.ldacc + n0);
   } else if (vec) {
-    vec = aligned16(static_cast<char*>(e.aux) + (m * e.ldaux + n0) * (int64_t)dt_size(e.aux_dt));
+    if (e.aux) vec = aligned16(static_cast<char*>(e.aux) + (m * e.ldaux + n0) * (int64_t)dt_size(e.aux_dt));
     if (e.kind == EPI_GELU_FWD) vec = vec && aligned16(static_cast<const char*>(e.bias) + n0 * (int64_t)dt_size(e.bias_dt));
   }
   if (!vec) {
@@ -118,7 +118,7 @@ __device__ __forceinline__ void epi_chunk_direct(const Epi& e, int64_t m, int64_
     load32(e.bias, e.bias_dt, n0, t);
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] += t[i];
-    store32(e.aux, e.aux_dt, m * e.ldaux + n0, v);
+    if (e.aux) store32(e.aux, e.aux_dt, m * e.ldaux + n0, v);
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
     store32(e.out, e.out_dt, m * e.ldo + n0, v);
@@ -341,7 +341,7 @@ __device__ __forceinline__ void epilogue_loop(const GemmArgs& g, const EpiMaps& 
         else for (int i = 0; i < 32; ++i) b[i] = n0 + i < g.N ? ld_elem(e.bias, n0 + i, e.bias_dt) : 0.f;
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] += b[i];
-        stage_write_row(sbuf, e.aux_dt, lane, v);              // u  -> first 2 KB
+        if (e.aux) stage_write_row(sbuf, e.aux_dt, lane, v);   // u  -> first 2 KB (unless not kept)
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = gelu_fast(v[i]);
         stage_write_row(sbuf + 2048, e.out_dt, lane, v);       // g  -> second 2 KB
@@ -357,7 +357,7 @@ __device__ __forceinline__ void epilogue_loop(const GemmArgs& g, const EpiMaps& 
       if (lane == 0) {
         const uint64_t pol = policy_evict_first();   // outputs stream out; keep L2 for the operands
         if (e.kind == EPI_GELU_FWD) {
-          tma_store_2d_hint(&em.aux, sbuf, n0, m0w, pol);
+          if (e.aux) tma_store_2d_hint(&em.aux, sbuf, n0, m0w, pol);
           tma_store_2d_hint(&em.out, sbuf + 2048, n0, m0w, pol);
         } else {
           tma_store_2d_hint(&em.out, sbuf, n0, m0w, pol);
@@ -696,8 +696,8 @@ static bool epi_maps(const GemmArgs& g, EpiMaps* em) {
   em->aux = em->out;
   em->in = em->out;
   if (e.kind == EPI_GELU_FWD) {
-    if (e.aux_dt != DT::BF16 || e.out_dt != DT::BF16) return false;
-    if (!box_map(&em->aux, e.aux, e.aux_dt, g.M, g.N, e.ldaux)) return false;
+    if (e.out_dt != DT::BF16 || (e.aux && e.aux_dt != DT::BF16)) return false;
+    if (e.aux && !box_map(&em->aux, e.aux, e.aux_dt, g.M, g.N, e.ldaux)) return false;
   } else if (e.kind == EPI_GELU_BWD) {
     if (!box_map(&em->in, e.aux, e.aux_dt, g.M, g.N, e.ldaux)) return false;
   } else if (e.res) {

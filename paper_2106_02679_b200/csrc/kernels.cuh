@@ -20,7 +20,7 @@ namespace lga {
 // wgrad    dW = X^T dY  : A(m,k) = X[k][m] (MN-major), B(n,k) = dY[k][n] (MN-major)
 enum EpiKind : int {
   EPI_STORE = 0,      // out = acc (+bias[n]) (+res[m][n]) (+acc_in[m][n])
-  EPI_GELU_FWD = 1,   // u = acc + bias[n] -> aux (E); out = GELU(u) (E)
+  EPI_GELU_FWD = 1,   // u = acc + bias[n] -> aux (E; not stored when aux == nullptr); out = GELU(u) (E)
   EPI_GELU_BWD = 2,   // out = acc * GELU'(aux[m][n])   (aux holds u; out may alias aux)
 };
 

@@ -592,13 +592,14 @@ static void layer_fwd(lga_handle* h, const Ws& w, const void* W, const float* x_
   }
   ln_fwd(w.h1, eoff((void*)W, E, c.o_ln2w), eoff((void*)W, E, c.o_ln2b), E, w.cn, E, w.st2, T, d, c.ln_eps, st);
   KCHECK();
-  {  // u = c W1 + b1 ; g = GELU(u)
+  {  // u = c W1 + b1 ; g = GELU(u).  u is read only by the backward's GELU': in the forward pass proper, when
+     // the backward recomputes the layer, it is not stored (T x 4d x E bytes of HBM writes per layer)
     GemmArgs g;
     g.M = T; g.N = c.f; g.K = d;
     g.A = w.cn; g.lda = d; g.a_kmajor = true;
     g.B = eoff((void*)W, E, c.o_w1); g.ldb = c.f; g.b_kmajor = false;
     g.epi.kind = EPI_GELU_FWD; g.epi.bias = eoff((void*)W, E, c.o_b1); g.epi.bias_dt = E;
-    g.epi.aux = w.u; g.epi.ldaux = c.f; g.epi.aux_dt = E;
+    g.epi.aux = (y_out && !c.norecomp) ? nullptr : w.u; g.epi.ldaux = c.f; g.epi.aux_dt = E;
     g.epi.out = w.g; g.epi.ldo = c.f; g.epi.out_dt = E;
     gemm(h, g, st);
     trace(h, "  ffn1 gemm", -1);
@@ -672,7 +673,7 @@ static void layer_fwd_post(lga_handle* h, const Ws& w, const void* W, const floa
     g.A = w.cn; g.lda = d; g.a_kmajor = true;
     g.B = eoff((void*)W, E, c.o_w1); g.ldb = c.f; g.b_kmajor = false;
     g.epi.kind = EPI_GELU_FWD; g.epi.bias = eoff((void*)W, E, c.o_b1); g.epi.bias_dt = E;
-    g.epi.aux = w.u; g.epi.ldaux = c.f; g.epi.aux_dt = E;
+    g.epi.aux = (y_out && !c.norecomp) ? nullptr : w.u; g.epi.ldaux = c.f; g.epi.aux_dt = E;
     g.epi.out = w.g; g.epi.ldo = c.f; g.epi.out_dt = E;
     gemm(h, g, st);
   }

@@ -72,7 +72,7 @@ def test_tc_gemm_store_f32(M, N, K, amaj, bmaj):
 
 
 @pytest.mark.parametrize("M,N,K", [(520, 384, 192), (2400, 8200, 128)])
-@pytest.mark.parametrize("kind", ["bias_bf16", "bias_res_acc", "gelu_fwd", "gelu_bwd"])
+@pytest.mark.parametrize("kind", ["bias_bf16", "bias_res_acc", "gelu_fwd", "gelu_fwd_no_u", "gelu_bwd"])
 def test_tc_gemm_epilogues(kind, M, N, K):
     g = torch.Generator(device="cuda").manual_seed(1)
     A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
@@ -98,6 +98,10 @@ def test_tc_gemm_epilogues(kind, M, N, K):
         uref = acc + bias.float()
         assert relerr(u.float(), uref) < 5e-3
         assert relerr(out.float(), torch.nn.functional.gelu(uref)) < 5e-3
+    elif kind == "gelu_fwd_no_u":   # forward pass under recompute: the pre-activation is not stored
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        gemm(1, A, True, B, False, M, N, K, out, kind=1, bias=bias, aux=None)
+        assert relerr(out.float(), torch.nn.functional.gelu(acc + bias.float())) < 5e-3
     else:
         u = (torch.randn(M, N, device="cuda", generator=g) * 2).bfloat16()
         out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)

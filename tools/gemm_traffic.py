@@ -24,9 +24,10 @@ def algorithmic_bytes(L, d, T, D, recompute=True):
     g_out = 4 if D == 1 else 2
     fwd = [T * d * b + d * 3 * d * b + T * 3 * d * b,                      # QKV (+ bias)
            T * d * b + d * d * b + T * d * f4 + T * d * f4,                # O-proj (+ residual, fp32 out)
-           T * d * b + d * f * b + 2 * T * f * b,                          # FFN1 (+ GELU: u and g out)
+           T * d * b + d * f * b + T * f * b * (1 if recompute else 2),    # FFN1 (+ GELU: g out; u only if kept)
            T * f * b + f * d * b + T * d * f4 + T * d * f4]                # FFN2 (+ residual, fp32 out)
-    rec = fwd[:3] if recompute else []
+    # the recompute's FFN1 writes u (read by the GELU backward) and g
+    rec = fwd[:2] + [T * d * b + d * f * b + 2 * T * f * b] if recompute else []
     bwd = [T * f * b + T * d * b + f * d * g_out,                         # FFN2 wgrad
            T * d * b + f * d * b + T * f * b + T * f * b,                  # FFN2 dgrad (+ GELU' reads u, writes dU)
            T * d * b + T * f * b + d * f * g_out,                          # FFN1 wgrad

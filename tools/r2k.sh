@@ -1,7 +1,7 @@
 # kernel + step parity tests, default bench, launch list of one C3 step (durations + DRAM bytes)
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_hbm_kernels.py tests/test_gpu_step.py -q -p no:cacheprovider 2>&1 | tail -2
+timeout 1200 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_hbm_kernels.py tests/test_gpu_step.py tests/test_gpu_post_ln.py tests/test_gpu_guard.py -q -p no:cacheprovider 2>&1 | tail -2
 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r2k_bench.json 2> gpurun_out/r2k_bench.err || exit 1
 python - <<'PY'
 import json
