@@ -403,8 +403,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     kb0 = ks * nkper;
     kb1 = min(nk_all, kb0 + nkper);
   };
-  // tile raster: groups of GM m-blocks sweep all n-blocks (L2 reuse of B).  (Groups sized to one wave of tiles,
-  // GM = grid / num_n, cut the FFN1 A over-fetch but raised FFN2's and the step time: measured, reverted.)
+  // tile raster (tile_coords): n fastest when the grid has at least as many m-blocks as n-blocks, else groups of
+  // GM m-blocks sweep all n-blocks.  (Groups sized to one wave of tiles, GM = grid / num_n, cut the FFN1 A
+  // over-fetch but raised FFN2's and the step time: measured, reverted.)
   constexpr int GM = 8;
 
   if (warp == 0 && lane == 0) {
@@ -422,6 +423,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   auto tile_coords = [&](int t, int& mb, int& nb) {
+    // the concurrently running tiles (one wave) share operand panels in L2; the panels a wave leaves half-read
+    // are read again from HBM by the next wave.  Walking n fastest re-reads B panels, walking m fastest (in
+    // groups of GM m-blocks) re-reads A panels: re-read the smaller operand (fewer blocks along its side).
+    if (num_m >= num_n) {
+      mb = t / num_n, nb = t % num_n;
+      return;
+    }
     const int per_group = GM * num_n;
     const int grp = t / per_group;
     const int first_m = grp * GM;
@@ -574,6 +582,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   auto tile_coords = [&](int t, int& mb, int& nb) {
+    // the concurrently running tiles (one wave) share operand panels in L2; the panels a wave leaves half-read
+    // are read again from HBM by the next wave.  Walking n fastest re-reads B panels, walking m fastest (in
+    // groups of GM m-blocks) re-reads A panels: re-read the smaller operand (fewer blocks along its side).
+    if (num_m >= num_n) {
+      mb = t / num_n, nb = t % num_n;
+      return;
+    }
     const int per_group = GM * num_n;
     const int grp = t / per_group;
     const int first_m = grp * GM;
