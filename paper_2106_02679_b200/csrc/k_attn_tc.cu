@@ -115,7 +115,10 @@ __global__ void __launch_bounds__(NT, 1) fwd_kernel(const __grid_constant__ CUte
   // work item t -> (query tile, head, sequence).  Items come in chunks of G (sequence, head) pairs, all
   // query tiles of a chunk together (heaviest first under causal masking), so the CTAs running at any time
   // share each pair's K / V tiles in L2 instead of streaming every tile from HBM once per query tile.
-  constexpr int G = 16;
+#ifndef LGA_FWD_G
+#define LGA_FWD_G 16
+#endif
+  constexpr int G = LGA_FWD_G;
   auto item = [&](int t, int& qt, int& h, int& sq, int& nkv) {
     const int chunk = t / (G * nqt), w = t % (G * nqt);
     const int np = min(G, per_q - chunk * G);   // pairs in this chunk (the last may be partial)

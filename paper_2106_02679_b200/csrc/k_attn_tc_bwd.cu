@@ -171,7 +171,10 @@ struct DkvSmem {
 // K / V tiles are loaded as soon as the current item's last S^T / dP^T MMAs have read them (kv_empty), and
 // its first S^T / dP^T MMAs run while the element-wise warps drain the previous item's dK / dV from TMEM;
 // only its first dV / dK MMAs wait for that drain (acc_free).
-constexpr int DKV_G = 8;
+#ifndef LGA_DKV_G
+#define LGA_DKV_G 8
+#endif
+constexpr int DKV_G = LGA_DKV_G;
 
 template <int DH>
 __global__ void __launch_bounds__(NT, 1)
