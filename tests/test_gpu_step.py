@@ -105,10 +105,13 @@ def test_bf16_layered_parity(sh, chunk):
 # micro-batches, as bench.py times it) with L and N small enough for the fp64 oracle (seconds).
 FULL = [synth.Shape(layers=2, d=2048, heads=16, seq=2048, micro_batch=1, n_micro=2),     # 1.3B layer (C3)
         synth.Shape(layers=1, d=768, heads=12, seq=1024, micro_batch=4, n_micro=2),       # GPT-2-small layer (C2)
-        synth.Shape(layers=1, d=4096, heads=32, seq=2048, micro_batch=1, n_micro=2)]      # ~10B layer (C4)
+        synth.Shape(layers=1, d=4096, heads=32, seq=2048, micro_batch=1, n_micro=2),      # ~10B layer (C4)
+        # C3 layer with 4 micro-batches in one launch: M = 8192 rows, so every GEMM of the layer takes the
+        # n-fastest raster the bench's M = 32768 launches take (as many m-blocks as n-blocks or more)
+        synth.Shape(layers=1, d=2048, heads=16, seq=2048, micro_batch=1, n_micro=4)]
 
 
-@pytest.mark.parametrize("sh", FULL, ids=["c3_layer", "c2_layer", "c4_layer"])
+@pytest.mark.parametrize("sh", FULL, ids=["c3_layer", "c2_layer", "c4_layer", "c3_layer_n4"])
 def test_bf16_full_width_parity(sh):
     out, (rp, rl, rg, init) = _run(sh, precision=LGA_BF16, style="train")
     per = per_layer_rel(out["grads"], rg, sh.layers)
