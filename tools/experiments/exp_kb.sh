@@ -1,4 +1,4 @@
-# A/B of builds (exp/<v>.so) on one kbench section: bash tools/exp_kb.sh <attn|gemm|ln> v1 v2 ...
+# A/B of builds (exp/<v>.so) on one kbench section: bash tools/experiments/exp_kb.sh <attn|gemm|ln> v1 v2 ...
 cd $GRAFT_REPO_ROOT
 what=$1; shift
 cp paper_2106_02679_b200/liblga.so /tmp/rel.so
