@@ -115,6 +115,20 @@ __device__ long long g_dq_trace[40][8];
 #define BTR(i, k)
 #define QTR(j, k)
 #endif
+#ifdef LGA_DKV_TRACE
+// Timing-only instrumentation (development builds): clock64() per global iteration g < 96 of CTA 0 of the
+// persistent dK/dV kernel: [g][0] S^T issued, [1] dP^T issued, [2] element-wise group saw s_full, [3] P / dS
+// arrived, [4] dV issued, [5] dK issued; per item [it][0] drain start, [1] drain end, [2] MMA item start.
+__device__ long long g_dkv_trace[96][8];
+__device__ long long g_dkv_items[32][4];
+#define DTR(g, k) \
+  if (blockIdx.x == 0 && (g) < 96) g_dkv_trace[g][k] = clock64()
+#define DIT(i, k) \
+  if (blockIdx.x == 0 && (i) < 32) g_dkv_items[i][k] = clock64()
+#else
+#define DTR(g, k)
+#define DIT(i, k)
+#endif
 
 // 4-byte cp.async global -> shared (zero-filled when !valid) and its completion arriving on an mbarrier
 // (.noinc: the barrier's expected count includes one arrival per issuing thread)
@@ -307,6 +321,7 @@ __global__ void __launch_bounds__(NT, 1)
             const uint32_t oa = (kk >> 2) * SM::SUB128 + (kk & 3) * 32, ob = (kk >> 2) * SM::SUB64 + (kk & 3) * 32;
             umma_f16(t_st(b), desc_add(dK, oa), desc_add(dq, ob), idesc_s, kk > 0);
           }
+          DTR(g, 0);
         }
         __syncwarp();
         if (g >= 2) mbar_wait(&g_done[b], ((g - 2) >> 1) & 1);
@@ -318,11 +333,13 @@ __global__ void __launch_bounds__(NT, 1)
             umma_f16(t_dpt(b), desc_add(dV, oa), desc_add(dg, ob), idesc_s, kk > 0);
           }
           umma_commit(&s_full[b]);
+          DTR(g, 1);
           if (i == nq - 1) umma_commit(kv_empty);   // K / V of this item fully read
         }
         __syncwarp();
       };
       mbar_wait(kv_full, it & 1);
+      if (lane == 0) DIT(it, 2);
       issue_s(gi, 0);
       if (nq > 1) issue_s(gi + 1, 1);
       for (int i = 0; i < nq; ++i) {  // dV += P^T dO, dK += dS^T Q (A from TMEM), then S^T(i+2)
@@ -339,6 +356,7 @@ __global__ void __launch_bounds__(NT, 1)
             umma_f16_ts(t_dv, t_st(b) + ta, desc_add(dg, ob), idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&dv_done[b]);
+          DTR(g, 4);
 #pragma unroll
           for (int kk = 0; kk < QB / 16; ++kk) {
             const uint32_t ta = 32 * (kk >> 1) + 8 * (kk & 1);
@@ -346,6 +364,7 @@ __global__ void __launch_bounds__(NT, 1)
             umma_f16_ts(t_dk, t_dpt(b) + ta, desc_add(dq, ob), idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&g_done[b]);
+          DTR(g, 5);
           umma_commit(&q_empty[st]);
         }
         __syncwarp();
@@ -378,6 +397,7 @@ __global__ void __launch_bounds__(NT, 1)
         __nv_bfloat16* dst_row =
             a.dsT ? static_cast<__nv_bfloat16*>(a.dsT) + (((int64_t)sq * a.heads + h) * s128 + kj) * s128 : nullptr;
         mbar_wait(&s_full[grp], (g >> 1) & 1);
+        if ((warp & 7) == 4 && lane == 0) DTR(g, 2);
         fence_after();
         mbar_wait(&q_full[st], (g / NST) & 1);   // lse / dsum of tile g landed with Q / dO
 #pragma unroll
@@ -424,6 +444,7 @@ __global__ void __launch_bounds__(NT, 1)
         tmem_wait_st();
         fence_before();
         mbar_arrive(&p_full[grp]);
+        if ((warp & 7) == 4 && lane == 0) DTR(g, 3);
       }
       // every gradient MMA of this item done: this group's last one (its own barrier: cannot alias an older
       // phase), then the item's very last one (the next phase of that barrier needs this thread's acc_free)
@@ -434,6 +455,7 @@ __global__ void __launch_bounds__(NT, 1)
         if (own != gl) mbar_wait(&g_done[gl & 1], (gl >> 1) & 1);
         fence_after();
       }
+      if (warp == 4 && lane == 0) DIT(t / (int)gridDim.x, 0);
       constexpr int OC = DH / 4;   // output columns per (group, half)
       const int oq = grp * 2 + hf;
       __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + kj) * 3 * d + h * DH + oq * OC;
@@ -442,6 +464,7 @@ __global__ void __launch_bounds__(NT, 1)
       store_row_bf16_global(out + 2 * d, t_dv + lrow + oq * OC, OC, 1.f, kj < s, cs ? cs + 2 * d : nullptr);
       fence_before();
       mbar_arrive(acc_free);   // dK / dV accumulators free for the next item
+      if (warp == 4 && lane == 0) DIT(t / (int)gridDim.x, 1);
       gi += nq;
     }
   }
@@ -912,6 +935,13 @@ extern "C" int lgatest_bwd_trace(long long* out) {
 }
 extern "C" int lgatest_dq_trace(long long* out) {
   return (int)cudaMemcpyFromSymbol(out, fatb::g_dq_trace, sizeof(fatb::g_dq_trace));
+}
+#endif
+#ifdef LGA_DKV_TRACE
+extern "C" int lgatest_dkv_trace(long long* iters, long long* items) {
+  cudaError_t e = cudaMemcpyFromSymbol(iters, fatb::g_dkv_trace, sizeof(fatb::g_dkv_trace));
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(items, fatb::g_dkv_items, sizeof(fatb::g_dkv_items));
+  return (int)e;
 }
 #endif
 
