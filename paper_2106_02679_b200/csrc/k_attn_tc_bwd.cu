@@ -460,10 +460,46 @@ __global__ void __launch_bounds__(NT, 1)
       const int oq = grp * 2 + hf;
       __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.dqkv) + ((int64_t)sq * s + kj) * 3 * d + h * DH + oq * OC;
       float* cs = a.colsum ? a.colsum + ((int64_t)(sq * nkt + kt) * 4 + qd) * 3 * d + h * DH + oq * OC : nullptr;
-      store_row_bf16_global(out + d, t_dk + lrow + oq * OC, OC, 1.f, kj < s, cs ? cs + d : nullptr);
-      store_row_bf16_global(out + 2 * d, t_dv + lrow + oq * OC, OC, 1.f, kj < s, cs ? cs + 2 * d : nullptr);
+      // all TMEM loads first, then release the accumulators (the next item's first dV / dK MMAs run while
+      // this row is stored); the key-bias gradient is identically zero (softmax shift invariance, pin P4):
+      // its partials are written as zeros instead of summed
+      constexpr int NC = OC / 16;
+      uint32_t rk[NC][16], rv[NC][16];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        tmem_ld16_nowait(t_dk + lrow + oq * OC + 16 * c, rk[c]);
+        tmem_ld16_nowait(t_dv + lrow + oq * OC + 16 * c, rv[c]);
+      }
+      tmem_wait_ld();
       fence_before();
       mbar_arrive(acc_free);   // dK / dV accumulators free for the next item
+      const bool valid = kj < s;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        if (cs) {
+          float w[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) w[i] = valid ? __uint_as_float(rv[c][i]) : 0.f;
+          const float sum = warp_colsum16(w);
+          if (lane < 16) {
+            cs[d + 16 * c + lane] = 0.f;
+            cs[2 * d + 16 * c + lane] = sum;
+          }
+        }
+        if (!valid) continue;
+        uint32_t pk[8], pv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          pk[i] = pack_bf16x2(__uint_as_float(rk[c][2 * i]), __uint_as_float(rk[c][2 * i + 1]));
+          pv[i] = pack_bf16x2(__uint_as_float(rv[c][2 * i]), __uint_as_float(rv[c][2 * i + 1]));
+        }
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(out + d + 16 * c), "r"(pk[0]),
+                     "r"(pk[1]), "r"(pk[2]), "r"(pk[3]), "r"(pk[4]), "r"(pk[5]), "r"(pk[6]), "r"(pk[7])
+                     : "memory");
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(out + 2 * d + 16 * c), "r"(pv[0]),
+                     "r"(pv[1]), "r"(pv[2]), "r"(pv[3]), "r"(pv[4]), "r"(pv[5]), "r"(pv[6]), "r"(pv[7])
+                     : "memory");
+      }
       if (warp == 4 && lane == 0) DIT(t / (int)gridDim.x, 1);
       gi += nq;
     }
