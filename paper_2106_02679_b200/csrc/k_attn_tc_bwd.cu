@@ -44,10 +44,10 @@ constexpr float LOG2E = 1.4426950408889634f;
 // 1.111 ms -- the backward's element-wise phase is not SFU-bound, so the default keeps every 2^x on the SFU
 constexpr int BWD_POLY = LGA_BWD_POLY;
 
-// rowsum(dO * o) per (sequence, head, position): d_h / 8 lanes per row (8 or 16, 16-byte loads), shuffle
-// reduction within the lane group
+// rowsum(dO * o) per (sequence, head, position): d_h / 16 lanes per row, 32 bytes of o and of dO per lane (two
+// 16-byte loads each, all four issued before the math), shuffle reduction within the lane group
 __global__ void __launch_bounds__(256) dsum_kernel(AttnArgs a) {
-  const int lph = a.dh >> 3;
+  const int lph = a.dh >> 4;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t row = gid / lph;   // token * heads + h
   const int part = (int)(gid % lph);
@@ -58,12 +58,14 @@ __global__ void __launch_bounds__(256) dsum_kernel(AttnArgs a) {
   if (valid) {
     h = (int)(row % a.heads);
     tok = row / a.heads;
-    const int64_t off = tok * a.d + (int64_t)h * a.dh + part * 8;
-    const uint4 x = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.o) + off);
-    const uint4 y = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.dO) + off);
-    const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+    const int64_t off = tok * a.d + (int64_t)h * a.dh + part * 16;
+    const uint4* po = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.o) + off);
+    const uint4* pg = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.dO) + off);
+    const uint4 x0 = po[0], x1 = po[1], y0 = pg[0], y1 = pg[1];
+    const uint32_t xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+    const uint32_t ys[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 8; ++i) {
       acc = fmaf(__uint_as_float(xs[i] << 16), __uint_as_float(ys[i] << 16), acc);
       acc = fmaf(__uint_as_float(xs[i] & 0xFFFF0000u), __uint_as_float(ys[i] & 0xFFFF0000u), acc);
     }
@@ -923,7 +925,7 @@ __global__ void __launch_bounds__(DQS_NT, 1)
 template <int DH>
 static cudaError_t run(const AttnArgs& a, cudaStream_t st) {
   const int64_t rows = (int64_t)a.nseq * a.seq * a.heads;
-  note_launch(), dsum_kernel<<<(unsigned)((rows * (a.dh / 8) + 255) / 256), 256, 0, st>>>(a);
+  note_launch(), dsum_kernel<<<(unsigned)((rows * (a.dh / 16) + 255) / 256), 256, 0, st>>>(a);
   CUtensorMap kv128, q64, g64, q128, g128;
   cudaError_t e;
   const uint64_t ld = 3ull * a.d;
