@@ -7,7 +7,9 @@
 //     P^T = exp(S^T*scale - lse), dS^T = P^T (dP^T - dsum) * scale   (element-wise warps, bf16 into TMEM)
 //     dV += P^T dO, dK += dS^T Q              (tcgen05, A = P^T / dS^T from TMEM, B = dO / Q read MN-major
 //                                              from the very tiles TMA loaded K-major for the first two MMAs)
-//   dQ kernel, one CTA per 128-query tile, looping over 64-key tiles:
+//     with a dS workspace (a.dsT) the element-wise warps also store dS^T (bf16, 32-byte sectors), and
+//   dQ = dS K is a persistent, causally blocked batched GEMM over it (dq_from_ds_kernel; 5 matmuls per block);
+//   without one, the dQ kernel (one CTA per 128-query tile, looping over 128-key tiles) recomputes
 //     S = Q K^T, dP = dO V^T ; dS = P (dP - dsum) * scale ; dQ += dS K   (dS from TMEM, K read MN-major)
 // P / dS never touch shared memory, which goes to deeper Q/dO (K/V) rings: the load latency, not the
 // tensor pipe, bounded the smem-staged version (MMA issuer stalled on the ring's full barrier).
