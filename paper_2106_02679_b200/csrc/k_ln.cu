@@ -256,6 +256,11 @@ __global__ void __launch_bounds__(NW * 32, LGA_LNF_MINB) ln_bwd_fused(const floa
         go[rr][k] = a.x, go[rr][k + 1] = a.y, go[rr][k + 2] = a.z, go[rr][k + 3] = a.w;
         xc[rr][k] = b.x, xc[rr][k + 1] = b.y, xc[rr][k + 2] = b.z, xc[rr][k + 3] = b.w;
       }
+#ifndef LGA_LN_NO_PREFETCH
+      // the residual row is read only after the cross-warp row sums: start its DRAM fetch now (into L2;
+      // registers are full at 3 blocks per SM)
+      if (resid) asm volatile("prefetch.global.L2 [%0];" ::"l"(resid + base));
+#endif
     }
 #pragma unroll
     for (int rr = 0; rr < LNF_ROWS; ++rr) {
