@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(256) ln_bwd_block(const float* __restrict__ do
 // dx, and accumulates dgamma / dbeta for its columns in registers -- one partial per block (fixed grid,
 // fixed row order: bitwise reproducible).
 // rows held in registers per group and resident blocks per SM (measured at the 1.3B shape, d = 2048, fused
-// backward with the 4 column sums: 4 rows x 2 blocks 0.232 ms, 2 x 3 0.223 ms (5.41 TB/s), 2 x 4 and 3 x 3 spill)
+// backward with the 4 column sums: 4 rows x 2 blocks 0.232 ms, 2 x 3 0.223 ms (5.41 TB/s), 2 x 4 and 3 x 3 spill;
+// 2 x 3 with the L2 prefetch of the residual row: 0.202 ms, 5.98 TB/s)
 #ifndef LGA_LNF_ROWS
 #define LGA_LNF_ROWS 2
 #endif
