@@ -534,7 +534,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // than the single-CTA 128 x 256 tile at the same MMA rate.  Each CTA drains its own TMEM (epilogue_loop).
 constexpr int PAIR_N = 256;
 struct Smem2 {
-  static constexpr int STAGES = 5;
+#ifndef LGA_GEMM2_STAGES
+#define LGA_GEMM2_STAGES 5
+#endif
+  static constexpr int STAGES = LGA_GEMM2_STAGES;
   static constexpr int A_BYTES = BM * BK * 2;            // this CTA's 128 rows of A
   static constexpr int B_BYTES = (PAIR_N / 2) * BK * 2;  // this CTA's 128 columns of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
