@@ -190,7 +190,7 @@ struct DkvSmem {
 // its first S^T / dP^T MMAs run while the element-wise warps drain the previous item's dK / dV from TMEM;
 // only its first dV / dK MMAs wait for that drain (acc_free).
 #ifndef LGA_DKV_G
-#define LGA_DKV_G 8
+#define LGA_DKV_G 4
 #endif
 constexpr int DKV_G = LGA_DKV_G;
 
