@@ -544,7 +544,10 @@ struct DqSmem {
 // pairs (their K / V tiles stay in L2), heaviest query tiles first; K / V rings, the S / dP buffer and the dS
 // buffers run on global counters; the next item's Q / dO tiles load once the current item's last S / dP MMAs
 // have read them (qg_empty), and only its first dQ MMA waits for the previous dQ drain (acc_free).
-constexpr int DQ_G = 16;
+#ifndef LGA_DQ_G
+#define LGA_DQ_G 16
+#endif
+constexpr int DQ_G = LGA_DQ_G;
 
 template <int DH>
 __global__ void __launch_bounds__(NT, 1)
