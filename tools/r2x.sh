@@ -1,0 +1,4 @@
+# dS^T through a staged TMA store in the dK/dV kernel: kernel tests, kbench A/B
+cd $GRAFT_REPO_ROOT
+timeout 600 python -m pytest tests/test_gpu_kernels.py -q -x -k "attn or attention" -p no:cacheprovider 2>&1 | tail -2
+bash tools/experiments/ab_kb.sh prev cur
